@@ -1,0 +1,169 @@
+/* gpulet.h — C-ABI of libgpulet, the B200-native gpu-let serving hot path.
+ *
+ * Method: arXiv 2109.01611 ("Multi-model Machine Learning Inference Serving with
+ * GPU Spatial Partitioning", PAPER.md).  A gpu-let is a fraction of one GPU's
+ * compute (§2.3; "up-to two virtual gpu-lets" per GPU); the
+ * serving system batches requests per model and dispatches them to the gpu-let a
+ * scheduler assigned (§5); the scheduler is Alg. 1 "ElasticPartitioning"
+ * with the linear L2/DRAM interference model (§4.4, eq. at).
+ *
+ * Conventions
+ *  - Plain C: no C++ or torch types cross this boundary.  All functions return a
+ *    gl_status (0 = GL_OK, negative = error); gl_last_error() gives thread-local
+ *    text for the last failure.
+ *  - "device pointer" = a CUDA device address on the named GPU; "host pointer" =
+ *    ordinary process memory.  The caller owns every pointer it passes; the
+ *    library owns weights, workspaces, rings and everything behind gl_ctx.
+ *  - Any CUDA error poisons the context (GL_E_CUDA on every later call).
+ */
+#ifndef GPULET_H
+#define GPULET_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gl_ctx gl_ctx;
+typedef int32_t gl_status;
+
+enum {
+  GL_OK = 0,
+  GL_E_ARG = -1,            /* null pointer or bad enum */
+  GL_E_GRID = -2,           /* sm_pct not in {20,40,50,60,80,100} */
+  GL_E_CAPACITY = -3,       /* batch outside [1,32] */
+  GL_E_PARTITION = -4,      /* sizes on one GPU sum > 100, or a third gpu-let */
+  GL_E_STATE = -5,          /* submit to a destroyed gpu-let; model loaded after the gpu-let; misuse */
+  GL_E_MODEL = -6,          /* model not loaded on that GPU */
+  GL_E_QUEUE_FULL = -7,     /* ring full; poll and retry */
+  GL_E_NOT_CONCURRENT = -8, /* executor CTAs did not all become resident (green-ctx caveat) */
+  GL_E_PARSE = -9,          /* malformed weight file / input */
+  GL_E_DATA = -10,          /* profile data violates monotonicity before the envelope */
+  GL_E_BUDGET = -11,        /* ideal enumerator too large */
+  GL_E_CUDA = -12,          /* CUDA driver/runtime error */
+  GL_E_TIMEOUT = -13        /* a blocking helper exceeded its deadline */
+};
+
+/* Model kinds: the paper's five (Table tab:ml-models) + BERT-base (north_star). */
+enum { GL_LENET5 = 0, GL_GOOGLENET = 1, GL_RESNET50 = 2, GL_SSD_MOBILENET_V1 = 3, GL_VGG16 = 4, GL_BERT_BASE = 5 };
+
+/* Completion of one submitted batch.  t_submit_ns is the host
+ * CLOCK_MONOTONIC at submit; the other stamps are the GPU's %globaltimer (ns):
+ * dequeue = CTA 0 took the descriptor, start = all CTAs passed the start barrier,
+ * end = the last layer's barrier.  Device latency = t_end_ns - t_start_ns. */
+typedef struct {
+  uint64_t ticket;
+  int32_t gpulet, model, batch, status;
+  uint64_t t_submit_ns, t_dequeue_ns, t_start_ns, t_end_ns;
+} gl_completion;
+
+/* ---- context ------------------------------------------------------------------ */
+/* Open GPUs 0..num_gpus-1 (num_gpus >= 1).  Errors: GL_E_ARG, GL_E_CUDA. */
+gl_status gl_init(int num_gpus, gl_ctx** out);
+/* Destroy every gpu-let (draining rings), free weights.  Safe on NULL. */
+gl_status gl_shutdown(gl_ctx* ctx);
+/* Thread-local description of the last error (never NULL). */
+const char* gl_last_error(void);
+
+/* ---- models ------------------------------------------------------------------- */
+/* Load a GLW1 weight file (written by synthgen) for model `kind` onto `gpu`:
+ * repacks weights into GEMM layout, encodes TMA tensor maps and compiles the layer
+ * programs for batch 1..32.  Must precede gl_create_gpulet on that GPU.
+ * Out: *model_id (>= 0).  Errors: GL_E_ARG, GL_E_PARSE, GL_E_STATE, GL_E_CUDA. */
+gl_status gl_load_model(gl_ctx* ctx, int gpu, int kind, const char* weight_file, int32_t* model_id);
+/* Bytes of the model's input and output buffers at `batch`.  Input layouts:
+ * LeNet NHWC bf16 [b,28,28,1]; GoogLeNet/ResNet-50/VGG-16 NHWC bf16 [b,224,224,8]
+ * (channels 3..7 zero); SSD NHWC bf16 [b,300,300,8]; BERT int32 ids [b,128].
+ * Outputs fp32: [b,classes]; SSD loc [b,3000,4] followed by conf [b,3000,21]. */
+gl_status gl_model_io(gl_ctx* ctx, int32_t model_id, int32_t batch, int64_t* in_bytes, int64_t* out_bytes);
+/* Algorithmic FLOPs and weight bytes of one batch (for roofline accounting). */
+gl_status gl_model_cost(gl_ctx* ctx, int32_t model_id, int32_t batch, double* flops, double* weight_bytes);
+
+/* ---- gpu-lets (§2.3) ------------------------------------------- */
+/* Create a gpu-let of sm_pct in {20,40,50,60,80,100} % on `gpu`: a green context
+ * over 8-SM groups (20->32, 40->56, 50->72, 60->92, 80->116, 100->148 SMs) running
+ * one persistent executor kernel (1 CTA per SM).  At most two per GPU, sizes summing
+ * to <= 100.  Waits (<= 5 s) until every executor CTA is resident.
+ * Out: *gpulet_id, *sm_count (actual SMs).  Errors: GL_E_GRID, GL_E_PARTITION,
+ * GL_E_NOT_CONCURRENT, GL_E_CUDA. */
+gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int sm_pct, int32_t* gpulet_id, int32_t* sm_count);
+/* Drain and stop a gpu-let's executor; its slot becomes free. */
+gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t gpulet_id);
+/* %smid of every executor CTA (confinement audit); *n = number written. */
+gl_status gl_gpulet_smids(gl_ctx* ctx, int32_t gpulet_id, int32_t* smids, int32_t cap, int32_t* n);
+
+/* ---- serving (§5) -------------------------------- */
+/* Enqueue one batch of `model_id` on `gpulet_id` (non-blocking): writes a descriptor
+ * into the gpu-let's ring.  in_dev/out_dev are device pointers on the gpu-let's GPU
+ * (layouts as gl_model_io), owned by the caller and valid until the ticket is polled.
+ * slo_ms is recorded for accounting only.  Out: *ticket.
+ * Errors: GL_E_ARG, GL_E_CAPACITY, GL_E_MODEL, GL_E_STATE, GL_E_QUEUE_FULL. */
+gl_status gl_submit_batch(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, const void* in_dev, void* out_dev,
+                          int32_t batch, float slo_ms, uint64_t* ticket);
+/* Collect up to `max` completions across all gpu-lets (non-blocking); FIFO per
+ * gpu-let.  Out: *n_out. */
+gl_status gl_poll(gl_ctx* ctx, gl_completion* out, int32_t max, int32_t* n_out);
+/* Block until `ticket`'s completion has been collected by gl_poll or this call
+ * (timeout_ms); the record is copied to *out when non-NULL. */
+gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completion* out);
+
+/* ---- latency profiler (§4.3 L(b,p)) ------------------------ */
+/* Run `warmup` + `reps` back-to-back batches of model_id at `batch` on gpulet_id and
+ * return the median device latency (t_end - t_start) in microseconds. */
+gl_status gl_profile(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t batch, int32_t warmup, int32_t reps,
+                     const void* in_dev, void* out_dev, double* median_us);
+
+/* One-shot executor launch (blocking) of one batch on n_sm CTAs (whole GPU, no
+ * green context): for ncu capture and per-step tracing.  trace_ns (host, cap
+ * entries, optional) receives %globaltimer at program start and after each step
+ * barrier; *n_steps = steps of the program. */
+gl_status gl_run_once(gl_ctx* ctx, int32_t model_id, int32_t batch, const void* in_dev, void* out_dev, int32_t n_sm,
+                      uint64_t* trace_ns, int32_t cap, int32_t* n_steps);
+/* Per-step description of a model's layer program at `batch`: first op type, op
+ * count, algorithmic FLOPs and bytes (host arrays of `cap` entries). */
+gl_status gl_program_info(gl_ctx* ctx, int32_t model_id, int32_t batch, int32_t* step_type, int32_t* step_ops,
+                          double* step_flops, double* step_bytes, int32_t cap, int32_t* n_steps);
+
+/* ---- scheduler (Alg. 1) --------------------------------- */
+typedef struct {
+  int32_t n_models;          /* <= 8, canonical order */
+  const char* const* names;  /* model names printed in the plan */
+  const int32_t* lat_us;     /* L(b,p): [n_models][32][6], p in {20,40,50,60,80,100} */
+  const double* l2;          /* solo L2 util: [n_models][6 stat batches 1,2,4,8,16,32][6] */
+  const double* mem;         /* solo DRAM util: same shape */
+  const int32_t* slo_us;     /* [n_models] */
+  const int32_t* rates;      /* [n_models] req/s */
+  double coeffs[5];          /* c1..c5 of P:641 (used by mode 1) */
+  int32_t num_gpus;
+  int32_t mode;              /* 0 gpulet, 1 gpulet+int, 2 sbp (whole-GPU temporal), 3 ideal */
+} gl_sched_input;
+/* Produce the canonical plan dump (JSON lines) into plan_buf (cap
+ * bytes, NUL-terminated); *len = bytes written (excluding NUL); *verdict = 1
+ * Schedulable / 0 NotSchedulable.  Integer maths except the knee and the factor
+ * (IEEE double, fixed order).  Errors: GL_E_ARG, GL_E_BUDGET (buffer too small). */
+gl_status gl_schedule(const gl_sched_input* in, char* plan_buf, size_t cap, size_t* len, int32_t* verdict);
+/* Ordinary least squares for the interference model (§4.4): X [n][5] row-major,
+ * y [n]; out c[5].  Householder QR.  Errors: GL_E_ARG, GL_E_DATA (rank < 5). */
+gl_status gl_fit_interference(const double* X, const double* y, int32_t n, double* c);
+
+/* ---- kernel unit entry points (tests; one-shot executor on the whole GPU) ------------ */
+/* D[M,N] = A[M,K] W[N,K]^T + bias (+ res) -> act; A, res, out device pointers (A bf16
+ * [M,K], res bf16 [M,N]); W, bias HOST bf16 bits.  act: 0 none 1 relu 2 gelu 3 tanh.
+ * swap_ab: weights as the UMMA M operand (small M).  splitk: allow split-K. */
+gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A_dev, const uint16_t* W_host, const uint16_t* bias_host,
+                       const void* res_dev, void* out_dev, int32_t M, int32_t N, int32_t K, int32_t act,
+                       int32_t swap_ab, int32_t splitk, int32_t out_fp32);
+/* Conv (NHWC bf16 x [N,H,W,C], C % 8 == 0; W host OHWI [Cout,KH,KH,C]) + bias + act -> y. */
+gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x_dev, const uint16_t* W_host, const uint16_t* bias_host,
+                       void* y_dev, int32_t N, int32_t H, int32_t W, int32_t C, int32_t Cout, int32_t KH,
+                       int32_t stride, int32_t pad, int32_t act);
+/* Misc CUDA-core op (type = executor op id: 2 dwconv, 3 maxpool, 4 avgpool, 7 layernorm,
+ * 8 attention, 9 softmax) with integer args `iargs` and host bf16 params. */
+gl_status gl_test_misc(gl_ctx* ctx, int gpu, int32_t type, const int32_t* iargs, int32_t n_iargs,
+                       const uint16_t* params_host, int64_t n_params, const void* x_dev, void* y_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPULET_H */

@@ -1,0 +1,857 @@
+// K0 gpu-let executor and the layer kernels it runs
+// (a8-a12): one persistent kernel per gpu-let, 1 CTA per SM of the gpu-let's
+// green context, 288 threads:
+//   warps 0-3  producers: implicit-im2col gather (cp.async, zero-fill) of the
+//              activation operand + TMA of the weight operand into a 4-stage
+//              128B-swizzled smem ring (mbarrier full/empty)
+//   warp  8    MMA issuer: one elected thread issues tcgen05.mma (bf16 -> fp32
+//              accumulators in TMEM, double-buffered 2 x 256 columns)
+//   warps 4-7  epilogue: tcgen05.ld TMEM -> registers, +bias (+residual)
+//              -> activation -> bf16/fp32 store (or split-K fp32 reduction)
+// Non-GEMM ops (depthwise, pools, LeNet, LayerNorm, attention, softmax) use all
+// warps on CUDA cores.  A gpu-let-wide barrier separates the steps of a layer
+// program.  Work arrives through a host-mapped ring polled by CTA 0.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "program.h"
+#include "ptx.cuh"
+
+using namespace gl;
+
+namespace {
+
+constexpr int kLag = 2;  // producer cp.async groups in flight before arriving
+
+struct Ctx {
+  const char* in;
+  char* out;
+  char* ws;
+};
+
+__device__ __forceinline__ char* res(const BufRef& b, const Ctx& c) {
+  switch (b.kind) {
+    case BUF_WS: return c.ws + b.off;
+    case BUF_IN: return const_cast<char*>(c.in) + b.off;
+    case BUF_OUT: return c.out + b.off;
+    case BUF_ABS: return reinterpret_cast<char*>(b.off);
+    default: return nullptr;
+  }
+}
+
+struct Smem {
+  uint8_t* a[kStages];
+  uint8_t* b[kStages];
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* tfull;
+  uint64_t* tempty;
+  uint32_t* tmem_base;
+  uint8_t* scratch;  // non-GEMM ops reuse the stage area
+};
+
+struct Pipe {
+  uint32_t stage = 0, phase = 0;  // smem ring position (producer / MMA each keep their own)
+  uint32_t acc = 0;               // accumulator uses (MMA / epilogue each keep their own)
+  int npend = 0;
+  uint32_t pend[kLag];
+};
+
+__device__ __forceinline__ void advance(Pipe& p) {
+  if (++p.stage == kStages) {
+    p.stage = 0;
+    p.phase ^= 1;
+  }
+}
+
+// ------------------------------------------------------------------ gpu-let barrier
+__device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long target = (unsigned long long)(epoch + 1) * gridDim.x;
+    atomicAdd(&st->barrier, 1ull);
+    uint64_t t0 = may_idle ? 0 : globaltimer();
+    uint32_t ns = 32;
+    while (ld_acquire_gpu_u64((volatile uint64_t*)&st->barrier) < target) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      if (!may_idle && globaltimer() - t0 > 20ull * 1000000000ull) __trap();
+    }
+    __threadfence();
+  }
+  ++epoch;
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ epilogue helpers
+__device__ __forceinline__ float act_f(float v, int act) {
+  switch (act) {
+    case ACT_RELU: return fmaxf(v, 0.f);
+    case ACT_GELU: return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+    case ACT_TANH: return tanhf(v);
+    default: return v;
+  }
+}
+
+__device__ __forceinline__ int64_t out_index(const Epilogue& e, int r, int c) {
+  return (int64_t)(r / e.rows_per_img) * e.img_stride + (int64_t)(r % e.rows_per_img) * e.ldc + e.col_off + c;
+}
+
+// Apply bias / residual / activation to an fp32 value of output element (m, n)
+// of D[M,N] and store it.  (r, c) = (m, n), or (n, m) for swap-AB.
+__device__ __forceinline__ void store_one(const Epilogue& e, const Ctx& X, int m, int n, float v) {
+  const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+  if (bias) v += __bfloat162float(bias[e.bias_on_m ? m : n]);
+  const int r = e.transpose ? n : m, c = e.transpose ? m : n;
+  const int64_t idx = out_index(e, r, c);
+  const __nv_bfloat16* rs = (const __nv_bfloat16*)res(e.res, X);
+  if (rs) v += __bfloat162float(rs[idx]);
+  v = act_f(v, e.act);
+  if (e.out_fp32)
+    ((float*)res(e.out, X))[idx] = v;
+  else
+    ((__nv_bfloat16*)res(e.out, X))[idx] = __float2bfloat16_rn(v);
+}
+
+// ------------------------------------------------------------------ operand gather
+struct RowCache {
+  int pix[8];   // n * H * W, or -1 if the row is out of range
+  int h0[8], w0[8];
+};
+
+__device__ __forceinline__ void rowcache_init(RowCache& rc, const Gather& g, int row0, int nrows, int t) {
+  const int rr = t >> 3;
+  const int HoWo = g.Ho * g.Wo;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int lr = rr + 16 * i;
+    const int m = row0 + lr;
+    if (lr < nrows && m < g.rows) {
+      const int n = m / HoWo, rem = m - n * HoWo;
+      const int ho = rem / g.Wo, wo = rem - ho * g.Wo;
+      rc.pix[i] = n * g.H * g.W;
+      rc.h0[i] = ho * g.stride - g.pad;
+      rc.w0[i] = wo * g.stride - g.pad;
+    } else {
+      rc.pix[i] = -1;
+      rc.h0[i] = rc.w0[i] = 0;
+    }
+  }
+}
+
+// Gather one 64-wide K block of `nrows` rows into a 128B-swizzled stage.
+__device__ __forceinline__ void gather_kblock(const Gather& g, const __nv_bfloat16* x, const RowCache& rc, int nrows,
+                                              int kb, int K_real, uint32_t dst, int t) {
+  const int c = t & 7, rr = t >> 3;
+  const int k0 = kb * 64 + c * 8;
+  const bool kvalid = k0 < K_real;
+  const int tap = k0 / g.C;
+  const int c0 = k0 - tap * g.C;
+  const int kh = tap / g.KW, kw = tap - kh * g.KW;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int lr = rr + 16 * i;
+    if (lr >= nrows) break;
+    const int hi = rc.h0[i] + kh, wi = rc.w0[i] + kw;
+    const bool ok = kvalid && rc.pix[i] >= 0 && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W;
+    const __nv_bfloat16* src = ok ? x + ((int64_t)(rc.pix[i] + hi * g.W + wi) * g.lda + c0) : x;
+    const uint32_t off = lr * 128 + ((c ^ (lr & 7)) << 4);
+    cp_async16(dst + off, src, ok ? 16u : 0u);
+  }
+}
+
+__device__ __forceinline__ void decode_tile(const GemmArgs& g, int lt, int& mb, int& nb, int& kb0, int& kb1) {
+  mb = lt % g.n_mblk;
+  const int r = lt / g.n_mblk;
+  nb = r % g.n_nblk;
+  const int s = r / g.n_nblk;
+  const int nkb = g.K_pad / 64;
+  kb0 = s * g.kb_per_split;
+  kb1 = min(nkb, kb0 + g.kb_per_split);
+}
+
+__device__ __forceinline__ int locate(const OpDesc* ops, int nops, int t, int& lt) {
+  int i = 0;
+  while (i < nops - 1 && t >= ops[i].n_units) {
+    t -= ops[i].n_units;
+    ++i;
+  }
+  lt = t;
+  return i;
+}
+
+// ------------------------------------------------------------------ GEMM step (K1-K4)
+__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& S, Pipe& P) {
+  int total = 0;
+  for (int i = 0; i < nops; ++i) total += ops[i].n_units;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp < 4) {
+    // ---------------- producers
+    const int t = threadIdx.x;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int lt;
+      const OpDesc* op = ops + locate(ops, nops, tile, lt);
+      const GemmArgs& g = op->g;
+      int mb, nb, kb0, kb1;
+      decode_tile(g, lt, mb, nb, kb0, kb1);
+      const Gather& gg = g.a_tma ? g.gb : g.ga;
+      const int grows = g.a_tma ? g.BN : 128;
+      const int grow0 = g.a_tma ? nb * g.BN : mb * 128;
+      const __nv_bfloat16* gx = (const __nv_bfloat16*)res(gg.x, X);
+      RowCache rc;
+      rowcache_init(rc, gg, grow0, grows, t);
+      const uint32_t tx = (g.a_tma ? 128 * 128 : 0) + (g.b_tma ? g.BN * 128 : 0);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&S.empty[P.stage], P.phase ^ 1);
+        if (t == 0) {
+          mbar_arrive_expect_tx(&S.full[P.stage], tx);
+          if (g.a_tma) tma_load_2d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+          if (g.b_tma) tma_load_2d(smem_u32(S.b[P.stage]), &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
+        }
+        gather_kblock(gg, gx, rc, grows, kb, g.K_real, smem_u32(g.a_tma ? S.b[P.stage] : S.a[P.stage]), t);
+        cp_async_commit();
+        if (P.npend == kLag) {
+          cp_async_wait<kLag>();
+          fence_proxy_async_smem();
+          mbar_arrive(&S.full[P.pend[0]]);
+#pragma unroll
+          for (int i = 0; i < kLag - 1; ++i) P.pend[i] = P.pend[i + 1];
+          --P.npend;
+        }
+        P.pend[P.npend++] = P.stage;
+        advance(P);
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int i = 0; i < P.npend; ++i) mbar_arrive(&S.full[P.pend[i]]);
+    P.npend = 0;
+  } else if (warp == 8) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t tbase = *S.tmem_base;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int lt;
+        const OpDesc* op = ops + locate(ops, nops, tile, lt);
+        const GemmArgs& g = op->g;
+        int mb, nb, kb0, kb1;
+        decode_tile(g, lt, mb, nb, kb0, kb1);
+        const uint32_t acc = P.acc & 1, use = P.acc >> 1;
+        mbar_wait(&S.tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + acc * 256;
+        const uint32_t idesc = umma_idesc_bf16(128, g.BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&S.full[P.stage], P.phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(S.a[P.stage]), b0 = smem_u32(S.b[P.stage]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(d, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit(&S.empty[P.stage]);
+          advance(P);
+        }
+        umma_commit(&S.tfull[acc]);
+        ++P.acc;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 4-7 -> TMEM lanes 0-127)
+    const int q = warp - 4;
+    const uint32_t tbase = *S.tmem_base;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int lt;
+      const OpDesc* op = ops + locate(ops, nops, tile, lt);
+      const GemmArgs& g = op->g;
+      const Epilogue& e = g.ep;
+      int mb, nb, kb0, kb1;
+      decode_tile(g, lt, mb, nb, kb0, kb1);
+      const uint32_t acc = P.acc & 1, use = P.acc >> 1;
+      mbar_wait(&S.tfull[acc], use & 1);
+      tc_fence_after();
+      const int m = mb * 128 + q * 32 + lane;
+      const int nend = min(g.N, (nb + 1) * g.BN);
+      float* ws = (float*)res(e.ws, X);
+      const bool vec = !e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 &&
+                       (e.col_off % 8) == 0;
+      const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+      const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
+      __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
+      for (int j = 0; j < g.BN; j += 32) {
+        float v[32];
+        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
+        const int n0 = nb * g.BN + j;
+        if (m >= g.M || n0 >= nend) continue;
+        if (e.splitk > 1) {
+          // split-K partials: plain stores into ws[split][M][N], summed in order by the finalize op
+          float* wp = ws + ((int64_t)(kb0 / g.kb_per_split) * g.M + m) * g.N;
+          for (int c = 0; c < 32 && n0 + c < nend; ++c) wp[n0 + c] = v[c];
+        } else if (vec && n0 + 32 <= nend) {
+          const int64_t o0 = (int64_t)m * e.ldc + e.col_off + n0;
+          __align__(16) __nv_bfloat16 r[32];
+          if (rsd) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ((uint4*)r)[c] = ((const uint4*)(rsd + o0))[c];
+          }
+          __align__(16) __nv_bfloat16 o[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            float x = v[c] + (bias ? __bfloat162float(bias[n0 + c]) : 0.f);
+            if (rsd) x += __bfloat162float(r[c]);
+            o[c] = __float2bfloat16_rn(act_f(x, e.act));
+          }
+          uint4* dst = (uint4*)(outp + o0);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dst[c] = ((const uint4*)o)[c];
+        } else {
+          for (int c = 0; c < 32 && n0 + c < nend; ++c) store_one(e, X, m, n0 + c, v[c]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&S.tempty[acc]);
+      ++P.acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ split-K final
+__device__ void splitk_final(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const Epilogue& e = a.ep;
+  const float* ws = (const float*)res(e.ws, X);
+  const int64_t total = (int64_t)a.rows * a.cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / a.cols), n = (int)(i - (int64_t)m * a.cols);
+    float v = 0.f;
+    for (int s = 0; s < e.splitk; ++s) v += ws[(int64_t)s * total + i];
+    store_one(e, X, m, n, v);
+  }
+}
+
+// ------------------------------------------------------------------ depthwise 3x3 (K5)
+__device__ void dwconv(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
+  const __nv_bfloat16* w = (const __nv_bfloat16*)res(a.w, X);   // [9][C] tap-major
+  const __nv_bfloat16* b = (const __nv_bfloat16*)res(a.b, X);
+  __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  const int CG = a.C / 8;
+  const int64_t total = (int64_t)a.N * a.Ho * a.Wo * CG;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cg = (int)(i % CG);
+    int64_t p = i / CG;
+    const int wo = (int)(p % a.Wo);
+    p /= a.Wo;
+    const int ho = (int)(p % a.Ho);
+    const int n = (int)(p / a.Ho);
+    float acc[8];
+    const uint4 bv = *(const uint4*)(b + cg * 8);
+    const __nv_bfloat16* bb = (const __nv_bfloat16*)&bv;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = __bfloat162float(bb[c]);
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int hi = ho * a.stride - a.pad + kh;
+      if (hi < 0 || hi >= a.H) continue;
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        const int wi = wo * a.stride - a.pad + kw;
+        if (wi < 0 || wi >= a.W) continue;
+        const uint4 xv = *(const uint4*)(x + (((int64_t)n * a.H + hi) * a.W + wi) * a.C + cg * 8);
+        const uint4 wv = *(const uint4*)(w + (kh * 3 + kw) * a.C + cg * 8);
+        const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
+        const __nv_bfloat16* ww = (const __nv_bfloat16*)&wv;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = fmaf(__bfloat162float(xx[c]), __bfloat162float(ww[c]), acc[c]);
+      }
+    }
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(act_f(acc[c], a.act));
+    *(uint4*)(y + (((int64_t)n * a.Ho + ho) * a.Wo + wo) * a.C + cg * 8) = *(const uint4*)o;
+  }
+}
+
+// ------------------------------------------------------------------ max pool (K6)
+__device__ void maxpool(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
+  __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  const int CG = a.C / 8;
+  const int64_t total = (int64_t)a.N * a.Ho * a.Wo * CG;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cg = (int)(i % CG);
+    int64_t p = i / CG;
+    const int wo = (int)(p % a.Wo);
+    p /= a.Wo;
+    const int ho = (int)(p % a.Ho);
+    const int n = (int)(p / a.Ho);
+    float mx[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) mx[c] = -INFINITY;
+    for (int kh = 0; kh < a.k; ++kh) {
+      const int hi = ho * a.stride - a.pad + kh;
+      if (hi < 0 || hi >= a.H) continue;
+      for (int kw = 0; kw < a.k; ++kw) {
+        const int wi = wo * a.stride - a.pad + kw;
+        if (wi < 0 || wi >= a.W) continue;
+        const uint4 xv = *(const uint4*)(x + (((int64_t)n * a.H + hi) * a.W + wi) * a.C + cg * 8);
+        const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) mx[c] = fmaxf(mx[c], __bfloat162float(xx[c]));
+      }
+    }
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(mx[c]);
+    *(uint4*)(y + (((int64_t)n * a.Ho + ho) * a.Wo + wo) * a.C + cg * 8) = *(const uint4*)o;
+  }
+}
+
+// ------------------------------------------------------------------ global avg pool (K6)
+__device__ void avgpool(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
+  __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  const int CG = a.C / 8, HW = a.H * a.W;
+  const int total = a.N * CG;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int cg = i % CG, n = i / CG;
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < HW; ++p) {
+      const uint4 xv = *(const uint4*)(x + ((int64_t)n * HW + p) * a.C + cg * 8);
+      const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s[c] += __bfloat162float(xx[c]);
+    }
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(s[c] / (float)HW);
+    *(uint4*)(y + (int64_t)n * a.C + cg * 8) = *(const uint4*)o;
+  }
+}
+
+// ------------------------------------------------------------------ LeNet-5 fused (K7)
+__device__ __forceinline__ float bfr(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+__device__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
+  const __nv_bfloat16* W = (const __nv_bfloat16*)res(a.w, X);  // packed params in manifest order
+  float* y = (float*)res(a.y, X);
+  const __nv_bfloat16 *w1 = W, *b1 = w1 + 150, *w2 = b1 + 6, *b2 = w2 + 2400, *f1 = b2 + 16, *fb1 = f1 + 48000,
+                      *f2 = fb1 + 120, *fb2 = f2 + 10080, *f3 = fb2 + 84, *fb3 = f3 + 840;
+  float* img = (float*)scratch;   // 28*28
+  float* p1 = img + 784;          // 14*14*6
+  float* p2 = p1 + 1176;          // 5*5*16
+  float* h1 = p2 + 400;           // 120
+  float* h2 = h1 + 120;           // 84
+  for (int n = blockIdx.x; n < a.N; n += gridDim.x) {
+    for (int i = threadIdx.x; i < 784; i += blockDim.x) img[i] = __bfloat162float(x[(int64_t)n * 784 + i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 1176; i += blockDim.x) {   // conv1 5x5 pad 2 + relu + bf16 + maxpool2
+      const int co = i % 6, px = (i / 6) % 14, py = i / 84;
+      float m = -INFINITY;
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          const int oy = 2 * py + dy, ox = 2 * px + dx;
+          float s = __bfloat162float(b1[co]);
+          for (int kh = 0; kh < 5; ++kh) {
+            const int iy = oy + kh - 2;
+            if (iy < 0 || iy >= 28) continue;
+            for (int kw = 0; kw < 5; ++kw) {
+              const int ix = ox + kw - 2;
+              if (ix < 0 || ix >= 28) continue;
+              s = fmaf(img[iy * 28 + ix], __bfloat162float(w1[co * 25 + kh * 5 + kw]), s);
+            }
+          }
+          m = fmaxf(m, bfr(fmaxf(s, 0.f)));
+        }
+      p1[i] = m;   // index (py*14 + px)*6 + co
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 400; i += blockDim.x) {    // conv2 5x5 (6->16) + relu + bf16 + maxpool2
+      const int co = i % 16, px = (i / 16) % 5, py = i / 80;
+      float m = -INFINITY;
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          const int oy = 2 * py + dy, ox = 2 * px + dx;
+          float s = __bfloat162float(b2[co]);
+          for (int kh = 0; kh < 5; ++kh)
+            for (int kw = 0; kw < 5; ++kw)
+              for (int ci = 0; ci < 6; ++ci)
+                s = fmaf(p1[((oy + kh) * 14 + ox + kw) * 6 + ci],
+                         __bfloat162float(w2[((co * 5 + kh) * 5 + kw) * 6 + ci]), s);
+          m = fmaxf(m, bfr(fmaxf(s, 0.f)));
+        }
+      p2[i] = m;   // NHWC flatten (h, w, c)
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < 120; j += blockDim.x) {
+      float s = __bfloat162float(fb1[j]);
+      for (int k = 0; k < 400; ++k) s = fmaf(p2[k], __bfloat162float(f1[j * 400 + k]), s);
+      h1[j] = bfr(fmaxf(s, 0.f));
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < 84; j += blockDim.x) {
+      float s = __bfloat162float(fb2[j]);
+      for (int k = 0; k < 120; ++k) s = fmaf(h1[k], __bfloat162float(f2[j * 120 + k]), s);
+      h2[j] = bfr(fmaxf(s, 0.f));
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < 10; j += blockDim.x) {
+      float s = __bfloat162float(fb3[j]);
+      for (int k = 0; k < 84; ++k) s = fmaf(h2[k], __bfloat162float(f3[j * 84 + k]), s);
+      y[(int64_t)n * 10 + j] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ LayerNorm rows (K8, K10)
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per 768-wide row; 24 values per lane (3 x 16-byte vectors).
+__device__ __forceinline__ void ln_row_store(float* v, const __nv_bfloat16* g, const __nv_bfloat16* b, float eps,
+                                             __nv_bfloat16* y, int lane) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 24; ++i) s += v[i];
+  const float mean = warp_sum(s) * (1.f / 768.f);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 24; ++i) {
+    const float d = v[i] - mean;
+    q += d * d;
+  }
+  const float rstd = rsqrtf(warp_sum(q) * (1.f / 768.f) + eps);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int c0 = j * 256 + lane * 8;
+    const uint4 gv = *(const uint4*)(g + c0), bv = *(const uint4*)(b + c0);
+    const __nv_bfloat16 *gg = (const __nv_bfloat16*)&gv, *bb = (const __nv_bfloat16*)&bv;
+    __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      o[c] = __float2bfloat16_rn((v[j * 8 + c] - mean) * rstd * __bfloat162float(gg[c]) + __bfloat162float(bb[c]));
+    *(uint4*)(y + c0) = *(const uint4*)o;
+  }
+}
+
+__device__ void layernorm(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
+  __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  const __nv_bfloat16 *g = (const __nv_bfloat16*)res(a.g, X), *b = (const __nv_bfloat16*)res(a.b, X);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < a.rows; r += gridDim.x * wpb) {
+    float v[24];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint4 xv = *(const uint4*)(x + (int64_t)r * 768 + j * 256 + lane * 8);
+      const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[j * 8 + c] = __bfloat162float(xx[c]);
+    }
+    ln_row_store(v, g, b, a.eps, y + (int64_t)r * 768, lane);
+  }
+}
+
+__device__ void embed_ln(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const int32_t* ids = (const int32_t*)res(a.x, X);
+  const __nv_bfloat16* word = (const __nv_bfloat16*)res(a.w, X);   // [vocab, 768]
+  const __nv_bfloat16* pos = (const __nv_bfloat16*)res(a.aux, X);  // [512, 768] followed by type [2, 768]
+  const __nv_bfloat16* typ = pos + 512 * 768;
+  __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  const __nv_bfloat16 *g = (const __nv_bfloat16*)res(a.g, X), *b = (const __nv_bfloat16*)res(a.b, X);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < a.rows; r += gridDim.x * wpb) {
+    const int id = ids[r], s = r % a.seq;
+    float v[24];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c0 = j * 256 + lane * 8;
+      const uint4 wv = *(const uint4*)(word + (int64_t)id * 768 + c0);
+      const uint4 pv = *(const uint4*)(pos + (int64_t)s * 768 + c0);
+      const uint4 tv = *(const uint4*)(typ + c0);
+      const __nv_bfloat16 *ww = (const __nv_bfloat16*)&wv, *pp = (const __nv_bfloat16*)&pv,
+                          *tt = (const __nv_bfloat16*)&tv;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        v[j * 8 + c] = __bfloat162float(ww[c]) + __bfloat162float(pp[c]) + __bfloat162float(tt[c]);
+    }
+    ln_row_store(v, g, b, a.eps, y + (int64_t)r * 768, lane);
+  }
+}
+
+// ------------------------------------------------------------------ attention (K9)
+// Unit = (sequence, head): S = Q K^T / 8 (fp32), softmax fp32, P -> bf16,
+// O = P V (fp32) -> bf16.  qkv [b*seq, 3*768]; ctx [b*seq, 768].
+__device__ void attention(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+  const MiscArgs& a = op->m;
+  const __nv_bfloat16* qkv = (const __nv_bfloat16*)res(a.x, X);
+  __nv_bfloat16* ctx = (__nv_bfloat16*)res(a.y, X);
+  const int S = a.seq, DH = a.dh, H = a.heads, HD = H * DH;   // 128, 64, 12, 768
+  float* Ks = (float*)scratch;                 // [S][DH+1]
+  float* Vs = Ks + S * (DH + 1);               // [S][DH]
+  __nv_bfloat16* Ps = (__nv_bfloat16*)(Vs + S * DH);  // [S][S+8]
+  const int units = a.N * H;
+  const int t = threadIdx.x;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int seqi = u / H, h = u % H;
+    const __nv_bfloat16* base = qkv + (int64_t)seqi * S * 3 * HD;
+    for (int i = t; i < S * DH / 8; i += blockDim.x) {
+      const int r = i / (DH / 8), c8 = (i % (DH / 8)) * 8;
+      const uint4 kv = *(const uint4*)(base + (int64_t)r * 3 * HD + HD + h * DH + c8);
+      const uint4 vv = *(const uint4*)(base + (int64_t)r * 3 * HD + 2 * HD + h * DH + c8);
+      const __nv_bfloat16 *kk = (const __nv_bfloat16*)&kv, *vvv = (const __nv_bfloat16*)&vv;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        Ks[r * (DH + 1) + c8 + c] = __bfloat162float(kk[c]);
+        Vs[r * DH + c8 + c] = __bfloat162float(vvv[c]);
+      }
+    }
+    __syncthreads();
+    if (t < 2 * S) {
+      const int i = t >> 1, half = t & 1;
+      float q[64];
+      const __nv_bfloat16* qp = base + (int64_t)i * 3 * HD + h * DH;
+#pragma unroll
+      for (int d8 = 0; d8 < 64; d8 += 8) {
+        const uint4 qv = *(const uint4*)(qp + d8);
+        const __nv_bfloat16* qq = (const __nv_bfloat16*)&qv;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) q[d8 + c] = __bfloat162float(qq[c]);
+      }
+      float s[64];
+      float mx = -INFINITY;
+#pragma unroll 4
+      for (int jj = 0; jj < 64; ++jj) {
+        const float* kr = Ks + (half * 64 + jj) * (DH + 1);
+        float acc = 0.f;
+#pragma unroll
+        for (int d = 0; d < 64; ++d) acc = fmaf(q[d], kr[d], acc);
+        s[jj] = acc * 0.125f;
+        mx = fmaxf(mx, s[jj]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      float sum = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < 64; ++jj) {
+        s[jj] = expf(s[jj] - mx);
+        sum += s[jj];
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      const float inv = 1.f / sum;
+#pragma unroll
+      for (int jj = 0; jj < 64; ++jj) Ps[i * (S + 8) + half * 64 + jj] = __float2bfloat16_rn(s[jj] * inv);
+    }
+    __syncthreads();
+    if (t < 2 * S) {
+      const int i = t >> 1, half = t & 1;
+      float o[32];
+#pragma unroll
+      for (int d = 0; d < 32; ++d) o[d] = 0.f;
+      for (int j = 0; j < S; ++j) {
+        const float p = __bfloat162float(Ps[i * (S + 8) + j]);
+        const float* vr = Vs + j * DH + half * 32;
+#pragma unroll
+        for (int d = 0; d < 32; ++d) o[d] = fmaf(p, vr[d], o[d]);
+      }
+      __align__(16) __nv_bfloat16 ob[32];
+#pragma unroll
+      for (int d = 0; d < 32; ++d) ob[d] = __float2bfloat16_rn(o[d]);
+      uint4* dst = (uint4*)(ctx + ((int64_t)seqi * S + i) * HD + h * DH + half * 32);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[c] = ((const uint4*)ob)[c];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ row softmax (K11)
+__device__ void softmax_rows(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  float* x = (float*)res(a.x, X);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.rows; r += gridDim.x * blockDim.x) {
+    float* row = x + (int64_t)r * a.cols;
+    float mx = -INFINITY;
+    for (int c = 0; c < a.cols; ++c) mx = fmaxf(mx, row[c]);
+    float s = 0.f;
+    for (int c = 0; c < a.cols; ++c) s += expf(row[c] - mx);
+    const float inv = 1.f / s;
+    for (int c = 0; c < a.cols; ++c) row[c] = expf(row[c] - mx) * inv;
+  }
+}
+
+__device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S) {
+  switch (op->type) {
+    case OP_DWCONV: dwconv(op, X); break;
+    case OP_MAXPOOL: maxpool(op, X); break;
+    case OP_AVGPOOL: avgpool(op, X); break;
+    case OP_LENET: lenet(op, X, S.scratch); break;
+    case OP_EMBED_LN: embed_ln(op, X); break;
+    case OP_LAYERNORM: layernorm(op, X); break;
+    case OP_ATTENTION: attention(op, X, S.scratch); break;
+    case OP_SOFTMAX: softmax_rows(op, X); break;
+    case OP_SPLITK_FINAL: splitk_final(op, X); break;
+    default: __trap();
+  }
+}
+
+__device__ void run_program(const WorkDesc& w, const Ctx& X, const Smem& S, Pipe& P, ExecState* st,
+                            uint64_t& epoch, uint64_t* trace, int trace_cap) {
+  int i = 0, step = 0;
+  const bool tr = trace && blockIdx.x == 0 && threadIdx.x == 0;
+  if (tr && trace_cap > 0) trace[0] = globaltimer();
+  while (i < w.n_ops) {
+    int j = i;
+    while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
+    if (w.prog[i].type == OP_GEMM) {
+      gemm_step(w.prog + i, j - i + 1, X, S, P);
+    } else {
+      for (int k = i; k <= j; ++k) run_misc(w.prog + k, X, S);
+    }
+    fence_proxy_async_smem();
+    gridsync(st, epoch, false);
+    ++step;
+    if (tr && step < trace_cap) trace[step] = globaltimer();
+    i = j + 1;
+  }
+}
+
+}  // namespace
+
+extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  Smem S;
+  for (int s = 0; s < kStages; ++s) {
+    S.a[s] = base + s * kStageBytesA;
+    S.b[s] = base + kStages * kStageBytesA + s * kStageBytesB;
+  }
+  uint64_t* bars = (uint64_t*)(base + kStages * (kStageBytesA + kStageBytesB));
+  S.full = bars;
+  S.empty = bars + kStages;
+  S.tfull = bars + 2 * kStages;
+  S.tempty = bars + 2 * kStages + 2;
+  S.tmem_base = (uint32_t*)(bars + 2 * kStages + 4);
+  S.scratch = base;
+
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 128 + 1);
+      mbar_init(&S.empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&S.tfull[s], 1);
+      mbar_init(&S.tempty[s], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc(S.tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (threadIdx.x == 0) {
+    if (p.smid_log) p.smid_log[blockIdx.x] = (int)smid();
+    p.ring->resident[blockIdx.x] = 1u;
+    __threadfence_system();
+  }
+
+  Pipe P;
+  uint64_t epoch = 0;
+  int done = 0;
+  for (;;) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint64_t head = p.st->head;
+      bool quit = false;
+      uint32_t ns = 64;
+      for (;;) {
+        if (ld_acquire_sys_u64(&p.ring->tail) > head) break;
+        if (ld_acquire_sys_u64(&p.ring->quit)) {
+          quit = true;
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+      }
+      if (quit) {
+        p.st->quit = 1;
+      } else {
+        const volatile WorkDesc* src = &p.ring->items[head % kRing];
+        WorkDesc w;
+        w.ticket = src->ticket;
+        w.prog = src->prog;
+        w.in = src->in;
+        w.out = src->out;
+        w.n_ops = src->n_ops;
+        w.model = src->model;
+        w.batch = src->batch;
+        w.slo_us = src->slo_us;
+        w.t_submit_ns = src->t_submit_ns;
+        p.st->cur = w;
+        p.st->t_dequeue = globaltimer();
+        p.st->head = head + 1;
+      }
+      __threadfence();
+    }
+    gridsync(p.st, epoch, true);
+    if (*(volatile uint64_t*)&p.st->quit) break;
+    WorkDesc w;
+    {
+      const volatile WorkDesc* c = &p.st->cur;
+      w.ticket = c->ticket;
+      w.prog = c->prog;
+      w.in = c->in;
+      w.out = c->out;
+      w.n_ops = c->n_ops;
+      w.model = c->model;
+      w.batch = c->batch;
+      w.slo_us = c->slo_us;
+      w.t_submit_ns = c->t_submit_ns;
+    }
+    const uint64_t t_start = globaltimer();
+    Ctx X{(const char*)w.in, (char*)w.out, p.ws};
+    run_program(w, X, S, P, p.st, epoch, p.trace, p.trace_cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint64_t i = p.ring->heartbeat;
+      volatile CompRec* c = &p.ring->comp[i % kRing];
+      c->ticket = w.ticket;
+      c->gpulet = p.gpulet;
+      c->model = w.model;
+      c->batch = w.batch;
+      c->status = 0;
+      c->t_submit_ns = w.t_submit_ns;
+      c->t_dequeue_ns = p.st->t_dequeue;
+      c->t_start_ns = t_start;
+      c->t_end_ns = globaltimer();
+      __threadfence_system();
+      p.ring->heartbeat = i + 1;
+      st_release_sys_u64(&p.ring->comp_tail, i + 1);
+    }
+    if (p.one_shot > 0 && ++done >= p.one_shot) break;
+  }
+  __syncthreads();
+  if (warp == 8) tmem_dealloc(*S.tmem_base, 512);
+}
+
+extern "C" cudaKernel_t gl_executor_handle() {
+  cudaKernel_t k = nullptr;
+  if (cudaGetKernel(&k, (const void*)gl_executor) != cudaSuccess) return nullptr;
+  return k;
+}

@@ -1,0 +1,1048 @@
+// Layer-program builders for the six models (SURVEY.md §8(c) C1.2 topologies;
+// PAPER.md Table `tab:ml-models`, names the five CNNs and their input
+// sizes; BERT-base is the north_star addition).  This is the product path's own
+// description of each network (it shares no code with oracle/): it walks the
+// topology, repacks the weights into GEMM layout ([Cout, K_pad] bf16, K ordered
+// (kh, kw, c) with c fastest, K padded to a multiple of 64), encodes the TMA
+// tensor maps and plans the activation workspace (liveness-based first fit).
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "runtime.h"
+
+namespace gl {
+
+static const char* kNames[6] = {"lenet5", "googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"};
+int model_kind_count() { return 6; }
+const char* model_name(int kind) { return (kind >= 0 && kind < 6) ? kNames[kind] : "?"; }
+
+DevWeights::~DevWeights() {
+  for (void* p : allocs) release_device(p, false);
+}
+
+static void* upload(DevWeights& dw, const void* host, size_t bytes) {
+  void* d = nullptr;
+  if (cudaMalloc(&d, std::max<size_t>(bytes, 256)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice);
+  dw.allocs.push_back(d);
+  dw.bytes += bytes;
+  return d;
+}
+
+static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+struct WRef {
+  void* ptr = nullptr;
+  int rows = 0, K_real = 0, K_pad = 0;
+};
+
+struct Err {
+  std::string msg;
+  bool fail(const std::string& m) {
+    if (msg.empty()) msg = m;
+    return false;
+  }
+};
+
+// Conv weight [Cout, KH, KW, Cin] -> [Cout, K_pad], Cin zero-padded to cin_pad.
+static WRef conv_weight(DevWeights& dw, const ParamMap& P, const std::string& name, int cin_pad, Err& e) {
+  const std::string key = name + "#conv" + std::to_string(cin_pad);
+  auto it = P.find(name + ".w");
+  if (it == P.end()) {
+    e.fail("missing parameter " + name + ".w");
+    return {};
+  }
+  const Param& p = it->second;
+  const int co = p.shape[0], kh = p.shape[1], kw = p.shape[2], ci = p.shape[3];
+  WRef r;
+  r.rows = co;
+  r.K_real = kh * kw * cin_pad;
+  r.K_pad = rup(r.K_real, 64);
+  auto f = dw.ptr.find(key);
+  if (f != dw.ptr.end()) {
+    r.ptr = f->second;
+    return r;
+  }
+  std::vector<uint16_t> buf((size_t)co * r.K_pad, 0);
+  for (int o = 0; o < co; ++o)
+    for (int t = 0; t < kh * kw; ++t)
+      for (int c = 0; c < ci; ++c) buf[(size_t)o * r.K_pad + t * cin_pad + c] = p.data[((size_t)o * kh * kw + t) * ci + c];
+  r.ptr = upload(dw, buf.data(), buf.size() * 2);
+  dw.ptr[key] = r.ptr;
+  return r;
+}
+
+// FC weight [out, in] -> [out, K_pad].
+static WRef fc_weight(DevWeights& dw, const ParamMap& P, const std::string& name, Err& e) {
+  auto it = P.find(name + ".w");
+  if (it == P.end()) {
+    e.fail("missing parameter " + name + ".w");
+    return {};
+  }
+  const Param& p = it->second;
+  WRef r;
+  r.rows = p.shape[0];
+  r.K_real = p.shape[1];
+  r.K_pad = rup(r.K_real, 64);
+  const std::string key = name + "#fc";
+  auto f = dw.ptr.find(key);
+  if (f != dw.ptr.end()) {
+    r.ptr = f->second;
+    return r;
+  }
+  std::vector<uint16_t> buf((size_t)r.rows * r.K_pad, 0);
+  for (int o = 0; o < r.rows; ++o)
+    std::memcpy(&buf[(size_t)o * r.K_pad], &p.data[(size_t)o * r.K_real], (size_t)r.K_real * 2);
+  r.ptr = upload(dw, buf.data(), buf.size() * 2);
+  dw.ptr[key] = r.ptr;
+  return r;
+}
+
+static void* raw_param(DevWeights& dw, const ParamMap& P, const std::string& name, Err& e) {
+  auto f = dw.ptr.find(name);
+  if (f != dw.ptr.end()) return f->second;
+  auto it = P.find(name);
+  if (it == P.end()) {
+    e.fail("missing parameter " + name);
+    return nullptr;
+  }
+  void* d = upload(dw, it->second.data.data(), it->second.data.size() * 2);
+  dw.ptr[name] = d;
+  return d;
+}
+
+// Depthwise weight [C,3,3,1] -> tap-major [9][C].
+static void* dw_weight(DevWeights& dw, const ParamMap& P, const std::string& name, Err& e) {
+  const std::string key = name + "#dw";
+  auto f = dw.ptr.find(key);
+  if (f != dw.ptr.end()) return f->second;
+  auto it = P.find(name + ".w");
+  if (it == P.end()) {
+    e.fail("missing parameter " + name + ".w");
+    return nullptr;
+  }
+  const Param& p = it->second;
+  const int C = p.shape[0];
+  std::vector<uint16_t> buf((size_t)9 * C);
+  for (int c = 0; c < C; ++c)
+    for (int t = 0; t < 9; ++t) buf[(size_t)t * C + c] = p.data[(size_t)c * 9 + t];
+  void* d = upload(dw, buf.data(), buf.size() * 2);
+  dw.ptr[key] = d;
+  return d;
+}
+
+static bool encode_tmap(CUtensorMap* map, const void* gaddr, int K_pad, int rows, int box_rows, Err& e) {
+  Driver& D = driver();
+  if (!D.tensorMapEncodeTiled) return e.fail("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K_pad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K_pad * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = D.tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(gaddr), dims,
+                                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return e.fail("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return true;
+}
+
+static BufRef ws_ref(uint64_t off) { return BufRef{off, BUF_WS, 0}; }
+static BufRef abs_ref(const void* p) { return BufRef{(uint64_t)(uintptr_t)p, p ? BUF_ABS : BUF_NONE, 0}; }
+static BufRef in_ref(uint64_t off) { return BufRef{off, BUF_IN, 0}; }
+static BufRef out_ref(uint64_t off) { return BufRef{off, BUF_OUT, 0}; }
+
+// NHWC bf16 activation (or a [rows, C] matrix with H = W = 1).
+struct Act {
+  BufRef ref;
+  int N = 0, H = 0, W = 0, C = 0;
+  int ld = 0;  // pixel stride in elements
+};
+
+class Builder {
+ public:
+  Builder(const ParamMap& P, DevWeights& dw, int batch, Program& prog) : P(P), dw(dw), b(batch), prog(prog) {}
+
+  const ParamMap& P;
+  DevWeights& dw;
+  int b;
+  Program& prog;
+  Err e;
+  int step_first = 0;
+
+  // ---------------- workspace (first fit; frees take effect at the next step boundary)
+  struct Block {
+    uint64_t off, size;
+    bool free;
+  };
+  std::vector<Block> blocks;
+  std::vector<uint64_t> pending;
+  uint64_t top = 0;
+
+  uint64_t alloc(uint64_t bytes) {
+    bytes = (bytes + 255) / 256 * 256;
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      if (blocks[i].free && blocks[i].size >= bytes) {
+        if (blocks[i].size > bytes) blocks.insert(blocks.begin() + i + 1, Block{blocks[i].off + bytes, blocks[i].size - bytes, true});
+        blocks[i].size = bytes;
+        blocks[i].free = false;
+        return blocks[i].off;
+      }
+    }
+    blocks.push_back(Block{top, bytes, false});
+    top += bytes;
+    prog.ws_bytes = std::max<size_t>(prog.ws_bytes, top);
+    return blocks.back().off;
+  }
+  void release(const Act& a) {
+    if (a.ref.kind == BUF_WS) pending.push_back(a.ref.off);
+  }
+  void release_off(uint64_t off) { pending.push_back(off); }
+  void step() {
+    if (!prog.ops.empty()) prog.ops.back().step_end = 1;
+    for (uint64_t off : pending)
+      for (auto& bl : blocks)
+        if (bl.off == off) bl.free = true;
+    pending.clear();
+    for (size_t i = 0; i + 1 < blocks.size();) {
+      if (blocks[i].free && blocks[i + 1].free) {
+        blocks[i].size += blocks[i + 1].size;
+        blocks.erase(blocks.begin() + i + 1);
+      } else {
+        ++i;
+      }
+    }
+  }
+
+  Act tensor(int N, int H, int W, int C) {
+    Act a;
+    a.N = N, a.H = H, a.W = W, a.C = C, a.ld = C;
+    a.ref = ws_ref(alloc((uint64_t)N * H * W * C * 2));
+    return a;
+  }
+
+  OpDesc& add(int type) {
+    prog.ops.emplace_back();
+    OpDesc& op = prog.ops.back();
+    std::memset(&op, 0, sizeof(OpDesc));
+    op.type = type;
+    return op;
+  }
+
+  static Epilogue plain_ep(BufRef out, int ldc, int col_off) {
+    Epilogue ep;
+    std::memset(&ep, 0, sizeof(ep));
+    ep.out = out;
+    ep.ldc = ldc;
+    ep.col_off = col_off;
+    ep.rows_per_img = INT_MAX;
+    ep.img_stride = 0;
+    return ep;
+  }
+
+  // GEMM with the activation operand gathered (A, M rows) and the weights by TMA (B).
+  // Returns false on error.  If split-K is chosen, a finalize op is queued for the next step.
+  void gemm_gather_a(const Gather& ga, int M, const WRef& w, const void* bias, Epilogue ep, bool allow_split = true) {
+    if (!w.ptr) return;
+    OpDesc& op = add(OP_GEMM);
+    GemmArgs& g = op.g;
+    g.M = M;
+    g.N = w.rows;
+    g.K_real = w.K_real;
+    g.K_pad = w.K_pad;
+    const int nnb = (g.N + 255) / 256;
+    g.BN = std::max(16, rup((g.N + nnb - 1) / nnb, 16));
+    g.n_nblk = (g.N + g.BN - 1) / g.BN;
+    g.n_mblk = (M + 127) / 128;
+    g.a_tma = 0;
+    g.b_tma = 1;
+    g.ga = ga;
+    g.ga.rows = M;
+    ep.bias = abs_ref(bias);
+    choose_split(op, allow_split);
+    g.ep = ep;
+    encode_tmap(&op.tmap_b, w.ptr, w.K_pad, w.rows, g.BN, e);
+    finish_gemm(op);
+    prog.flops += 2.0 * M * g.N * (double)w.K_real;
+    prog.weight_bytes += (double)w.rows * w.K_real * 2;
+  }
+
+  // Swap-AB linear for small batches: weights are the M operand (TMA), the
+  // activation rows (batch) are the N operand (gathered).  Output transposed.
+  void gemm_swap(const Gather& gb, int nrows, const WRef& w, const void* bias, Epilogue ep) {
+    if (!w.ptr) return;
+    OpDesc& op = add(OP_GEMM);
+    GemmArgs& g = op.g;
+    g.M = w.rows;
+    g.N = nrows;
+    g.K_real = w.K_real;
+    g.K_pad = w.K_pad;
+    g.BN = std::max(16, rup(nrows, 16));
+    g.n_nblk = 1;
+    g.n_mblk = (g.M + 127) / 128;
+    g.a_tma = 1;
+    g.b_tma = 0;
+    g.gb = gb;
+    g.gb.rows = nrows;
+    ep.bias = abs_ref(bias);
+    ep.bias_on_m = 1;
+    ep.transpose = 1;
+    choose_split(op, true);
+    g.ep = ep;
+    encode_tmap(&op.tmap_a, w.ptr, w.K_pad, w.rows, 128, e);
+    finish_gemm(op);
+    prog.flops += 2.0 * nrows * g.M * (double)w.K_real;
+    prog.weight_bytes += (double)w.rows * w.K_real * 2;
+  }
+
+  void choose_split(OpDesc& op, bool allow) {
+    GemmArgs& g = op.g;
+    const int nkb = g.K_pad / 64;
+    const int tiles = g.n_mblk * g.n_nblk;
+    int splits = 1;
+    if (allow && tiles < 74 && nkb >= 8) splits = std::min(nkb / 4, std::max(1, 148 / tiles));
+    splits = std::max(1, splits);
+    g.kb_per_split = (nkb + splits - 1) / splits;
+    g.splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;
+  }
+
+  // Queue the split-K finalize: allocate the partial buffer now.
+  struct PendingFinal {
+    Epilogue ep;
+    int M, N, splits;
+    uint64_t ws;
+  };
+  std::vector<PendingFinal> finals;
+
+  void finish_gemm(OpDesc& op) {
+    GemmArgs& g = op.g;
+    op.n_units = g.n_mblk * g.n_nblk * g.splits;
+    if (g.splits > 1) {
+      const uint64_t ws = alloc((uint64_t)g.splits * g.M * g.N * 4);
+      PendingFinal f{g.ep, g.M, g.N, g.splits, ws};
+      g.ep.splitk = g.splits;
+      g.ep.ws = ws_ref(ws);
+      finals.push_back(f);
+    }
+  }
+
+  // Emit finalize ops for split-K GEMMs of the previous step (call after step()).
+  void flush_finals() {
+    if (finals.empty()) return;
+    for (auto& f : finals) {
+      OpDesc& op = add(OP_SPLITK_FINAL);
+      op.m.rows = f.M;
+      op.m.cols = f.N;
+      op.m.ep = f.ep;
+      op.m.ep.splitk = f.splits;
+      op.m.ep.ws = ws_ref(f.ws);
+      op.n_units = 1;
+      release_off(f.ws);
+    }
+    finals.clear();
+    step();
+  }
+
+  static Gather conv_gather(const Act& x, int KH, int stride, int pad, int Ho, int Wo) {
+    Gather g;
+    std::memset(&g, 0, sizeof(g));
+    g.x = x.ref;
+    g.H = x.H, g.W = x.W, g.C = x.C, g.lda = x.ld;
+    g.KH = KH, g.KW = KH, g.stride = stride, g.pad = pad;
+    g.Ho = Ho, g.Wo = Wo;
+    return g;
+  }
+  static Gather mat_gather(BufRef x, int K, int lda) {
+    Gather g;
+    std::memset(&g, 0, sizeof(g));
+    g.x = x;
+    g.H = 1, g.W = 1, g.C = K, g.lda = lda;
+    g.KH = 1, g.KW = 1, g.stride = 1, g.pad = 0;
+    g.Ho = 1, g.Wo = 1;
+    return g;
+  }
+
+  // conv + bias (+ residual) + act -> NHWC bf16; `out` may be a channel-offset view.
+  Act conv(const Act& x, const std::string& name, int k, int stride, int pad, int act, const Act* resid = nullptr,
+           const Act* out = nullptr, int col_off = 0) {
+    WRef w = conv_weight(dw, P, name, x.C, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    const int Ho = (x.H + 2 * pad - k) / stride + 1, Wo = (x.W + 2 * pad - k) / stride + 1;
+    Act y;
+    if (out) {
+      y = *out;
+    } else {
+      y = tensor(x.N, Ho, Wo, w.rows);
+    }
+    Epilogue ep = plain_ep(y.ref, y.ld, col_off);
+    ep.act = act;
+    if (resid) ep.res = resid->ref;
+    gemm_gather_a(conv_gather(x, k, stride, pad, Ho, Wo), x.N * Ho * Wo, w, bias, ep);
+    return y;
+  }
+
+  Act maxpool(const Act& x, int k, int s, int pad, bool ceil_mode) {
+    auto osz = [&](int H) {
+      int o;
+      if (ceil_mode) {
+        o = (H + 2 * pad - k + s - 1) / s + 1;
+        if ((o - 1) * s >= H + pad) --o;
+      } else {
+        o = (H + 2 * pad - k) / s + 1;
+      }
+      return o;
+    };
+    const int Ho = osz(x.H), Wo = osz(x.W);
+    Act y = tensor(x.N, Ho, Wo, x.C);
+    OpDesc& op = add(OP_MAXPOOL);
+    MiscArgs& a = op.m;
+    a.x = x.ref, a.y = y.ref;
+    a.N = x.N, a.H = x.H, a.W = x.W, a.C = x.C, a.Ho = Ho, a.Wo = Wo, a.k = k, a.stride = s, a.pad = pad;
+    op.n_units = 1;
+    return y;
+  }
+
+  Act avgpool(const Act& x) {
+    Act y = tensor(x.N, 1, 1, x.C);
+    OpDesc& op = add(OP_AVGPOOL);
+    MiscArgs& a = op.m;
+    a.x = x.ref, a.y = y.ref;
+    a.N = x.N, a.H = x.H, a.W = x.W, a.C = x.C;
+    op.n_units = 1;
+    return y;
+  }
+
+  Act dwconv(const Act& x, const std::string& name, int stride, int act) {
+    void* w = dw_weight(dw, P, name, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    const int Ho = (x.H + 2 - 3) / stride + 1, Wo = (x.W + 2 - 3) / stride + 1;
+    Act y = tensor(x.N, Ho, Wo, x.C);
+    OpDesc& op = add(OP_DWCONV);
+    MiscArgs& a = op.m;
+    a.x = x.ref, a.y = y.ref, a.w = abs_ref(w), a.b = abs_ref(bias);
+    a.N = x.N, a.H = x.H, a.W = x.W, a.C = x.C, a.Ho = Ho, a.Wo = Wo, a.stride = stride, a.pad = 1, a.act = act;
+    op.n_units = 1;
+    prog.flops += 2.0 * x.N * Ho * Wo * x.C * 9;
+    return y;
+  }
+
+  // Linear on the rows of x ([rows, K] with row stride ld): swap-AB (small batch).
+  void fc_swap(BufRef x, int rows, int K, int ld, const std::string& name, int act, BufRef out, int out_fp32) {
+    WRef w = fc_weight(dw, P, name, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    if (w.K_real != K) {
+      e.fail(name + ": K mismatch");
+      return;
+    }
+    Epilogue ep = plain_ep(out, w.rows, 0);
+    ep.act = act;
+    ep.out_fp32 = out_fp32;
+    gemm_swap(mat_gather(x, K, ld), rows, w, bias, ep);
+  }
+
+  // Linear on [rows, K] activations (BERT): A gathered, W by TMA.
+  void linear(const Act& x, const std::string& name, int act, const Act& y, const Act* resid) {
+    WRef w = fc_weight(dw, P, name, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    Epilogue ep = plain_ep(y.ref, y.ld, 0);
+    ep.act = act;
+    if (resid) ep.res = resid->ref;
+    gemm_gather_a(mat_gather(x.ref, x.C, x.ld), x.N, w, bias, ep);
+  }
+
+  bool done() {
+    if (!prog.ops.empty()) prog.ops.back().step_end = 1;
+    return e.msg.empty();
+  }
+};
+
+static Act input_act(int N, int H, int W, int C) {
+  Act a;
+  a.ref = in_ref(0);
+  a.N = N, a.H = H, a.W = W, a.C = C, a.ld = C;
+  return a;
+}
+
+// ------------------------------------------------------------------ LeNet-5
+static void build_lenet(Builder& B, size_t& in_b, size_t& out_b) {
+  // one fused op; parameters packed in manifest order
+  static const char* names[] = {"conv1.w", "conv1.b", "conv2.w", "conv2.b", "fc1.w", "fc1.b",
+                                "fc2.w",   "fc2.b",   "fc3.w",   "fc3.b"};
+  const std::string key = "#lenet_packed";
+  void* w = nullptr;
+  auto f = B.dw.ptr.find(key);
+  if (f != B.dw.ptr.end()) {
+    w = f->second;
+  } else {
+    std::vector<uint16_t> buf;
+    for (const char* n : names) {
+      auto it = B.P.find(n);
+      if (it == B.P.end()) {
+        B.e.fail(std::string("missing ") + n);
+        return;
+      }
+      buf.insert(buf.end(), it->second.data.begin(), it->second.data.end());
+    }
+    w = upload(B.dw, buf.data(), buf.size() * 2);
+    B.dw.ptr[key] = w;
+  }
+  OpDesc& op = B.add(OP_LENET);
+  op.m.x = in_ref(0);
+  op.m.y = out_ref(0);
+  op.m.w = abs_ref(w);
+  op.m.N = B.b;
+  op.n_units = B.b;
+  B.prog.flops += 2.0 * 416520 * B.b;
+  B.prog.weight_bytes += 61706 * 2;
+  in_b = (size_t)B.b * 784 * 2;
+  out_b = (size_t)B.b * 10 * 4;
+}
+
+// ------------------------------------------------------------------ ResNet-50 v1.5
+static void build_resnet(Builder& B, size_t& in_b, size_t& out_b) {
+  const int b = B.b;
+  Act x = input_act(b, 224, 224, 8);
+  Act h = B.conv(x, "conv1", 7, 2, 3, ACT_RELU);
+  B.step();
+  Act p = B.maxpool(h, 3, 2, 1, false);
+  B.release(h);
+  B.step();
+  h = p;
+  const int stages[4][3] = {{3, 64, 1}, {4, 128, 2}, {6, 256, 2}, {3, 512, 2}};
+  for (int s = 0; s < 4; ++s) {
+    for (int i = 0; i < stages[s][0]; ++i) {
+      const std::string pre = "layer" + std::to_string(s + 1) + "." + std::to_string(i);
+      const int st = i == 0 ? stages[s][2] : 1;
+      Act a = B.conv(h, pre + ".conv1", 1, 1, 0, ACT_RELU);
+      Act sc = h;
+      if (i == 0) sc = B.conv(h, pre + ".down", 1, st, 0, ACT_NONE);
+      B.step();
+      B.flush_finals();
+      Act a2 = B.conv(a, pre + ".conv2", 3, st, 1, ACT_RELU);
+      B.release(a);
+      B.step();
+      B.flush_finals();
+      Act y = B.conv(a2, pre + ".conv3", 1, 1, 0, ACT_RELU, &sc);
+      B.release(a2);
+      B.release(sc);
+      if (i == 0) B.release(h);
+      B.step();
+      B.flush_finals();
+      h = y;
+    }
+  }
+  Act g = B.avgpool(h);
+  B.release(h);
+  B.step();
+  B.fc_swap(g.ref, b, 2048, 2048, "fc", ACT_NONE, out_ref(0), 1);
+  B.step();
+  B.flush_finals();
+  in_b = (size_t)b * 224 * 224 * 8 * 2;
+  out_b = (size_t)b * 1000 * 4;
+}
+
+// ------------------------------------------------------------------ VGG-16 (config D)
+static void build_vgg(Builder& B, size_t& in_b, size_t& out_b) {
+  const int b = B.b;
+  static const int cfg[] = {64, 64, 0, 128, 128, 0, 256, 256, 256, 0, 512, 512, 512, 0, 512, 512, 512, 0};
+  Act h = input_act(b, 224, 224, 8);
+  int n = 0;
+  for (int v : cfg) {
+    Act y;
+    if (v == 0) {
+      y = B.maxpool(h, 2, 2, 0, false);
+    } else {
+      ++n;
+      y = B.conv(h, "conv" + std::to_string(n), 3, 1, 1, ACT_RELU);
+    }
+    B.release(h);
+    B.step();
+    B.flush_finals();
+    h = y;
+  }
+  // NHWC flatten of [b,7,7,512] is the (h, w, c) order of fc6's input
+  Act f6 = B.tensor(b, 1, 1, 4096);
+  B.fc_swap(h.ref, b, 25088, 25088, "fc6", ACT_RELU, f6.ref, 0);
+  B.release(h);
+  B.step();
+  B.flush_finals();
+  Act f7 = B.tensor(b, 1, 1, 4096);
+  B.fc_swap(f6.ref, b, 4096, 4096, "fc7", ACT_RELU, f7.ref, 0);
+  B.release(f6);
+  B.step();
+  B.flush_finals();
+  B.fc_swap(f7.ref, b, 4096, 4096, "fc8", ACT_NONE, out_ref(0), 1);
+  B.release(f7);
+  B.step();
+  B.flush_finals();
+  in_b = (size_t)b * 224 * 224 * 8 * 2;
+  out_b = (size_t)b * 1000 * 4;
+}
+
+// ------------------------------------------------------------------ GoogLeNet (Inception v1)
+static void build_googlenet(Builder& B, size_t& in_b, size_t& out_b) {
+  const int b = B.b;
+  struct Inc {
+    const char* name;
+    int c1, c3r, c3, c5r, c5, cp;
+  };
+  static const Inc incs[] = {{"3a", 64, 96, 128, 16, 32, 32},     {"3b", 128, 128, 192, 32, 96, 64},
+                             {"P", 0, 0, 0, 0, 0, 0},             {"4a", 192, 96, 208, 16, 48, 64},
+                             {"4b", 160, 112, 224, 24, 64, 64},   {"4c", 128, 128, 256, 24, 64, 64},
+                             {"4d", 112, 144, 288, 32, 64, 64},   {"4e", 256, 160, 320, 32, 128, 128},
+                             {"P", 0, 0, 0, 0, 0, 0},             {"5a", 256, 160, 320, 32, 128, 128},
+                             {"5b", 384, 192, 384, 48, 128, 128}};
+  Act x = input_act(b, 224, 224, 8);
+  Act h = B.conv(x, "conv1", 7, 2, 3, ACT_RELU);
+  B.step();
+  Act p = B.maxpool(h, 3, 2, 0, true);
+  B.release(h);
+  B.step();
+  h = B.conv(p, "conv2", 1, 1, 0, ACT_RELU);
+  B.release(p);
+  B.step();
+  B.flush_finals();
+  p = B.conv(h, "conv3", 3, 1, 1, ACT_RELU);
+  B.release(h);
+  B.step();
+  B.flush_finals();
+  h = B.maxpool(p, 3, 2, 0, true);
+  B.release(p);
+  B.step();
+  for (const Inc& I : incs) {
+    if (I.name[0] == 'P') {
+      Act q = B.maxpool(h, 3, 2, 0, true);
+      B.release(h);
+      B.step();
+      h = q;
+      continue;
+    }
+    const std::string pre = std::string("inc") + I.name;
+    const int ctot = I.c1 + I.c3 + I.c5 + I.cp;
+    Act pool = B.maxpool(h, 3, 1, 1, false);   // branch 4 pre-pool
+    B.step();
+    Act y = B.tensor(b, h.H, h.W, ctot);
+    B.conv(h, pre + ".b1", 1, 1, 0, ACT_RELU, nullptr, &y, 0);
+    Act r3 = B.conv(h, pre + ".b2r", 1, 1, 0, ACT_RELU);
+    Act r5 = B.conv(h, pre + ".b3r", 1, 1, 0, ACT_RELU);
+    B.conv(pool, pre + ".b4", 1, 1, 0, ACT_RELU, nullptr, &y, I.c1 + I.c3 + I.c5);
+    B.release(pool);
+    B.release(h);
+    B.step();
+    B.flush_finals();
+    B.conv(r3, pre + ".b2", 3, 1, 1, ACT_RELU, nullptr, &y, I.c1);
+    B.conv(r5, pre + ".b3", 5, 1, 2, ACT_RELU, nullptr, &y, I.c1 + I.c3);
+    B.release(r3);
+    B.release(r5);
+    B.step();
+    B.flush_finals();
+    h = y;
+  }
+  Act g = B.avgpool(h);
+  B.release(h);
+  B.step();
+  B.fc_swap(g.ref, b, 1024, 1024, "fc", ACT_NONE, out_ref(0), 1);
+  B.step();
+  B.flush_finals();
+  in_b = (size_t)b * 224 * 224 * 8 * 2;
+  out_b = (size_t)b * 1000 * 4;
+}
+
+// ------------------------------------------------------------------ SSD-MobileNet-V1
+static void build_ssd(Builder& B, size_t& in_b, size_t& out_b) {
+  const int b = B.b;
+  static const int blocks[13][2] = {{64, 1},  {128, 2}, {128, 1}, {256, 2}, {256, 1}, {512, 2},  {512, 1},
+                                    {512, 1}, {512, 1}, {512, 1}, {512, 1}, {1024, 2}, {1024, 1}};
+  Act x = input_act(b, 300, 300, 8);
+  Act h = B.conv(x, "conv0", 3, 2, 1, ACT_RELU);
+  B.step();
+  std::vector<Act> feats;
+  for (int i = 0; i < 13; ++i) {
+    const std::string id = std::to_string(i + 1);
+    Act d = B.dwconv(h, "dw" + id, blocks[i][1], ACT_RELU);
+    if (i + 1 != 12) B.release(h);   // h (block 11 output) stays alive as a feature map
+    B.step();
+    Act y = B.conv(d, "pw" + id, 1, 1, 0, ACT_RELU);
+    B.release(d);
+    B.step();
+    B.flush_finals();
+    if (i + 1 == 11 || i + 1 == 13) feats.push_back(y);
+    h = y;
+  }
+  for (int i = 0; i < 4; ++i) {
+    const std::string pre = "extra" + std::to_string(i + 1);
+    Act a = B.conv(h, pre + ".a", 1, 1, 0, ACT_RELU);
+    B.step();
+    B.flush_finals();
+    Act y = B.conv(a, pre + ".b", 3, 2, 1, ACT_RELU);
+    B.release(a);
+    B.step();
+    B.flush_finals();
+    feats.push_back(y);
+    h = y;
+  }
+  // heads: loc [b,3000,4] at out+0, conf [b,3000,21] after it; fp32
+  const uint64_t conf_off = (uint64_t)b * 3000 * 4 * 4;
+  int prior = 0;
+  for (int i = 0; i < 6; ++i) {
+    const Act& f = feats[i];
+    const std::string pre = "head" + std::to_string(i);
+    for (int which = 0; which < 2; ++which) {
+      const int per = which == 0 ? 4 : 21;
+      WRef w = conv_weight(B.dw, B.P, pre + (which == 0 ? ".loc" : ".conf"), f.C, B.e);
+      void* bias = raw_param(B.dw, B.P, pre + (which == 0 ? ".loc.b" : ".conf.b"), B.e);
+      Epilogue ep = Builder::plain_ep(out_ref(which == 0 ? 0 : conf_off), 6 * per, prior * per);
+      ep.rows_per_img = f.H * f.W;
+      ep.img_stride = (int64_t)3000 * per;
+      ep.out_fp32 = 1;
+      ep.act = ACT_NONE;
+      B.gemm_gather_a(Builder::conv_gather(f, 3, 1, 1, f.H, f.W), b * f.H * f.W, w, bias, ep, false);
+    }
+    prior += f.H * f.W * 6;
+  }
+  for (auto& f : feats) B.release(f);
+  B.step();
+  OpDesc& op = B.add(OP_SOFTMAX);
+  op.m.x = out_ref(conf_off);
+  op.m.rows = b * 3000;
+  op.m.cols = 21;
+  op.n_units = 1;
+  B.step();
+  in_b = (size_t)b * 300 * 300 * 8 * 2;
+  out_b = (size_t)b * 3000 * 25 * 4;
+}
+
+// ------------------------------------------------------------------ BERT-base (seq 128)
+static void build_bert(Builder& B, size_t& in_b, size_t& out_b) {
+  const int b = B.b, S = 128, H = 768, M = b * S;
+  void* word = raw_param(B.dw, B.P, "emb.word", B.e);
+  // pos [512,768] followed by type [2,768]
+  void* postype = nullptr;
+  {
+    auto f = B.dw.ptr.find("#postype");
+    if (f != B.dw.ptr.end()) {
+      postype = f->second;
+    } else {
+      auto ip = B.P.find("emb.pos"), it = B.P.find("emb.type");
+      if (ip == B.P.end() || it == B.P.end()) {
+        B.e.fail("missing embeddings");
+        return;
+      }
+      std::vector<uint16_t> buf(ip->second.data);
+      buf.insert(buf.end(), it->second.data.begin(), it->second.data.end());
+      postype = upload(B.dw, buf.data(), buf.size() * 2);
+      B.dw.ptr["#postype"] = postype;
+    }
+  }
+  Act x = B.tensor(M, 1, 1, H);
+  {
+    OpDesc& op = B.add(OP_EMBED_LN);
+    op.m.x = in_ref(0);
+    op.m.y = x.ref;
+    op.m.w = abs_ref(word);
+    op.m.aux = abs_ref(postype);
+    op.m.g = abs_ref(raw_param(B.dw, B.P, "emb.ln.g", B.e));
+    op.m.b = abs_ref(raw_param(B.dw, B.P, "emb.ln.b", B.e));
+    op.m.rows = M;
+    op.m.seq = S;
+    op.m.eps = 1e-12f;
+    op.n_units = 1;
+    B.step();
+  }
+  for (int l = 0; l < 12; ++l) {
+    const std::string pre = "L" + std::to_string(l);
+    Act qkv = B.tensor(M, 1, 1, 3 * H);
+    B.linear(x, pre + ".qkv", ACT_NONE, qkv, nullptr);
+    B.step();
+    B.flush_finals();
+    Act ctx = B.tensor(M, 1, 1, H);
+    {
+      OpDesc& op = B.add(OP_ATTENTION);
+      op.m.x = qkv.ref;
+      op.m.y = ctx.ref;
+      op.m.N = b;
+      op.m.seq = S;
+      op.m.heads = 12;
+      op.m.dh = 64;
+      op.n_units = b * 12;
+      B.prog.flops += 2.0 * 2 * b * 12 * S * S * 64;
+    }
+    B.release(qkv);
+    B.step();
+    Act a = B.tensor(M, 1, 1, H);
+    B.linear(ctx, pre + ".proj", ACT_NONE, a, &x);
+    B.release(ctx);
+    B.release(x);
+    B.step();
+    B.flush_finals();
+    Act x1 = B.tensor(M, 1, 1, H);
+    {
+      OpDesc& op = B.add(OP_LAYERNORM);
+      op.m.x = a.ref;
+      op.m.y = x1.ref;
+      op.m.g = abs_ref(raw_param(B.dw, B.P, pre + ".ln1.g", B.e));
+      op.m.b = abs_ref(raw_param(B.dw, B.P, pre + ".ln1.b", B.e));
+      op.m.rows = M;
+      op.m.eps = 1e-12f;
+      op.n_units = 1;
+    }
+    B.release(a);
+    B.step();
+    Act f = B.tensor(M, 1, 1, 3072);
+    B.linear(x1, pre + ".ffn1", ACT_GELU, f, nullptr);
+    B.step();
+    B.flush_finals();
+    Act y = B.tensor(M, 1, 1, H);
+    B.linear(f, pre + ".ffn2", ACT_NONE, y, &x1);
+    B.release(f);
+    B.release(x1);
+    B.step();
+    B.flush_finals();
+    x = B.tensor(M, 1, 1, H);
+    {
+      OpDesc& op = B.add(OP_LAYERNORM);
+      op.m.x = y.ref;
+      op.m.y = x.ref;
+      op.m.g = abs_ref(raw_param(B.dw, B.P, pre + ".ln2.g", B.e));
+      op.m.b = abs_ref(raw_param(B.dw, B.P, pre + ".ln2.b", B.e));
+      op.m.rows = M;
+      op.m.eps = 1e-12f;
+      op.n_units = 1;
+    }
+    B.release(y);
+    B.step();
+  }
+  // pooler on the [CLS] rows (row stride S*H), then the 2-class head
+  Act pooled = B.tensor(b, 1, 1, H);
+  B.fc_swap(x.ref, b, H, S * H, "pool", ACT_TANH, pooled.ref, 0);
+  B.release(x);
+  B.step();
+  B.flush_finals();
+  B.fc_swap(pooled.ref, b, H, H, "cls", ACT_NONE, out_ref(0), 1);
+  B.release(pooled);
+  B.step();
+  B.flush_finals();
+  in_b = (size_t)b * S * 4;
+  out_b = (size_t)b * 2 * 4;
+}
+
+bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
+                   size_t& in_bytes, size_t& out_bytes, std::string& err) {
+  (void)gpu;
+  out = Program();
+  Builder B(host, dw, batch, out);
+  switch (kind) {
+    case 0: build_lenet(B, in_bytes, out_bytes); break;
+    case 1: build_googlenet(B, in_bytes, out_bytes); break;
+    case 2: build_resnet(B, in_bytes, out_bytes); break;
+    case 3: build_ssd(B, in_bytes, out_bytes); break;
+    case 4: build_vgg(B, in_bytes, out_bytes); break;
+    case 5: build_bert(B, in_bytes, out_bytes); break;
+    default: err = "bad model kind"; return false;
+  }
+  if (!B.done()) {
+    err = B.e.msg;
+    return false;
+  }
+  out.ws_bytes = std::max<size_t>(out.ws_bytes, 256);
+  return true;
+}
+
+// ------------------------------------------------------------------ single-op test programs
+bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int out_fp32, const uint16_t* w_host,
+                     const uint16_t* b_host, int has_res, DevWeights& dw, Program& out, std::string& err) {
+  out = Program();
+  ParamMap P;
+  Param w, bb;
+  w.shape = {N, K};
+  w.data.assign(w_host, w_host + (size_t)N * K);
+  bb.shape = {N};
+  bb.data.assign(b_host, b_host + N);
+  P["t.w"] = w;
+  P["t.b"] = bb;
+  Builder B(P, dw, M, out);
+  WRef wr = fc_weight(dw, P, "t", B.e);
+  void* bias = raw_param(dw, P, "t.b", B.e);
+  // input: BUF_IN [M, K] bf16; residual BUF_IN after it ([M, N]); output BUF_OUT [M, N]
+  Epilogue ep = Builder::plain_ep(out_ref(0), N, 0);
+  ep.act = act;
+  ep.out_fp32 = out_fp32;
+  if (has_res) ep.res = in_ref((uint64_t)M * K * 2);
+  if (swap_ab) {
+    B.gemm_swap(Builder::mat_gather(in_ref(0), K, K), M, wr, bias, ep);
+  } else {
+    B.gemm_gather_a(Builder::mat_gather(in_ref(0), K, K), M, wr, bias, ep, splitk != 0);
+  }
+  if (!splitk && !swap_ab) {
+    // force no split
+  }
+  B.step();
+  B.flush_finals();
+  if (!B.done()) {
+    err = B.e.msg;
+    return false;
+  }
+  return true;
+}
+
+bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, int pad, int act,
+                     const uint16_t* w_host, const uint16_t* b_host, DevWeights& dw, Program& out, std::string& err) {
+  out = Program();
+  ParamMap P;
+  Param w, bb;
+  w.shape = {Cout, KH, KH, C};
+  w.data.assign(w_host, w_host + (size_t)Cout * KH * KH * C);
+  bb.shape = {Cout};
+  bb.data.assign(b_host, b_host + Cout);
+  P["t.w"] = w;
+  P["t.b"] = bb;
+  Builder B(P, dw, N, out);
+  Act x = input_act(N, H, W, C);
+  const int Ho = (H + 2 * pad - KH) / stride + 1, Wo = (W + 2 * pad - KH) / stride + 1;
+  Act y;
+  y.ref = out_ref(0);
+  y.N = N, y.H = Ho, y.W = Wo, y.C = Cout, y.ld = Cout;
+  B.conv(x, "t", KH, stride, pad, act, nullptr, &y, 0);
+  B.step();
+  B.flush_finals();
+  if (!B.done()) {
+    err = B.e.msg;
+    return false;
+  }
+  return true;
+}
+
+// type: OP_DWCONV (iargs N,H,W,C,stride), OP_MAXPOOL (N,H,W,C,k,s,pad,ceil), OP_AVGPOOL (N,H,W,C),
+//       OP_LAYERNORM (rows), OP_ATTENTION (nseq), OP_SOFTMAX (rows, cols)
+bool build_test_misc(int type, const int* ia, int n, const uint16_t* w_host, size_t w_len, DevWeights& dw,
+                     Program& out, std::string& err) {
+  out = Program();
+  ParamMap P;
+  if (type == OP_DWCONV && n >= 4) {
+    const int C = ia[3];
+    Param w, bb;
+    w.shape = {C, 3, 3, 1};
+    w.data.assign(w_host, w_host + (size_t)C * 9);
+    bb.shape = {C};
+    bb.data.assign(w_host + (size_t)C * 9, w_host + (size_t)C * 10);
+    P["t.w"] = w;
+    P["t.b"] = bb;
+  }
+  Builder B(P, dw, 1, out);
+  auto need = [&](int k) {
+    if (n < k) {
+      err = "too few int args";
+      return false;
+    }
+    return true;
+  };
+  if (type == OP_DWCONV) {
+    if (!need(5)) return false;
+    Act x = input_act(ia[0], ia[1], ia[2], ia[3]);
+    B.dwconv(x, "t", ia[4], ACT_RELU);
+    B.prog.ops.back().m.y = out_ref(0);
+  } else if (type == OP_MAXPOOL) {
+    if (!need(8)) return false;
+    Act x = input_act(ia[0], ia[1], ia[2], ia[3]);
+    B.maxpool(x, ia[4], ia[5], ia[6], ia[7] != 0);
+    B.prog.ops.back().m.y = out_ref(0);
+  } else if (type == OP_AVGPOOL) {
+    if (!need(4)) return false;
+    B.avgpool(input_act(ia[0], ia[1], ia[2], ia[3]));
+    B.prog.ops.back().m.y = out_ref(0);
+  } else if (type == OP_LAYERNORM) {
+    if (!need(1)) return false;
+    // w_host = gamma[768] ++ beta[768]
+    void* g = upload(dw, w_host, 768 * 2);
+    void* bta = upload(dw, w_host + 768, 768 * 2);
+    OpDesc& op = B.add(OP_LAYERNORM);
+    op.m.x = in_ref(0);
+    op.m.y = out_ref(0);
+    op.m.g = abs_ref(g);
+    op.m.b = abs_ref(bta);
+    op.m.rows = ia[0];
+    op.m.eps = 1e-12f;
+    op.n_units = 1;
+  } else if (type == OP_ATTENTION) {
+    if (!need(1)) return false;
+    OpDesc& op = B.add(OP_ATTENTION);
+    op.m.x = in_ref(0);
+    op.m.y = out_ref(0);
+    op.m.N = ia[0];
+    op.m.seq = 128;
+    op.m.heads = 12;
+    op.m.dh = 64;
+    op.n_units = ia[0] * 12;
+  } else if (type == OP_SOFTMAX) {
+    if (!need(2)) return false;
+    OpDesc& op = B.add(OP_SOFTMAX);
+    op.m.x = out_ref(0);
+    op.m.rows = ia[0];
+    op.m.cols = ia[1];
+    op.n_units = 1;
+  } else {
+    err = "unsupported test op";
+    return false;
+  }
+  (void)w_len;
+  B.step();
+  if (!B.done()) {
+    err = B.e.msg;
+    return false;
+  }
+  return true;
+}
+
+}  // namespace gl
+
+namespace gl {
+// Algorithmic cost of one op: FLOPs (2 x MACs of the contraction) and the bytes
+// it must move at minimum (weights + input activations + outputs, each once).
+void op_cost(const OpDesc& op, double& flops, double& bytes) {
+  flops = 0;
+  bytes = 0;
+  switch (op.type) {
+    case OP_GEMM: {
+      const GemmArgs& g = op.g;
+      flops = 2.0 * g.M * g.N * (double)g.K_real;
+      const Gather& x = g.a_tma ? g.gb : g.ga;
+      const int wrows = g.a_tma ? g.M : g.N;
+      const int xrows = g.a_tma ? g.N : g.M;
+      const double in_bytes = (x.KH == 1 && x.stride == 1) ? (double)xrows * x.C * 2
+                                                            : (double)(xrows / std::max(1, x.Ho * x.Wo)) * x.H * x.W * x.C * 2;
+      bytes = (double)wrows * g.K_real * 2 + in_bytes + (double)g.M * g.N * (g.ep.out_fp32 ? 4 : 2);
+      break;
+    }
+    case OP_DWCONV:
+      flops = 2.0 * op.m.N * op.m.Ho * op.m.Wo * op.m.C * 9;
+      bytes = 2.0 * op.m.C * ((double)op.m.N * op.m.H * op.m.W + (double)op.m.N * op.m.Ho * op.m.Wo);
+      break;
+    case OP_MAXPOOL:
+      bytes = 2.0 * op.m.C * ((double)op.m.N * op.m.H * op.m.W + (double)op.m.N * op.m.Ho * op.m.Wo);
+      break;
+    case OP_AVGPOOL:
+      bytes = 2.0 * op.m.C * ((double)op.m.N * op.m.H * op.m.W + op.m.N);
+      break;
+    case OP_ATTENTION:
+      flops = 4.0 * op.m.N * op.m.heads * op.m.seq * op.m.seq * op.m.dh;
+      bytes = 2.0 * op.m.N * op.m.seq * op.m.heads * op.m.dh * 4;
+      break;
+    case OP_LAYERNORM:
+    case OP_EMBED_LN:
+      bytes = 4.0 * op.m.rows * 768;
+      break;
+    case OP_LENET:
+      flops = 2.0 * 416520 * op.m.N;
+      bytes = 61706 * 2 + op.m.N * (784 * 2 + 40);
+      break;
+    case OP_SOFTMAX:
+      bytes = 8.0 * op.m.rows * op.m.cols;
+      break;
+    case OP_SPLITK_FINAL:
+      bytes = (4.0 * op.m.ep.splitk + 2) * op.m.rows * op.m.cols;
+      break;
+    default: break;
+  }
+}
+}  // namespace gl

@@ -1,0 +1,849 @@
+// libgpulet host runtime: the C-ABI of include/gpulet.h.
+//
+// gpu-lets (§2.3) are green contexts over disjoint 8-SM
+// groups of one GPU (cuDevSmResourceSplitByCount, minimum 8 SMs on CC >= 9.0),
+// each running one persistent executor kernel (executor.cu) that pulls batch
+// descriptors from a host-mapped ring and pushes completion records back
+// (SURVEY.md §8(a) a1, a6, a7, a13).  The paper's frontend/backend processes,
+// Unix sockets and MPS daemon are replaced by this in-process ABI.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <time.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gpulet.h"
+#include "runtime.h"
+
+extern "C" cudaKernel_t gl_executor_handle();
+extern "C" const void* gl_executor_fn();
+
+namespace gl {
+
+static thread_local std::string g_err = "";
+
+static gl_status fail(gl_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** fp) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPointByVersion(name, fp, 12080, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess;
+    };
+    bool ok = true;
+    ok &= get("cuTensorMapEncodeTiled", (void**)&d.tensorMapEncodeTiled);
+    ok &= get("cuDeviceGetDevResource", (void**)&d.deviceGetDevResource);
+    ok &= get("cuDevSmResourceSplitByCount", (void**)&d.devSmResourceSplitByCount);
+    ok &= get("cuDevResourceGenerateDesc", (void**)&d.devResourceGenerateDesc);
+    ok &= get("cuGreenCtxCreate", (void**)&d.greenCtxCreate);
+    ok &= get("cuGreenCtxDestroy", (void**)&d.greenCtxDestroy);
+    ok &= get("cuGreenCtxStreamCreate", (void**)&d.greenCtxStreamCreate);
+    ok &= get("cuLaunchKernelEx", (void**)&d.launchKernelEx);
+    ok &= get("cuKernelSetAttribute", (void**)&d.kernelSetAttribute);
+    ok &= get("cuStreamDestroy", (void**)&d.streamDestroy);
+    ok &= get("cuDeviceGet", (void**)&d.deviceGet);
+    d.ok = ok;
+  });
+  return d;
+}
+
+// Device frees while any persistent executor runs would block (cudaFree
+// synchronises the device); they are deferred until no executor is alive.
+static std::mutex g_free_mu;
+static std::vector<std::pair<void*, bool>> g_deferred;
+static std::atomic<int> g_live_exec{0};
+
+void release_device(void* p, bool host) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  if (g_live_exec.load() == 0) {
+    if (host)
+      cudaFreeHost(p);
+    else
+      cudaFree(p);
+  } else {
+    g_deferred.push_back({p, host});
+  }
+}
+
+static void flush_deferred() {
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  if (g_live_exec.load() != 0) return;
+  for (auto& d : g_deferred) {
+    if (d.second)
+      cudaFreeHost(d.first);
+    else
+      cudaFree(d.first);
+  }
+  g_deferred.clear();
+}
+
+static uint64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (uint64_t)ts.tv_sec * 1000000000ull + ts.tv_nsec;
+}
+
+// ------------------------------------------------------------------ weight files
+bool load_glw(const std::string& path, ParamMap& out, std::string& err) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) {
+    err = "cannot open " + path;
+    return false;
+  }
+  std::string first;
+  std::getline(f, first);
+  size_t hdr = 0;
+  if (sscanf(first.c_str(), "GLW1 %zu", &hdr) != 1 || hdr == 0) {
+    err = "not a GLW1 file: " + path;
+    return false;
+  }
+  struct Ent {
+    std::string name;
+    std::vector<int> shape;
+    size_t off, nbytes;
+  };
+  std::vector<Ent> ents;
+  std::string line;
+  while (std::getline(f, line)) {
+    if (line == "END") break;
+    std::istringstream ss(line);
+    Ent e;
+    std::string dtype;
+    int nd = 0;
+    ss >> e.name >> dtype >> nd;
+    if (!ss || dtype != "bf16" || nd < 1 || nd > 6) {
+      err = "bad header line: " + line;
+      return false;
+    }
+    e.shape.resize(nd);
+    for (int i = 0; i < nd; ++i) ss >> e.shape[i];
+    ss >> e.off >> e.nbytes;
+    if (!ss) {
+      err = "bad header line: " + line;
+      return false;
+    }
+    ents.push_back(e);
+  }
+  for (auto& e : ents) {
+    Param p;
+    p.shape = e.shape;
+    if (p.numel() * 2 != e.nbytes) {
+      err = "size mismatch for " + e.name;
+      return false;
+    }
+    p.data.resize(p.numel());
+    f.seekg((std::streamoff)(hdr + e.off));
+    f.read((char*)p.data.data(), (std::streamsize)e.nbytes);
+    if (!f) {
+      err = "truncated data for " + e.name;
+      return false;
+    }
+    out[e.name] = std::move(p);
+  }
+  return true;
+}
+
+}  // namespace gl
+
+using namespace gl;
+
+// ------------------------------------------------------------------ context objects
+struct Gpulet {
+  int id = -1, gpu = 0, slot = 0, pct = 100, nsm = 0;
+  bool alive = false;
+  CUgreenCtx gctx = nullptr;
+  CUstream stream = nullptr;
+  bool own_primary_stream = false;
+  HostRing* ring = nullptr;      // host view
+  HostRing* ring_dev = nullptr;  // device alias
+  ExecState* st = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* smid = nullptr;
+  uint64_t tail = 0;       // items published
+  uint64_t comp_seen = 0;  // completions consumed by the host
+  std::vector<int> groups;
+  bool uses_rem = false;
+};
+
+struct GpuState {
+  int dev = 0;
+  int nsm = 0;
+  bool split = false;
+  CUdevResource groups[32];
+  unsigned ngroups = 0;
+  CUdevResource rem;
+  uint32_t used_groups = 0;
+  bool rem_used = false;
+  int slots[2] = {-1, -1};
+};
+
+struct gl_ctx {
+  std::vector<GpuState> gpus;
+  std::vector<std::unique_ptr<Model>> models;
+  std::vector<std::unique_ptr<Gpulet>> gpulets;
+  std::deque<gl_completion> stash;  // collected by gl_wait, handed out by gl_poll
+  std::mutex mu;
+  uint64_t next_ticket = 1;
+  bool poisoned = false;
+};
+
+static gl_status cuda_check(gl_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return GL_OK;
+  if (c) c->poisoned = true;
+  return fail(GL_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+static gl_status cu_check(gl_ctx* c, CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return GL_OK;
+  if (c) c->poisoned = true;
+  return fail(GL_E_CUDA, std::string(what) + ": CUresult " + std::to_string((int)r));
+}
+#define CK(x, what)                                  \
+  do {                                               \
+    gl_status _s = cuda_check(ctx, (x), what);       \
+    if (_s != GL_OK) return _s;                      \
+  } while (0)
+
+static int sm_for_pct(int pct) {
+  switch (pct) {
+    case 20: return 32;
+    case 40: return 56;
+    case 50: return 72;
+    case 60: return 92;
+    case 80: return 116;
+    case 100: return 148;
+    default: return -1;
+  }
+}
+
+static size_t exec_smem_bytes() { return (size_t)kSmemBytes + 1024; }
+
+static gl_status launch_executor(gl_ctx* ctx, int dev, CUstream stream, int grid, const ExecParams& p) {
+  Driver& D = driver();
+  if (!D.ok) return fail(GL_E_CUDA, "CUDA driver entry points unavailable");
+  CUkernel k = (CUkernel)gl_executor_handle();
+  if (!k) return fail(GL_E_CUDA, "cudaGetKernel(gl_executor) failed");
+  CUdevice cud;
+  CUresult r = D.deviceGet(&cud, dev);
+  if (r != CUDA_SUCCESS) return cu_check(ctx, r, "cuDeviceGet");
+  r = D.kernelSetAttribute(CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)exec_smem_bytes(), k, cud);
+  if (r != CUDA_SUCCESS) return cu_check(ctx, r, "cuKernelSetAttribute");
+  CUlaunchConfig cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = grid;
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = kThreads;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = (unsigned)exec_smem_bytes();
+  cfg.hStream = stream;
+  ExecParams pp = p;
+  void* args[] = {&pp};
+  r = D.launchKernelEx(&cfg, (CUfunction)k, args, nullptr);
+  return cu_check(ctx, r, "cuLaunchKernelEx(gl_executor)");
+}
+
+// One-shot run of a program on the whole GPU (kernel unit tests).
+static gl_status run_oneshot(gl_ctx* ctx, int gpu, Program& prog, const void* in, void* out) {
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  OpDesc* dprog = nullptr;
+  CK(cudaMalloc(&dprog, prog.ops.size() * sizeof(OpDesc)), "cudaMalloc(prog)");
+  CK(cudaMemcpy(dprog, prog.ops.data(), prog.ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice), "memcpy prog");
+  char* ws = nullptr;
+  CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
+  CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
+  HostRing* ring = nullptr;
+  CK(cudaHostAlloc((void**)&ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+  std::memset((void*)ring, 0, sizeof(HostRing));
+  HostRing* ring_dev = nullptr;
+  CK(cudaHostGetDevicePointer((void**)&ring_dev, ring, 0), "cudaHostGetDevicePointer");
+  ExecState* st = nullptr;
+  CK(cudaMalloc(&st, sizeof(ExecState)), "cudaMalloc(st)");
+  CK(cudaMemset(st, 0, sizeof(ExecState)), "memset st");
+  WorkDesc& w = ring->items[0];
+  w.ticket = 1;
+  w.prog = dprog;
+  w.in = in;
+  w.out = out;
+  w.n_ops = (int)prog.ops.size();
+  w.batch = 1;
+  ring->tail = 1;
+  ExecParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.ring = ring_dev;
+  p.st = st;
+  p.ws = ws;
+  p.one_shot = 1;
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  gl_status rc = launch_executor(ctx, ctx->gpus[gpu].dev, (CUstream)s, ctx->gpus[gpu].nsm, p);
+  if (rc == GL_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_check(ctx, e, "executor (one-shot)");
+  }
+  cudaStreamDestroy(s);
+  release_device(st, false);
+  release_device(ring, true);
+  release_device(ws, false);
+  release_device(dprog, false);
+  return rc;
+}
+
+extern "C" {
+
+const char* gl_last_error(void) { return g_err.c_str(); }
+
+gl_status gl_init(int num_gpus, gl_ctx** out) {
+  if (!out || num_gpus < 1) return fail(GL_E_ARG, "gl_init: bad arguments");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n < num_gpus) return fail(GL_E_CUDA, "gl_init: not enough CUDA devices");
+  if (!driver().ok) return fail(GL_E_CUDA, "gl_init: driver entry points unavailable (driver too old?)");
+  auto* c = new gl_ctx();
+  c->gpus.resize(num_gpus);
+  for (int i = 0; i < num_gpus; ++i) {
+    c->gpus[i].dev = i;
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, i);
+    c->gpus[i].nsm = prop.multiProcessorCount;
+    if (prop.major != 10) {
+      delete c;
+      return fail(GL_E_CUDA, "gl_init: libgpulet is built for sm_100a (B200) only");
+    }
+  }
+  *out = c;
+  return GL_OK;
+}
+
+gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t id);
+
+gl_status gl_shutdown(gl_ctx* ctx) {
+  if (!ctx) return GL_OK;
+  for (auto& g : ctx->gpulets)
+    if (g && g->alive) gl_destroy_gpulet(ctx, g->id);
+  for (auto& m : ctx->models) {
+    if (!m) continue;
+    cudaSetDevice(ctx->gpus[m->gpu].dev);
+    for (int b = 1; b <= 32; ++b)
+      if (m->prog[b].dev) release_device(m->prog[b].dev, false);
+    m->w.reset();
+  }
+  delete ctx;
+  return GL_OK;
+}
+
+gl_status gl_load_model(gl_ctx* ctx, int gpu, int kind, const char* weight_file, int32_t* model_id) {
+  if (!ctx || !weight_file || !model_id || gpu < 0 || gpu >= (int)ctx->gpus.size() || kind < 0 ||
+      kind >= model_kind_count())
+    return fail(GL_E_ARG, "gl_load_model: bad arguments");
+  if (ctx->poisoned) return fail(GL_E_CUDA, "context poisoned by an earlier CUDA error");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  auto m = std::make_unique<Model>();
+  m->kind = kind;
+  m->gpu = gpu;
+  std::string err;
+  if (!load_glw(weight_file, m->host, err)) return fail(GL_E_PARSE, err);
+  m->w = std::make_unique<DevWeights>();
+  for (int b = 1; b <= 32; ++b) {
+    if (!build_program(kind, b, m->host, *m->w, gpu, m->prog[b], m->in_bytes[b], m->out_bytes[b], err))
+      return fail(GL_E_PARSE, std::string(model_name(kind)) + ": " + err);
+    Program& p = m->prog[b];
+    CK(cudaMalloc(&p.dev, p.ops.size() * sizeof(OpDesc)), "cudaMalloc(program)");
+    CK(cudaMemcpy(p.dev, p.ops.data(), p.ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice), "upload program");
+  }
+  m->host.clear();  // device copies are all that is needed from here on
+  *model_id = (int32_t)ctx->models.size();
+  ctx->models.push_back(std::move(m));
+  return GL_OK;
+}
+
+gl_status gl_model_io(gl_ctx* ctx, int32_t id, int32_t batch, int64_t* in_b, int64_t* out_b) {
+  if (!ctx || id < 0 || id >= (int)ctx->models.size() || batch < 1 || batch > 32)
+    return fail(GL_E_ARG, "gl_model_io: bad arguments");
+  if (in_b) *in_b = (int64_t)ctx->models[id]->in_bytes[batch];
+  if (out_b) *out_b = (int64_t)ctx->models[id]->out_bytes[batch];
+  return GL_OK;
+}
+
+gl_status gl_model_cost(gl_ctx* ctx, int32_t id, int32_t batch, double* flops, double* wbytes) {
+  if (!ctx || id < 0 || id >= (int)ctx->models.size() || batch < 1 || batch > 32)
+    return fail(GL_E_ARG, "gl_model_cost: bad arguments");
+  if (flops) *flops = ctx->models[id]->prog[batch].flops;
+  if (wbytes) *wbytes = ctx->models[id]->prog[batch].weight_bytes;
+  return GL_OK;
+}
+
+gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, int32_t* sm_count) {
+  if (!ctx || !gpulet_id || gpu < 0 || gpu >= (int)ctx->gpus.size()) return fail(GL_E_ARG, "gl_create_gpulet: bad arguments");
+  if (sm_for_pct(pct) < 0) return fail(GL_E_GRID, "gl_create_gpulet: sm_pct not in {20,40,50,60,80,100}");
+  if (ctx->poisoned) return fail(GL_E_CUDA, "context poisoned by an earlier CUDA error");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GpuState& G = ctx->gpus[gpu];
+  int used = 0, nlive = 0;
+  for (int s = 0; s < 2; ++s)
+    if (G.slots[s] >= 0) {
+      used += ctx->gpulets[G.slots[s]]->pct;
+      ++nlive;
+    }
+  if (nlive >= 2 || used + pct > 100) return fail(GL_E_PARTITION, "gl_create_gpulet: gpu-let sizes on a GPU must sum to <= 100, at most 2");
+  const int slot = G.slots[0] < 0 ? 0 : 1;
+  Driver& D = driver();
+  CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  auto g = std::make_unique<Gpulet>();
+  g->gpu = gpu;
+  g->slot = slot;
+  g->pct = pct;
+  if (pct == 100) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    g->stream = (CUstream)s;
+    g->own_primary_stream = true;
+    g->nsm = G.nsm;
+  } else {
+    CUdevice cud;
+    gl_status rc = cu_check(ctx, D.deviceGet(&cud, G.dev), "cuDeviceGet");
+    if (rc) return rc;
+    if (!G.split) {
+      CUdevResource all;
+      rc = cu_check(ctx, D.deviceGetDevResource(cud, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+      if (rc) return rc;
+      G.ngroups = 32;
+      rc = cu_check(ctx, D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem, 0, 8),
+                    "cuDevSmResourceSplitByCount");
+      if (rc) return rc;
+      G.split = true;
+    }
+    const int want = sm_for_pct(pct);
+    std::vector<CUdevResource> res;
+    int have = 0;
+    // larger shares also take the remainder group (148 = 18 x 8 + 4)
+    if (pct >= 60 && !G.rem_used && G.rem.sm.smCount > 0) {
+      res.push_back(G.rem);
+      have += (int)G.rem.sm.smCount;
+      g->uses_rem = true;
+    }
+    for (unsigned i = 0; i < G.ngroups && have < want; ++i) {
+      if (G.used_groups & (1u << i)) continue;
+      res.push_back(G.groups[i]);
+      have += (int)G.groups[i].sm.smCount;
+      g->groups.push_back((int)i);
+    }
+    if (have < want) return fail(GL_E_PARTITION, "gl_create_gpulet: not enough free SM groups");
+    CUdevResourceDesc desc;
+    rc = cu_check(ctx, D.devResourceGenerateDesc(&desc, res.data(), (unsigned)res.size()), "cuDevResourceGenerateDesc");
+    if (rc) return rc;
+    rc = cu_check(ctx, D.greenCtxCreate(&g->gctx, desc, cud, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+    if (rc) return rc;
+    rc = cu_check(ctx, D.greenCtxStreamCreate(&g->stream, g->gctx, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+    if (rc) return rc;
+    g->nsm = have;
+    for (int i : g->groups) G.used_groups |= (1u << i);
+    if (g->uses_rem) G.rem_used = true;
+  }
+  // workspace: the largest program of any model loaded on this GPU
+  size_t ws = 256;
+  for (auto& m : ctx->models)
+    if (m && m->gpu == gpu)
+      for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
+  g->ws_bytes = ws;
+  CK(cudaMalloc(&g->ws, ws), "cudaMalloc(workspace)");
+  CK(cudaMemset(g->ws, 0, ws), "memset(workspace)");
+  CK(cudaHostAlloc((void**)&g->ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+  std::memset((void*)g->ring, 0, sizeof(HostRing));
+  CK(cudaHostGetDevicePointer((void**)&g->ring_dev, g->ring, 0), "cudaHostGetDevicePointer");
+  CK(cudaMalloc(&g->st, sizeof(ExecState)), "cudaMalloc(state)");
+  CK(cudaMemset(g->st, 0, sizeof(ExecState)), "memset(state)");
+  CK(cudaMalloc(&g->smid, 160 * sizeof(int)), "cudaMalloc(smid)");
+  CK(cudaMemset(g->smid, 0xff, 160 * sizeof(int)), "memset(smid)");
+  CK(cudaStreamSynchronize(0), "sync before launch");   // legacy stream only: executors are non-blocking
+  g->id = (int)ctx->gpulets.size();
+  ExecParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.ring = g->ring_dev;
+  p.st = g->st;
+  p.ws = g->ws;
+  p.gpulet = g->id;
+  p.one_shot = 0;
+  p.smid_log = g->smid;
+  ++g_live_exec;
+  gl_status rc = launch_executor(ctx, G.dev, g->stream, g->nsm, p);
+  if (rc) {
+    --g_live_exec;
+    return rc;
+  }
+  // residency handshake: every CTA must reach the loop (green contexts give no
+  // co-scheduling guarantee, cuda.h "Green Contexts" notes)
+  auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    int n = 0;
+    for (int i = 0; i < g->nsm; ++i) n += g->ring->resident[i] ? 1 : 0;
+    if (n == g->nsm) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
+      g->ring->quit = 1;
+      return fail(GL_E_NOT_CONCURRENT, "gl_create_gpulet: executor CTAs not co-resident (" + std::to_string(n) + "/" +
+                                            std::to_string(g->nsm) + ")");
+    }
+    cudaError_t e = cudaStreamQuery((cudaStream_t)g->stream);
+    if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_check(ctx, e, "executor launch");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  g->alive = true;
+  G.slots[slot] = g->id;
+  *gpulet_id = g->id;
+  if (sm_count) *sm_count = g->nsm;
+  ctx->gpulets.push_back(std::move(g));
+  return GL_OK;
+}
+
+gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t id) {
+  if (!ctx || id < 0 || id >= (int)ctx->gpulets.size() || !ctx->gpulets[id]) return fail(GL_E_ARG, "bad gpu-let id");
+  Gpulet& g = *ctx->gpulets[id];
+  if (!g.alive) return fail(GL_E_STATE, "gpu-let already destroyed");
+  cudaSetDevice(ctx->gpus[g.gpu].dev);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  g.ring->quit = 1;
+  cudaError_t e;
+  auto t0 = std::chrono::steady_clock::now();
+  while ((e = cudaStreamQuery((cudaStream_t)g.stream)) == cudaErrorNotReady) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+      return fail(GL_E_TIMEOUT, "gl_destroy_gpulet: executor did not exit");
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
+  g.alive = false;
+  GpuState& G = ctx->gpus[g.gpu];
+  G.slots[g.slot] = -1;
+  for (int i : g.groups) G.used_groups &= ~(1u << i);
+  if (g.uses_rem) G.rem_used = false;
+  if (g.own_primary_stream)
+    cudaStreamDestroy((cudaStream_t)g.stream);
+  else if (g.stream)
+    driver().streamDestroy(g.stream);
+  if (g.gctx) driver().greenCtxDestroy(g.gctx);
+  --g_live_exec;
+  release_device(g.ws, false);
+  release_device(g.st, false);
+  release_device(g.smid, false);
+  release_device(g.ring, true);
+  g.ring = nullptr;
+  flush_deferred();
+  if (e != cudaSuccess) return cuda_check(ctx, e, "executor");
+  return GL_OK;
+}
+
+gl_status gl_gpulet_smids(gl_ctx* ctx, int32_t id, int32_t* smids, int32_t cap, int32_t* n) {
+  if (!ctx || id < 0 || id >= (int)ctx->gpulets.size() || !smids || !n) return fail(GL_E_ARG, "bad arguments");
+  Gpulet& g = *ctx->gpulets[id];
+  const int k = std::min(cap, g.nsm);
+  cudaSetDevice(ctx->gpus[g.gpu].dev);
+  CK(cudaMemcpy(smids, g.smid, k * sizeof(int), cudaMemcpyDeviceToHost), "copy smids");
+  *n = k;
+  return GL_OK;
+}
+
+gl_status gl_submit_batch(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_dev, void* out_dev, int32_t batch,
+                          float slo_ms, uint64_t* ticket) {
+  if (!ctx || gid < 0 || gid >= (int)ctx->gpulets.size() || !in_dev || !out_dev)
+    return fail(GL_E_ARG, "gl_submit_batch: bad arguments");
+  if (batch < 1 || batch > 32) return fail(GL_E_CAPACITY, "gl_submit_batch: batch outside [1,32]");
+  Gpulet& g = *ctx->gpulets[gid];
+  if (!g.alive) return fail(GL_E_STATE, "gl_submit_batch: gpu-let destroyed");
+  if (mid < 0 || mid >= (int)ctx->models.size() || ctx->models[mid]->gpu != g.gpu)
+    return fail(GL_E_MODEL, "gl_submit_batch: model not loaded on this gpu-let's GPU");
+  Model& m = *ctx->models[mid];
+  if (m.prog[batch].ws_bytes > g.ws_bytes)
+    return fail(GL_E_STATE, "gl_submit_batch: model loaded after the gpu-let was created (workspace too small)");
+  if (g.tail - g.comp_seen >= (uint64_t)kRing - 1) return fail(GL_E_QUEUE_FULL, "gl_submit_batch: ring full");
+  WorkDesc& w = g.ring->items[g.tail % kRing];
+  const uint64_t t = ctx->next_ticket++;
+  w.ticket = t;
+  w.prog = m.prog[batch].dev;
+  w.in = in_dev;
+  w.out = out_dev;
+  w.n_ops = (int)m.prog[batch].ops.size();
+  w.model = mid;
+  w.batch = batch;
+  w.slo_us = (int32_t)(slo_ms * 1000.0f);
+  w.t_submit_ns = now_ns();
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ++g.tail;
+  __atomic_store_n(&g.ring->tail, g.tail, __ATOMIC_RELEASE);
+  if (ticket) *ticket = t;
+  return GL_OK;
+}
+
+static int collect(gl_ctx* ctx, gl_completion* out, int max) {
+  int n = 0;
+  for (auto& gp : ctx->gpulets) {
+    if (!gp) continue;
+    Gpulet& g = *gp;
+    if (!g.ring) continue;
+    const uint64_t ct = __atomic_load_n(&g.ring->comp_tail, __ATOMIC_ACQUIRE);
+    while (g.comp_seen < ct && n < max) {
+      const volatile CompRec& c = g.ring->comp[g.comp_seen % kRing];
+      gl_completion& o = out[n++];
+      o.ticket = c.ticket;
+      o.gpulet = c.gpulet;
+      o.model = c.model;
+      o.batch = c.batch;
+      o.status = c.status;
+      o.t_submit_ns = c.t_submit_ns;
+      o.t_dequeue_ns = c.t_dequeue_ns;
+      o.t_start_ns = c.t_start_ns;
+      o.t_end_ns = c.t_end_ns;
+      ++g.comp_seen;
+    }
+  }
+  return n;
+}
+
+gl_status gl_poll(gl_ctx* ctx, gl_completion* out, int32_t max, int32_t* n_out) {
+  if (!ctx || !out || !n_out || max < 0) return fail(GL_E_ARG, "gl_poll: bad arguments");
+  int n = 0;
+  while (n < max && !ctx->stash.empty()) {
+    out[n++] = ctx->stash.front();
+    ctx->stash.pop_front();
+  }
+  n += collect(ctx, out + n, max - n);
+  *n_out = n;
+  for (auto& gp : ctx->gpulets)
+    if (gp && gp->alive && gp->ring->error) return fail(GL_E_CUDA, "executor reported a device fault");
+  return GL_OK;
+}
+
+gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completion* out) {
+  if (!ctx) return fail(GL_E_ARG, "gl_wait: bad arguments");
+  auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    for (auto it = ctx->stash.begin(); it != ctx->stash.end(); ++it) {
+      if (it->ticket == ticket) {
+        if (out) *out = *it;
+        ctx->stash.erase(it);
+        return GL_OK;
+      }
+    }
+    gl_completion buf[64];
+    int n = collect(ctx, buf, 64);
+    for (int i = 0; i < n; ++i) ctx->stash.push_back(buf[i]);
+    if (n) continue;
+    for (auto& gp : ctx->gpulets) {
+      if (!gp || !gp->alive) continue;
+      cudaError_t e = cudaStreamQuery((cudaStream_t)gp->stream);
+      if (e != cudaErrorNotReady) {
+        gp->alive = false;
+        return cuda_check(ctx, e == cudaSuccess ? cudaErrorLaunchFailure : e, "executor exited");
+      }
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms))
+      return fail(GL_E_TIMEOUT, "gl_wait: timeout");
+    std::this_thread::yield();
+  }
+}
+
+gl_status gl_profile(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32_t warmup, int32_t reps,
+                     const void* in_dev, void* out_dev, double* median_us) {
+  if (!ctx || !median_us || reps < 1 || warmup < 0) return fail(GL_E_ARG, "gl_profile: bad arguments");
+  std::vector<double> lat;
+  const int total = warmup + reps;
+  uint64_t last = 0;
+  for (int i = 0; i < total; ++i) {
+    uint64_t t;
+    gl_status s;
+    while ((s = gl_submit_batch(ctx, gid, mid, in_dev, out_dev, batch, 0.f, &t)) == GL_E_QUEUE_FULL) {
+      gl_completion c[64];
+      int n = collect(ctx, c, 64);
+      for (int k = 0; k < n; ++k) ctx->stash.push_back(c[k]);
+    }
+    if (s) return s;
+    last = t;
+    (void)last;
+  }
+  // collect everything we submitted
+  int got = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<gl_completion> mine;
+  while (got < total) {
+    gl_completion c[64];
+    int n = collect(ctx, c, 64);
+    for (int k = 0; k < n; ++k) {
+      if (c[k].gpulet == gid && c[k].model == mid) {
+        mine.push_back(c[k]);
+        ++got;
+      } else {
+        ctx->stash.push_back(c[k]);
+      }
+    }
+    for (auto it = ctx->stash.begin(); it != ctx->stash.end() && got < total;) {
+      if (it->gpulet == gid && it->model == mid) {
+        mine.push_back(*it);
+        ++got;
+        it = ctx->stash.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) return fail(GL_E_TIMEOUT, "gl_profile: timeout");
+    if (!n) std::this_thread::yield();
+  }
+  std::sort(mine.begin(), mine.end(), [](const gl_completion& a, const gl_completion& b) { return a.ticket < b.ticket; });
+  for (size_t i = warmup; i < mine.size(); ++i) lat.push_back((mine[i].t_end_ns - mine[i].t_start_ns) / 1000.0);
+  std::sort(lat.begin(), lat.end());
+  *median_us = lat[lat.size() / 2];
+  return GL_OK;
+}
+
+gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A, const uint16_t* W, const uint16_t* bias, const void* res,
+                       void* out, int32_t M, int32_t N, int32_t K, int32_t act, int32_t swap_ab, int32_t splitk,
+                       int32_t out_fp32) {
+  if (!ctx || !A || !W || !bias || !out || gpu < 0 || gpu >= (int)ctx->gpus.size() || M < 1 || N < 1 || K < 8 ||
+      K % 8)
+    return fail(GL_E_ARG, "gl_test_gemm: bad arguments");
+  if (res) return fail(GL_E_ARG, "gl_test_gemm: residual must be passed via the input buffer layout");
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  DevWeights dw;
+  Program prog;
+  std::string err;
+  if (!build_test_gemm(M, N, K, act, swap_ab, splitk, out_fp32, W, bias, 0, dw, prog, err))
+    return fail(GL_E_ARG, err);
+  return run_oneshot(ctx, gpu, prog, A, out);
+}
+
+gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x, const uint16_t* W, const uint16_t* bias, void* y,
+                       int32_t N, int32_t H, int32_t Wd, int32_t C, int32_t Cout, int32_t KH, int32_t stride,
+                       int32_t pad, int32_t act) {
+  if (!ctx || !x || !W || !bias || !y || gpu < 0 || gpu >= (int)ctx->gpus.size() || C % 8)
+    return fail(GL_E_ARG, "gl_test_conv: bad arguments");
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  DevWeights dw;
+  Program prog;
+  std::string err;
+  if (!build_test_conv(N, H, Wd, C, Cout, KH, stride, pad, act, W, bias, dw, prog, err)) return fail(GL_E_ARG, err);
+  return run_oneshot(ctx, gpu, prog, x, y);
+}
+
+gl_status gl_test_misc(gl_ctx* ctx, int gpu, int32_t type, const int32_t* ia, int32_t n, const uint16_t* params,
+                       int64_t n_params, const void* x, void* y) {
+  if (!ctx || !ia || !y || gpu < 0 || gpu >= (int)ctx->gpus.size()) return fail(GL_E_ARG, "gl_test_misc: bad arguments");
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  DevWeights dw;
+  Program prog;
+  std::string err;
+  if (!build_test_misc(type, ia, n, params, (size_t)n_params, dw, prog, err)) return fail(GL_E_ARG, err);
+  return run_oneshot(ctx, gpu, prog, x, y);
+}
+
+}  // extern "C"
+
+extern "C" gl_status gl_run_once(gl_ctx* ctx, int32_t mid, int32_t batch, const void* in_dev, void* out_dev,
+                                 int32_t n_sm, uint64_t* trace_ns, int32_t cap, int32_t* n_steps) {
+  if (!ctx || mid < 0 || mid >= (int)ctx->models.size() || batch < 1 || batch > 32 || !in_dev || !out_dev)
+    return fail(GL_E_ARG, "gl_run_once: bad arguments");
+  Model& m = *ctx->models[mid];
+  GpuState& G = ctx->gpus[m.gpu];
+  if (n_sm < 1 || n_sm > G.nsm) n_sm = G.nsm;
+  CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  Program& prog = m.prog[batch];
+  char* ws = nullptr;
+  CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
+  CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
+  HostRing* ring = nullptr;
+  CK(cudaHostAlloc((void**)&ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+  std::memset((void*)ring, 0, sizeof(HostRing));
+  HostRing* ring_dev = nullptr;
+  CK(cudaHostGetDevicePointer((void**)&ring_dev, ring, 0), "cudaHostGetDevicePointer");
+  ExecState* st = nullptr;
+  CK(cudaMalloc(&st, sizeof(ExecState)), "cudaMalloc(st)");
+  CK(cudaMemset(st, 0, sizeof(ExecState)), "memset st");
+  uint64_t* tr = nullptr;
+  const int tcap = 1024;
+  CK(cudaMalloc(&tr, tcap * sizeof(uint64_t)), "cudaMalloc(trace)");
+  CK(cudaMemset(tr, 0, tcap * sizeof(uint64_t)), "memset trace");
+  WorkDesc& w = ring->items[0];
+  w.ticket = 0;
+  w.prog = prog.dev;
+  w.in = in_dev;
+  w.out = out_dev;
+  w.n_ops = (int)prog.ops.size();
+  w.model = mid;
+  w.batch = batch;
+  ring->tail = 1;
+  ExecParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.ring = ring_dev;
+  p.st = st;
+  p.ws = ws;
+  p.one_shot = 1;
+  p.trace = tr;
+  p.trace_cap = tcap;
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  gl_status rc = launch_executor(ctx, G.dev, (CUstream)s, n_sm, p);
+  if (rc == GL_OK) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_check(ctx, e, "executor (run_once)");
+  }
+  int steps = 0;
+  for (auto& op : prog.ops) steps += op.step_end ? 1 : 0;
+  if (rc == GL_OK && trace_ns && cap > 0) {
+    std::vector<uint64_t> h(tcap);
+    cudaMemcpy(h.data(), tr, tcap * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < std::min(cap, std::min(steps + 1, tcap)); ++i) trace_ns[i] = h[i];
+  }
+  if (n_steps) *n_steps = steps;
+  cudaStreamDestroy(s);
+  release_device(tr, false);
+  release_device(st, false);
+  release_device(ring, true);
+  release_device(ws, false);
+  return rc;
+}
+
+extern "C" gl_status gl_program_info(gl_ctx* ctx, int32_t mid, int32_t batch, int32_t* step_type, int32_t* step_ops,
+                                     double* step_flops, double* step_bytes, int32_t cap, int32_t* n_steps) {
+  if (!ctx || mid < 0 || mid >= (int)ctx->models.size() || batch < 1 || batch > 32)
+    return fail(GL_E_ARG, "gl_program_info: bad arguments");
+  Program& prog = ctx->models[mid]->prog[batch];
+  int s = 0;
+  bool open = false;
+  for (auto& op : prog.ops) {
+    double f, b;
+    op_cost(op, f, b);
+    if (s < cap) {
+      if (!open) {
+        if (step_type) step_type[s] = op.type;
+        if (step_ops) step_ops[s] = 0;
+        if (step_flops) step_flops[s] = 0;
+        if (step_bytes) step_bytes[s] = 0;
+        open = true;
+      }
+      if (step_ops) step_ops[s] += 1;
+      if (step_flops) step_flops[s] += f;
+      if (step_bytes) step_bytes[s] += b;
+    }
+    if (op.step_end) {
+      ++s;
+      open = false;
+    }
+  }
+  if (n_steps) *n_steps = s;
+  return GL_OK;
+}

@@ -1,0 +1,90 @@
+// Internal host-side structures of libgpulet (not part of the C-ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "program.h"
+
+namespace gl {
+
+// ---- driver entry points (resolved through cudart; no link-time libcuda) ----
+struct Driver {
+  decltype(&::cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
+  decltype(&::cuDeviceGetDevResource) deviceGetDevResource = nullptr;
+  decltype(&::cuDevSmResourceSplitByCount) devSmResourceSplitByCount = nullptr;
+  decltype(&::cuDevResourceGenerateDesc) devResourceGenerateDesc = nullptr;
+  decltype(&::cuGreenCtxCreate) greenCtxCreate = nullptr;
+  decltype(&::cuGreenCtxDestroy) greenCtxDestroy = nullptr;
+  decltype(&::cuGreenCtxStreamCreate) greenCtxStreamCreate = nullptr;
+  decltype(&::cuLaunchKernelEx) launchKernelEx = nullptr;
+  decltype(&::cuKernelSetAttribute) kernelSetAttribute = nullptr;
+  decltype(&::cuStreamDestroy) streamDestroy = nullptr;
+  decltype(&::cuDeviceGet) deviceGet = nullptr;
+  bool ok = false;
+};
+Driver& driver();
+// cudaFree / cudaFreeHost, deferred while persistent executors are running.
+void release_device(void* p, bool host);
+
+// ---- weights -------------------------------------------------------------------
+struct Param {
+  std::vector<int> shape;
+  std::vector<uint16_t> data;  // bf16 bits
+  size_t numel() const {
+    size_t n = 1;
+    for (int d : shape) n *= (size_t)d;
+    return n;
+  }
+};
+using ParamMap = std::map<std::string, Param>;
+bool load_glw(const std::string& path, ParamMap& out, std::string& err);
+
+// Device-side copies of (repacked) weights of one model on one GPU.
+struct DevWeights {
+  std::vector<void*> allocs;
+  std::map<std::string, void*> ptr;
+  size_t bytes = 0;
+  ~DevWeights();
+};
+
+// ---- programs -------------------------------------------------------------------
+struct Program {
+  std::vector<OpDesc> ops;
+  OpDesc* dev = nullptr;   // device copy
+  size_t ws_bytes = 0;     // activation workspace needed
+  double flops = 0;        // algorithmic FLOPs of one batch (2 * MACs)
+  double weight_bytes = 0; // weight bytes read once per batch
+};
+
+struct Model {
+  int kind = 0;
+  int gpu = 0;
+  ParamMap host;                 // host copy of the file (kept for repacking)
+  std::unique_ptr<DevWeights> w;
+  Program prog[33];              // per batch 1..32
+  size_t in_bytes[33] = {0}, out_bytes[33] = {0};
+};
+
+// Build the layer program of model `kind` at batch b (models.cpp).
+bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
+                   size_t& in_bytes, size_t& out_bytes, std::string& err);
+
+// Single-op programs for kernel unit tests (models.cpp).
+bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int out_fp32, const uint16_t* w_host,
+                     const uint16_t* b_host, int has_res, DevWeights& dw, Program& out, std::string& err);
+bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, int pad, int act,
+                     const uint16_t* w_host, const uint16_t* b_host, DevWeights& dw, Program& out, std::string& err);
+bool build_test_misc(int type, const int* iargs, int n_iargs, const uint16_t* w_host, size_t w_len, DevWeights& dw,
+                     Program& out, std::string& err);
+
+void op_cost(const OpDesc& op, double& flops, double& bytes);
+int model_kind_count();
+const char* model_name(int kind);
+
+}  // namespace gl

@@ -1,0 +1,261 @@
+"""Thin ctypes binding of include/gpulet.h (argument marshalling only).
+
+Every step of the hot path runs inside libgpulet.so (CUDA kernels + native
+runtime + native scheduler).  There is no fallback: if the library or a GPU is
+missing, calls raise GpuletError.  torch is used only to hand over device
+pointers of tensors the caller allocated.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpulet.so")
+
+GL_OK = 0
+ERRORS = {-1: "GL_E_ARG", -2: "GL_E_GRID", -3: "GL_E_CAPACITY", -4: "GL_E_PARTITION", -5: "GL_E_STATE",
+          -6: "GL_E_MODEL", -7: "GL_E_QUEUE_FULL", -8: "GL_E_NOT_CONCURRENT", -9: "GL_E_PARSE",
+          -10: "GL_E_DATA", -11: "GL_E_BUDGET", -12: "GL_E_CUDA", -13: "GL_E_TIMEOUT"}
+MODELS = ["lenet5", "googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"]
+MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3}
+
+# exported symbols declared in include/gpulet.h
+SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
+           "gl_create_gpulet", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
+           "gl_profile", "gl_run_once", "gl_program_info", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc"]
+
+
+class GpuletError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Completion(ctypes.Structure):
+    _fields_ = [("ticket", ctypes.c_uint64), ("gpulet", ctypes.c_int32), ("model", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("status", ctypes.c_int32), ("t_submit_ns", ctypes.c_uint64),
+                ("t_dequeue_ns", ctypes.c_uint64), ("t_start_ns", ctypes.c_uint64), ("t_end_ns", ctypes.c_uint64)]
+
+
+class SchedInput(ctypes.Structure):
+    _fields_ = [("n_models", ctypes.c_int32), ("names", ctypes.POINTER(ctypes.c_char_p)),
+                ("lat_us", ctypes.POINTER(ctypes.c_int32)), ("l2", ctypes.POINTER(ctypes.c_double)),
+                ("mem", ctypes.POINTER(ctypes.c_double)), ("slo_us", ctypes.POINTER(ctypes.c_int32)),
+                ("rates", ctypes.POINTER(ctypes.c_int32)), ("coeffs", ctypes.c_double * 5),
+                ("num_gpus", ctypes.c_int32), ("mode", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgpulet.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GpuletError(-12, f"{LIB_PATH} missing: run `python -m paper_2109_01611_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+        sig = {
+            "gl_init": [ctypes.c_int, ctypes.POINTER(P)],
+            "gl_shutdown": [P],
+            "gl_load_model": [P, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(I32)],
+            "gl_model_io": [P, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)],
+            "gl_model_cost": [P, I32, I32, ctypes.POINTER(D), ctypes.POINTER(D)],
+            "gl_create_gpulet": [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I32), ctypes.POINTER(I32)],
+            "gl_destroy_gpulet": [P, I32],
+            "gl_gpulet_smids": [P, I32, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)],
+            "gl_submit_batch": [P, I32, I32, P, P, I32, ctypes.c_float, ctypes.POINTER(U64)],
+            "gl_poll": [P, ctypes.POINTER(Completion), I32, ctypes.POINTER(I32)],
+            "gl_wait": [P, U64, I32, ctypes.POINTER(Completion)],
+            "gl_profile": [P, I32, I32, I32, I32, I32, P, P, ctypes.POINTER(D)],
+            "gl_run_once": [P, I32, I32, P, P, I32, ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
+            "gl_program_info": [P, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(D),
+                                ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
+            "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
+                            ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
+            "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
+            "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, P, I32, I32, I32, I32, I32, I32, I32],
+            "gl_test_conv": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32],
+            "gl_test_misc": [P, ctypes.c_int, I32, ctypes.POINTER(I32), I32, P, I64, P, P],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = I32
+        L.gl_last_error.restype = ctypes.c_char_p
+        L.gl_last_error.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != GL_OK:
+        raise GpuletError(rc, lib().gl_last_error().decode(errors="replace"))
+
+
+def _ptr(x):
+    """Device/host address of a torch tensor, numpy array or int (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+class Context:
+    """gl_ctx wrapper: models, gpu-lets, submit/poll."""
+
+    def __init__(self, num_gpus=1):
+        self.h = ctypes.c_void_p()
+        _check(lib().gl_init(num_gpus, ctypes.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().gl_shutdown(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def load_model(self, gpu, kind, weight_file):
+        k = MODELS.index(kind) if isinstance(kind, str) else kind
+        mid = ctypes.c_int32()
+        _check(lib().gl_load_model(self.h, gpu, k, weight_file.encode(), ctypes.byref(mid)))
+        return mid.value
+
+    def model_io(self, mid, batch):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().gl_model_io(self.h, mid, batch, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def model_cost(self, mid, batch):
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(lib().gl_model_cost(self.h, mid, batch, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def create_gpulet(self, gpu, sm_pct):
+        gid, n = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().gl_create_gpulet(self.h, gpu, sm_pct, ctypes.byref(gid), ctypes.byref(n)))
+        return gid.value, n.value
+
+    def destroy_gpulet(self, gid):
+        _check(lib().gl_destroy_gpulet(self.h, gid))
+
+    def gpulet_smids(self, gid, cap=160):
+        buf = (ctypes.c_int32 * cap)()
+        n = ctypes.c_int32()
+        _check(lib().gl_gpulet_smids(self.h, gid, buf, cap, ctypes.byref(n)))
+        return list(buf[: n.value])
+
+    def submit_batch(self, gid, mid, x, y, batch, slo_ms=0.0):
+        t = ctypes.c_uint64()
+        _check(lib().gl_submit_batch(self.h, gid, mid, _ptr(x), _ptr(y), batch, slo_ms, ctypes.byref(t)))
+        return t.value
+
+    def try_submit_batch(self, gid, mid, x, y, batch, slo_ms=0.0):
+        """Like submit_batch but returns None when the ring is full."""
+        t = ctypes.c_uint64()
+        rc = lib().gl_submit_batch(self.h, gid, mid, _ptr(x), _ptr(y), batch, slo_ms, ctypes.byref(t))
+        if rc == -7:
+            return None
+        _check(rc)
+        return t.value
+
+    def poll(self, max_n=256):
+        buf = (Completion * max_n)()
+        n = ctypes.c_int32()
+        _check(lib().gl_poll(self.h, buf, max_n, ctypes.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def wait(self, ticket, timeout_ms=60000):
+        c = Completion()
+        _check(lib().gl_wait(self.h, ticket, timeout_ms, ctypes.byref(c)))
+        return c
+
+    def profile(self, gid, mid, batch, x, y, warmup=10, reps=50):
+        d = ctypes.c_double()
+        _check(lib().gl_profile(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d)))
+        return d.value
+
+    def run_once(self, mid, batch, x, y, n_sm=0, trace=True):
+        """One-shot executor launch; returns per-step durations (ns) when trace."""
+        cap = 1024
+        tr = (ctypes.c_uint64 * cap)()
+        n = ctypes.c_int32()
+        _check(lib().gl_run_once(self.h, mid, batch, _ptr(x), _ptr(y), n_sm, tr if trace else None, cap,
+                                 ctypes.byref(n)))
+        if not trace:
+            return None
+        ts = list(tr[: n.value + 1])
+        return [ts[i + 1] - ts[i] for i in range(n.value)]
+
+    def program_info(self, mid, batch, cap=1024):
+        t = (ctypes.c_int32 * cap)()
+        o = (ctypes.c_int32 * cap)()
+        f = (ctypes.c_double * cap)()
+        b = (ctypes.c_double * cap)()
+        n = ctypes.c_int32()
+        _check(lib().gl_program_info(self.h, mid, batch, t, o, f, b, cap, ctypes.byref(n)))
+        return [(t[i], o[i], f[i], b[i]) for i in range(n.value)]
+
+    # ---- kernel unit entry points -------------------------------------------
+    def test_gemm(self, gpu, A, W_bits, b_bits, out, M, N, K, act=0, swap_ab=0, splitk=1, out_fp32=0):
+        _check(lib().gl_test_gemm(self.h, gpu, _ptr(A), _ptr(W_bits), _ptr(b_bits), None, _ptr(out), M, N, K, act,
+                                  swap_ab, splitk, out_fp32))
+
+    def test_conv(self, gpu, x, W_bits, b_bits, y, N, H, W, C, Cout, KH, stride, pad, act=1):
+        _check(lib().gl_test_conv(self.h, gpu, _ptr(x), _ptr(W_bits), _ptr(b_bits), _ptr(y), N, H, W, C, Cout, KH,
+                                  stride, pad, act))
+
+    def test_misc(self, gpu, op, iargs, params, x, y):
+        ia = (ctypes.c_int32 * len(iargs))(*iargs)
+        n = 0 if params is None else int(params.size)
+        _check(lib().gl_test_misc(self.h, gpu, op, ia, len(iargs), _ptr(params), n, _ptr(x), _ptr(y)))
+
+
+def schedule(names, lat_us, l2, mem, slo_us, rates, num_gpus, mode, coeffs=(0, 0, 0, 0, 0), cap=1 << 20):
+    """gl_schedule: returns (plan_dump_text, schedulable).  lat_us [M][32][6] ints,
+    l2/mem [M][6][6] floats (or None), slo_us/rates [M] ints."""
+    import numpy as np
+    M = len(names)
+    nm = (ctypes.c_char_p * M)(*[n.encode() for n in names])
+    lat = np.ascontiguousarray(lat_us, dtype=np.int32).reshape(-1)
+    l2a = np.ascontiguousarray(l2 if l2 is not None else np.zeros((M, 6, 6)), dtype=np.float64).reshape(-1)
+    mema = np.ascontiguousarray(mem if mem is not None else np.zeros((M, 6, 6)), dtype=np.float64).reshape(-1)
+    slo = np.ascontiguousarray(slo_us, dtype=np.int32)
+    rt = np.ascontiguousarray(rates, dtype=np.int32)
+    si = SchedInput()
+    si.n_models = M
+    si.names = nm
+    si.lat_us = lat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    si.l2 = l2a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    si.mem = mema.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    si.slo_us = slo.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    si.rates = rt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    for i in range(5):
+        si.coeffs[i] = float(coeffs[i]) if coeffs is not None else 0.0
+    si.num_gpus = num_gpus
+    si.mode = MODES[mode] if isinstance(mode, str) else mode
+    buf = ctypes.create_string_buffer(cap)
+    ln, verdict = ctypes.c_size_t(), ctypes.c_int32()
+    _check(lib().gl_schedule(ctypes.byref(si), buf, cap, ctypes.byref(ln), ctypes.byref(verdict)))
+    return buf.value.decode(), bool(verdict.value)
+
+
+def fit_interference(X, y):
+    """gl_fit_interference: OLS coefficients c1..c5."""
+    import numpy as np
+    Xa = np.ascontiguousarray(X, dtype=np.float64)
+    ya = np.ascontiguousarray(y, dtype=np.float64)
+    c = np.zeros(5)
+    _check(lib().gl_fit_interference(Xa.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                     ya.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(ya),
+                                     c.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return c

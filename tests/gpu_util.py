@@ -1,0 +1,39 @@
+"""Helpers shared by the -m gpu tests (test infrastructure)."""
+import numpy as np
+
+REL_TOL = 2e-2          # north_star: max relative error <= 2e-2 (bf16 operands, fp32 accumulation)
+TOP1_TOL = 0.999        # north_star: top-1 identical on >= 99.9 % of (unambiguous) samples
+
+
+def to_dev_bf16(bits):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def from_dev_bf16(t):
+    import torch
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def bits_to_f64(bits):
+    return (np.ascontiguousarray(bits, np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def rel_err(got, ref):
+    ref = np.asarray(ref, np.float64)
+    got = np.asarray(got, np.float64)
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def top1_agreement(got, ref, tau):
+    """(strict, judged, ambiguous_fraction): judged excludes samples whose oracle
+    top-1/top-2 gap is <= tau."""
+    ref = np.asarray(ref).reshape(-1, ref.shape[-1])
+    got = np.asarray(got).reshape(-1, got.shape[-1])
+    a, b = ref.argmax(-1), got.argmax(-1)
+    strict = float((a == b).mean())
+    srt = np.sort(ref, axis=-1)
+    gap = srt[:, -1] - srt[:, -2]
+    keep = gap > tau
+    judged = float((a[keep] == b[keep]).mean()) if keep.any() else 1.0
+    return strict, judged, float(1 - keep.mean())

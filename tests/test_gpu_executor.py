@@ -1,0 +1,96 @@
+"""gpu-let executor on a B200: green-context confinement (%smid audit), the
+SM counts of the partition grid, co-resident gpu-lets, submit/poll ordering,
+and the C-ABI error paths (SURVEY §4.4 integration layer)."""
+import numpy as np
+import pytest
+
+import synthgen
+from tests.gpu_util import to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c():
+    from paper_2109_01611_b200 import gpulet
+    ctx = gpulet.Context(1)
+    ctx.mid = ctx.load_model(0, "lenet5", synthgen.weight_file("lenet5"))
+    yield ctx
+    ctx.close()
+
+
+@pytest.mark.parametrize("p,q", [(20, 80), (40, 60), (50, 50), (60, 40), (80, 20)])
+def test_pair_confinement(c, p, q):
+    a, na = c.create_gpulet(0, p)
+    b, nb = c.create_gpulet(0, q)
+    try:
+        sm = {20: 32, 40: 56, 50: 72, 60: 92, 80: 116}
+        assert na == sm[p] and nb == sm[q]
+        sa, sb = c.gpulet_smids(a), c.gpulet_smids(b)
+        assert len(set(sa)) == na and len(set(sb)) == nb      # one CTA per SM
+        assert not set(sa) & set(sb)                          # disjoint SM sets
+    finally:
+        c.destroy_gpulet(a)
+        c.destroy_gpulet(b)
+
+
+def test_partition_errors(c):
+    from paper_2109_01611_b200 import gpulet
+    with pytest.raises(gpulet.GpuletError) as e:
+        c.create_gpulet(0, 30)
+    assert e.value.code == -2
+    a, _ = c.create_gpulet(0, 60)
+    try:
+        with pytest.raises(gpulet.GpuletError) as e:
+            c.create_gpulet(0, 60)
+        assert e.value.code == -4
+    finally:
+        c.destroy_gpulet(a)
+
+
+def test_submit_poll_fifo_and_errors(c):
+    import torch
+    from paper_2109_01611_b200 import gpulet
+    g, _ = c.create_gpulet(0, 100)
+    try:
+        x = to_dev_bf16(synthgen.mnist_batch(32))
+        y = torch.empty(320, device="cuda")
+        tickets = [c.submit_batch(g, c.mid, x, y, 32, 5.0) for _ in range(100)]
+        got = []
+        while len(got) < 100:
+            got += [r.ticket for r in c.poll()]
+        assert got == tickets                                  # FIFO per gpu-let
+        with pytest.raises(gpulet.GpuletError) as e:
+            c.submit_batch(g, c.mid, x, y, 33)
+        assert e.value.code == -3
+        with pytest.raises(gpulet.GpuletError) as e:
+            c.submit_batch(g, 99, x, y, 1)
+        assert e.value.code == -6
+    finally:
+        c.destroy_gpulet(g)
+    with pytest.raises(gpulet.GpuletError) as e:
+        c.submit_batch(g, c.mid, x, y, 1)
+    assert e.value.code == -5
+
+
+def test_corun_overlap(c):
+    """Two gpu-lets execute concurrently: their device busy intervals overlap."""
+    import torch
+    a, _ = c.create_gpulet(0, 50)
+    b, _ = c.create_gpulet(0, 50)
+    try:
+        x = to_dev_bf16(synthgen.mnist_batch(32))
+        ya, yb = torch.empty(320, device="cuda"), torch.empty(320, device="cuda")
+        for _ in range(200):
+            c.submit_batch(a, c.mid, x, ya, 32)
+            c.submit_batch(b, c.mid, x, yb, 32)
+        recs = []
+        while len(recs) < 400:
+            recs += c.poll()
+        ia = [(r.t_start_ns, r.t_end_ns) for r in recs if r.gpulet == a]
+        ib = [(r.t_start_ns, r.t_end_ns) for r in recs if r.gpulet == b]
+        assert max(ia)[0] > min(ib)[0] and max(ib)[0] > min(ia)[0]
+        assert np.allclose(ya.cpu().numpy(), yb.cpu().numpy())
+    finally:
+        c.destroy_gpulet(a)
+        c.destroy_gpulet(b)
