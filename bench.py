@@ -111,15 +111,6 @@ def init_dist(world, backend):
     return None
 
 
-def allreduce(dist, vals, op):
-    if dist is None:
-        return vals
-    import torch
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
-    dist.all_reduce(t, op=op)
-    return t.tolist()
-
-
 # ----------------------------------------------------------------------------- oracle arm
 def reference_arm(a, world, rank):
     if rank != 0:
@@ -318,13 +309,8 @@ def our_arm(a, world, rank, local, dist):
                 "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(ach / peak, 4), "traffic": None,
                 "kernel": f"gl_executor one launch: {ln['model']} b={ln['batch']} on 148 SMs",
                 "launch_us": round(t * 1e6, 1), "peak_source": peak_src}
-    vals = allreduce(dist, [sat, tot, dev_s, wall], None) if False else [sat, tot, dev_s, wall]
-    if dist:
-        import torch.distributed as tdist
-        s = allreduce(dist, [sat, tot], tdist.ReduceOp.SUM)
-        m = allreduce(dist, [dev_s, wall], tdist.ReduceOp.MAX)
-        vals = [s[0], s[1], m[0], m[1]]
-    sat_all, tot_all, dev_max, wall_max = vals
+    from tools.dist_agg import aggregate
+    sat_all, tot_all, dev_max, wall_max = aggregate(dist, sat, tot, dev_s, wall)
     if rank != 0:
         ctx.close()
         return None

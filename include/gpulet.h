@@ -125,6 +125,27 @@ gl_status gl_run_once(gl_ctx* ctx, int32_t model_id, int32_t batch, const void* 
 gl_status gl_program_info(gl_ctx* ctx, int32_t model_id, int32_t batch, int32_t* step_type, int32_t* step_ops,
                           double* step_flops, double* step_bytes, int32_t cap, int32_t* n_steps);
 
+/* ---- serving frontend (§5) ---------------------------- */
+/* One lane of a plan: a model's share on a gpu-let (temporal sharing within it). */
+typedef struct {
+  int32_t gpulet;       /* gpu-let id */
+  int32_t model_id;     /* loaded model id */
+  int32_t model_slot;   /* index of the model in the arrival trace / slo_us */
+  int32_t batch;        /* planned batch b_i (dispatch when this many are queued) */
+  int32_t duty_us;      /* duty cycle D of the gpu-let (dispatch when the window is this old) */
+  int32_t weight;       /* routing weight = assigned rate (smooth weighted round-robin) */
+  int32_t drop_us;      /* Leff(1): a request with (now - arrival) + drop_us > SLO is dropped */
+  int32_t pad_;
+  const void* in_dev;   /* device input holding `batch` requests (first k used for a k-batch) */
+  void* out_dev;        /* device output */
+} gl_lane;
+/* Replay an arrival trace in real time (host clock): arr_us[n_req] sorted arrival
+ * times (us from the call), arr_model[n_req] model slot of each request.  Returns
+ * per-request latency in lat_us (us; -1 dropped).  Blocks until every request is
+ * completed or dropped.  Errors: GL_E_ARG, GL_E_TIMEOUT, errors of submit/poll. */
+gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                   const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us);
+
 /* ---- scheduler (Alg. 1) --------------------------------- */
 typedef struct {
   int32_t n_models;          /* <= 8, canonical order */

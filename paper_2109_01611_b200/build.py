@@ -24,6 +24,7 @@ SOURCES = [
     ("executor.cu", []),
     ("runtime.cpp", []),
     ("models.cpp", []),
+    ("frontend.cpp", []),
     ("sched.cpp", ["-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fno-fast-math"]),
 ]
 HEADERS = ["program.h", "ptx.cuh", "runtime.h"]

@@ -21,7 +21,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3}
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
-           "gl_profile", "gl_run_once", "gl_program_info", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc"]
+           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc"]
 
 
 class GpuletError(RuntimeError):
@@ -42,6 +42,13 @@ class SchedInput(ctypes.Structure):
                 ("mem", ctypes.POINTER(ctypes.c_double)), ("slo_us", ctypes.POINTER(ctypes.c_int32)),
                 ("rates", ctypes.POINTER(ctypes.c_int32)), ("coeffs", ctypes.c_double * 5),
                 ("num_gpus", ctypes.c_int32), ("mode", ctypes.c_int32)]
+
+
+class Lane(ctypes.Structure):
+    _fields_ = [("gpulet", ctypes.c_int32), ("model_id", ctypes.c_int32), ("model_slot", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("duty_us", ctypes.c_int32), ("weight", ctypes.c_int32),
+                ("drop_us", ctypes.c_int32), ("pad_", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
+                ("out_dev", ctypes.c_void_p)]
 
 
 _lib = None
@@ -71,6 +78,8 @@ def lib():
             "gl_run_once": [P, I32, I32, P, P, I32, ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
             "gl_program_info": [P, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(D),
                                 ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
+            "gl_serve": [P, ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
+                         ctypes.POINTER(I32), ctypes.POINTER(I64)],
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
@@ -195,6 +204,25 @@ class Context:
             return None
         ts = list(tr[: n.value + 1])
         return [ts[i + 1] - ts[i] for i in range(n.value)]
+
+    def serve(self, lanes, n_models, arr_us, arr_model, slo_us):
+        """gl_serve: lanes = list of dicts (gpulet, model_id, model_slot, batch, duty_us,
+        weight, drop_us, x, y); returns per-request latency (us, -1 dropped)."""
+        import numpy as np
+        L = (Lane * len(lanes))()
+        for i, d in enumerate(lanes):
+            L[i].gpulet, L[i].model_id, L[i].model_slot = d["gpulet"], d["model_id"], d["model_slot"]
+            L[i].batch, L[i].duty_us, L[i].weight, L[i].drop_us = d["batch"], d["duty_us"], d["weight"], d["drop_us"]
+            L[i].in_dev, L[i].out_dev = _ptr(d["x"]), _ptr(d["y"])
+        a = np.ascontiguousarray(arr_us, dtype=np.int64)
+        m = np.ascontiguousarray(arr_model, dtype=np.int32)
+        s = np.ascontiguousarray(slo_us, dtype=np.int32)
+        out = np.zeros(len(a), dtype=np.int64)
+        _check(lib().gl_serve(self.h, L, len(lanes), n_models, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                              m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
+                              s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return out
 
     def program_info(self, mid, batch, cap=1024):
         t = (ctypes.c_int32 * cap)()
