@@ -44,6 +44,12 @@ import numpy as np  # noqa: E402
 import synthgen  # noqa: E402
 
 METRIC = "SLO-satisfying req/s (six-model mix on gpu-lets)"
+VERBOSE = False
+
+
+def log(*a):
+    if VERBOSE:
+        print(*a, file=sys.stderr, flush=True)
 UNIT = "req/s"
 
 
@@ -195,22 +201,32 @@ def our_arm(a, world, rank, local, dist):
     coeffs = common.load_coeffs()
     x, rates, dump, ok = plan_for(lat_env, l2, mem, slo, coeffs, a.mode, a.scenario)
     gls, verdict = common.parse_plan(dump)
+    log(f"plan x={x:.3f} rates={rates} slo={slo}\n{dump}")
     # ---- build the plan: gpu-lets and resident per-lane inputs
+    # all device buffers are allocated before any executor starts (a device
+    # allocation can synchronise the device and wait behind a persistent kernel)
     lanes = []      # (gid, model, batch, D_us, x, y, slo_us)
     made = {}
-    for g in sorted(gls, key=lambda d: d["slot"]):
-        if not g["lanes"]:
-            continue
-        gid, nsm = ctx.create_gpulet(gpu, g["size"])
-        made[gid] = (g["size"], nsm)
+    used = [g for g in sorted(gls, key=lambda d: d["slot"]) if g["lanes"]]
+    for g in used:
         for ln in g["lanes"]:
             m = ln["model"]
             mi = common.MODELS.index(m)
             xin = common.device_input(m, ln["batch"])
             yout = torch.empty(ctx.model_io(mids[m], ln["batch"])[1] // 4, device="cuda")
-            lanes.append(dict(gid=gid, model=m, mid=mids[m], batch=ln["batch"], D=g["D_us"], x=xin, y=yout,
-                              slo=slo[mi], exec_us=ln["exec_us"]))
+            lanes.append(dict(gid=None, slot=g["slot"], model=m, mid=mids[m], batch=ln["batch"], D=g["D_us"], x=xin,
+                              y=yout, slo=slo[mi], exec_us=ln["exec_us"]))
+    hx = [common.host_input(ln["model"], ln["batch"]) for ln in lanes]          # e2e leg: pinned host buffers
+    hy = [torch.empty(ln["y"].numel(), dtype=torch.float32).pin_memory() for ln in lanes]
+    cs = torch.cuda.Stream()
     torch.cuda.current_stream().synchronize()
+    for g in used:
+        gid, nsm = ctx.create_gpulet(gpu, g["size"])
+        log(f"created gpu-let {gid}: {g['size']}% -> {nsm} SMs")
+        made[gid] = (g["size"], nsm)
+        for ln in lanes:
+            if ln["slot"] == g["slot"]:
+                ln["gid"] = gid
 
     def round_once(collect):
         tickets = {}
@@ -223,8 +239,9 @@ def our_arm(a, world, rank, local, dist):
         if collect is not None:
             collect.append([(tickets[r.ticket], r.t_dequeue_ns, r.t_start_ns, r.t_end_ns) for r in recs])
 
-    for _ in range(a.warmup):
+    for w in range(a.warmup):
         round_once(None)
+        log(f"warmup round {w} done")
     rounds = []
     if dist:
         dist.barrier()
@@ -257,11 +274,8 @@ def our_arm(a, world, rank, local, dist):
     # ---- e2e leg: host buffers, H2D/D2H inside every step
     e2e = None
     if not a.no_e2e:
-        hx = [common.host_input(ln["model"], ln["batch"]) for ln in lanes]
-        hy = [torch.empty(ln["y"].numel(), dtype=torch.float32).pin_memory() for ln in lanes]
         h2d = sum(t.numel() * t.element_size() for t in hx)
         d2h = sum(t.numel() * 4 for t in hy)
-        cs = torch.cuda.Stream()
         e_sat = e_tot = 0
         t0 = time.perf_counter()
         for _ in range(a.steps):
@@ -347,7 +361,12 @@ def main():
     ap.add_argument("--scenario", default="mix6")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("GL_BENCH_WATCHDOG_S", "1200")), exit=True)
+    global VERBOSE
+    VERBOSE = a.verbose
     world, rank, local = dist_env()
     if a.impl == "reference":
         line = reference_arm(a, world, rank)

@@ -169,16 +169,18 @@ gl_status gl_schedule(const gl_sched_input* in, char* plan_buf, size_t cap, size
 gl_status gl_fit_interference(const double* X, const double* y, int32_t n, double* c);
 
 /* ---- kernel unit entry points (tests; one-shot executor on the whole GPU) ------------ */
-/* D[M,N] = A[M,K] W[N,K]^T + bias (+ res) -> act; A, res, out device pointers (A bf16
- * [M,K], res bf16 [M,N]); W, bias HOST bf16 bits.  act: 0 none 1 relu 2 gelu 3 tanh.
- * swap_ab: weights as the UMMA M operand (small M).  splitk: allow split-K. */
+/* D[M,N] = A[M,K] W[N,K]^T + bias -> act; A, out device pointers (A bf16 [M,K]); W, bias
+ * HOST bf16 bits.  act: 0 none 1 relu 2 gelu 3 tanh.  swap_ab: weights as the UMMA M
+ * operand (small M).  splitk: allow split-K.  a_in_ws: copy A into the executor
+ * workspace first so the TMA operand path (bound tensor map) is exercised. */
 gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A_dev, const uint16_t* W_host, const uint16_t* bias_host,
-                       const void* res_dev, void* out_dev, int32_t M, int32_t N, int32_t K, int32_t act,
-                       int32_t swap_ab, int32_t splitk, int32_t out_fp32);
-/* Conv (NHWC bf16 x [N,H,W,C], C % 8 == 0; W host OHWI [Cout,KH,KH,C]) + bias + act -> y. */
+                       void* out_dev, int32_t M, int32_t N, int32_t K, int32_t act, int32_t swap_ab, int32_t splitk,
+                       int32_t out_fp32, int32_t a_in_ws);
+/* Conv (NHWC bf16 x [N,H,W,C], C % 8 == 0; W host OHWI [Cout,KH,KH,C]) + bias + act -> y.
+ * x_in_ws: stage x in the workspace (TMA 2-D / im2col operand paths). */
 gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x_dev, const uint16_t* W_host, const uint16_t* bias_host,
                        void* y_dev, int32_t N, int32_t H, int32_t W, int32_t C, int32_t Cout, int32_t KH,
-                       int32_t stride, int32_t pad, int32_t act);
+                       int32_t stride, int32_t pad, int32_t act, int32_t x_in_ws);
 /* Misc CUDA-core op (type = executor op id: 2 dwconv, 3 maxpool, 4 avgpool, 7 layernorm,
  * 8 attention, 9 softmax) with integer args `iargs` and host bf16 params. */
 gl_status gl_test_misc(gl_ctx* ctx, int gpu, int32_t type, const int32_t* iargs, int32_t n_iargs,

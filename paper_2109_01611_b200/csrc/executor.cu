@@ -49,11 +49,23 @@ struct Smem {
   uint64_t* tempty;
   uint32_t* tmem_base;
   uint8_t* scratch;  // non-GEMM ops reuse the stage area
+  uint64_t* att;     // attention barriers: [0] Q/K/V landed, [1] S = QK^T done, [2] O = PV done
+  int* epi_flag;     // epilogue broadcast word (split-K last arriver)
+  uint64_t* dbg;     // optional per-step role stamps of CTA 0 (one-shot trace mode)
+  int step;          // current step index (for dbg)
 };
+
+// CTA 0 role stamps: [0] producer first tile start, [1] producer all issued,
+// [2] MMA first stage acquired, [3] MMA last commit, [4] epilogue first tfull,
+// [5] epilogue done, [6] CTA at barrier, [7] barrier released.
+__device__ __forceinline__ void dbg_mark(const Smem& S, int k) {
+  if (S.dbg && blockIdx.x == 0 && S.step < 1000) S.dbg[S.step * 8 + k] = globaltimer();
+}
 
 struct Pipe {
   uint32_t stage = 0, phase = 0;  // smem ring position (producer / MMA each keep their own)
   uint32_t acc = 0;               // accumulator uses (MMA / epilogue each keep their own)
+  uint32_t att_phase = 0;         // attention barrier parity (every thread tracks it)
   int npend = 0;
   uint32_t pend[kLag];
 };
@@ -191,25 +203,55 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   if (warp < 4) {
     // ---------------- producers
     const int t = threadIdx.x;
+    if (t == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const OpDesc* op = ops + locate(ops, nops, tile, lt);
       const GemmArgs& g = op->g;
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
+      const bool gather = g.a_tma == SRC_GATHER || g.b_tma == SRC_GATHER;
+      if (!gather && P.npend) {
+        // a TMA-only tile follows gathered ones: publish the lagged stages first
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        for (int i = 0; i < P.npend; ++i) mbar_arrive(&S.full[P.pend[i]]);
+        P.npend = 0;
+      }
       const Gather& gg = g.a_tma ? g.gb : g.ga;
       const int grows = g.a_tma ? g.BN : 128;
       const int grow0 = g.a_tma ? nb * g.BN : mb * 128;
       const __nv_bfloat16* gx = (const __nv_bfloat16*)res(gg.x, X);
       RowCache rc;
-      rowcache_init(rc, gg, grow0, grows, t);
+      if (gather) rowcache_init(rc, gg, grow0, grows, t);
+      // im2col traversal start: window top-left of the tile's first output pixel
+      int icw = 0, ich = 0, icn = 0;
+      if (g.a_tma == SRC_IM2COL && t == 0) {
+        const int m0 = mb * 128, HoWo = g.ga.Ho * g.ga.Wo;
+        icn = m0 / HoWo;
+        const int rem = m0 - icn * HoWo, ho = rem / g.ga.Wo, wo = rem - ho * g.ga.Wo;
+        ich = ho * g.ga.stride - g.ga.pad;
+        icw = wo * g.ga.stride - g.ga.pad;
+      }
       const uint32_t tx = (g.a_tma ? 128 * 128 : 0) + (g.b_tma ? g.BN * 128 : 0);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&S.empty[P.stage], P.phase ^ 1);
         if (t == 0) {
           mbar_arrive_expect_tx(&S.full[P.stage], tx);
-          if (g.a_tma) tma_load_2d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+          if (g.a_tma == SRC_TMA) {
+            tma_load_2d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+          } else if (g.a_tma == SRC_IM2COL) {
+            const int k0 = kb * 64, tap = k0 / g.ga.C, c0 = k0 - tap * g.ga.C;
+            const int kh = tap / g.ga.KW, kw = tap - kh * g.ga.KW;
+            tma_load_im2col_4d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], c0, icw, ich, icn,
+                               (uint16_t)kw, (uint16_t)kh);
+          }
           if (g.b_tma) tma_load_2d(smem_u32(S.b[P.stage]), &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
+        }
+        if (!gather) {
+          mbar_arrive(&S.full[P.stage]);
+          advance(P);
+          continue;
         }
         gather_kblock(gg, gx, rc, grows, kb, g.K_real, smem_u32(g.a_tma ? S.b[P.stage] : S.a[P.stage]), t);
         cp_async_commit();
@@ -229,6 +271,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     fence_proxy_async_smem();
     for (int i = 0; i < P.npend; ++i) mbar_arrive(&S.full[P.pend[i]]);
     P.npend = 0;
+    if (t == 0) dbg_mark(S, 1);
   } else if (warp == 8) {
     // ---------------- MMA issuer
     if (lane == 0) {
@@ -247,6 +290,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&S.full[P.stage], P.phase);
           tc_fence_after();
+          if (tile == (int)blockIdx.x && kb == kb0) dbg_mark(S, 2);
           const uint32_t a0 = smem_u32(S.a[P.stage]), b0 = smem_u32(S.b[P.stage]);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -258,6 +302,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         umma_commit(&S.tfull[acc]);
         ++P.acc;
       }
+      dbg_mark(S, 3);
     }
     __syncwarp();
   } else {
@@ -274,6 +319,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const uint32_t acc = P.acc & 1, use = P.acc >> 1;
       mbar_wait(&S.tfull[acc], use & 1);
       tc_fence_after();
+      if (tile == (int)blockIdx.x && q == 0 && lane == 0) dbg_mark(S, 4);
       const int m = mb * 128 + q * 32 + lane;
       const int nend = min(g.N, (nb + 1) * g.BN);
       float* ws = (float*)res(e.ws, X);
@@ -282,16 +328,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
       const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
       __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
-      for (int j = 0; j < g.BN; j += 32) {
-        float v[32];
-        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
-        const int n0 = nb * g.BN + j;
-        if (m >= g.M || n0 >= nend) continue;
-        if (e.splitk > 1) {
-          // split-K partials: plain stores into ws[split][M][N], summed in order by the finalize op
-          float* wp = ws + ((int64_t)(kb0 / g.kb_per_split) * g.M + m) * g.N;
-          for (int c = 0; c < 32 && n0 + c < nend; ++c) wp[n0 + c] = v[c];
-        } else if (vec && n0 + 32 <= nend) {
+      // bias / residual / activation / store of 32 consecutive output columns
+      auto finish_chunk = [&](int n0, const float* v) {
+        if (vec && n0 + 32 <= nend) {
           const int64_t o0 = (int64_t)m * e.ldc + e.col_off + n0;
           __align__(16) __nv_bfloat16 r[32];
           if (rsd) {
@@ -311,11 +350,62 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         } else {
           for (int c = 0; c < 32 && n0 + c < nend; ++c) store_one(e, X, m, n0 + c, v[c]);
         }
+      };
+      if (e.splitk <= 1) {
+        for (int j = 0; j < g.BN; j += 32) {
+          float v[32];
+          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
+          const int n0 = nb * g.BN + j;
+          if (m < g.M && n0 < nend) finish_chunk(n0, v);
+        }
+        tc_fence_before();
+        mbar_arrive(&S.tempty[acc]);
+        ++P.acc;
+      } else {
+        // split-K: store this split's fp32 partial tile; the last split of the
+        // tile to arrive sums all partials in split order and runs the epilogue
+        // (no separate reduction step).
+        const int split = kb0 / g.kb_per_split;
+        float* wp = ws + ((int64_t)split * g.M + m) * g.N;
+        for (int j = 0; j < g.BN; j += 32) {
+          float v[32];
+          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
+          const int n0 = nb * g.BN + j;
+          if (m < g.M && n0 < nend)
+            for (int c = 0; c < 32 && n0 + c < nend; ++c) wp[n0 + c] = v[c];
+        }
+        tc_fence_before();
+        mbar_arrive(&S.tempty[acc]);
+        ++P.acc;
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          int* cnt = (int*)res(e.cnt, X) + mb + nb * g.n_mblk;
+          const int old = atomicAdd(cnt, 1);
+          const bool last = old == g.splits - 1;
+          if (last) *cnt = 0;   // self-reset for the next run of the program
+          *S.epi_flag = last ? 1 : 0;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (*(volatile int*)S.epi_flag) {
+          __threadfence();
+          for (int j = 0; j < g.BN; j += 32) {
+            const int n0 = nb * g.BN + j;
+            if (m >= g.M || n0 >= nend) continue;
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = 0.f;
+            for (int s = 0; s < g.splits; ++s) {
+              const volatile float* pp = ws + ((int64_t)s * g.M + m) * g.N + n0;
+              for (int c = 0; c < 32 && n0 + c < nend; ++c) v[c] += pp[c];
+            }
+            finish_chunk(n0, v);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-      tc_fence_before();
-      mbar_arrive(&S.tempty[acc]);
-      ++P.acc;
     }
+    if (q == 0 && lane == 0) dbg_mark(S, 5);
   }
 }
 
@@ -492,22 +582,31 @@ __device__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
       p2[i] = m;   // NHWC flatten (h, w, c)
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < 120; j += blockDim.x) {
-      float s = __bfloat162float(fb1[j]);
-      for (int k = 0; k < 400; ++k) s = fmaf(p2[k], __bfloat162float(f1[j * 400 + k]), s);
-      h1[j] = bfr(fmaxf(s, 0.f));
+    // fully connected layers: one warp per output neuron, lanes stride over k
+    // (coalesced weight rows), shuffle reduction
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < 120; j += nw) {
+      float s = 0.f;
+      for (int k = lane; k < 400; k += 32) s = fmaf(p2[k], __bfloat162float(f1[j * 400 + k]), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) h1[j] = bfr(fmaxf(s + __bfloat162float(fb1[j]), 0.f));
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < 84; j += blockDim.x) {
-      float s = __bfloat162float(fb2[j]);
-      for (int k = 0; k < 120; ++k) s = fmaf(h1[k], __bfloat162float(f2[j * 120 + k]), s);
-      h2[j] = bfr(fmaxf(s, 0.f));
+    for (int j = warp; j < 84; j += nw) {
+      float s = 0.f;
+      for (int k = lane; k < 120; k += 32) s = fmaf(h1[k], __bfloat162float(f2[j * 120 + k]), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) h2[j] = bfr(fmaxf(s + __bfloat162float(fb2[j]), 0.f));
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < 10; j += blockDim.x) {
-      float s = __bfloat162float(fb3[j]);
-      for (int k = 0; k < 84; ++k) s = fmaf(h2[k], __bfloat162float(f3[j * 84 + k]), s);
-      y[(int64_t)n * 10 + j] = s;
+    for (int j = warp; j < 10; j += nw) {
+      float s = 0.f;
+      for (int k = lane; k < 84; k += 32) s = fmaf(h2[k], __bfloat162float(f3[j * 84 + k]), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) y[(int64_t)n * 10 + j] = s + __bfloat162float(fb3[j]);
     }
     __syncthreads();
   }
@@ -681,6 +780,102 @@ __device__ void attention(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
   }
 }
 
+// Tensor-core attention (K9): one (sequence, head) unit per CTA iteration.
+// TMA brings Q, K, V [128 x 64] (128B-swizzled) from the bound qkv tensor map;
+// S = Q K^T is one 128x128x64 UMMA into TMEM columns [0,128); the epilogue warps
+// (one query row per thread) read S three times (max, sum, normalise), write
+// P = softmax(S/8) as bf16 into smem in the UMMA K-major layout; O = P V is a
+// 128x64x128 UMMA with V as an MN-major B operand into TMEM columns [128,192);
+// O is rounded to bf16 and stored.  Rounding points match the oracle (C1.4).
+__device__ void attention_tc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P) {
+  const MiscArgs& a = op->m;
+  __nv_bfloat16* ctx = (__nv_bfloat16*)res(a.y, X);
+  const int H = a.heads, units = a.N * H, HD = H * 64;
+  uint8_t *sQ = S.a[0], *sK = S.a[1], *sV = S.a[2], *sP = S.b[0];
+  const uint32_t tbase = *S.tmem_base;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int seq = u / H, h = u - seq * H, row0 = seq * 128;
+    const uint32_t ph = P.att_phase & 1;
+    if (t == 0) {
+      mbar_arrive_expect_tx(&S.att[0], 3 * 16384);
+      tma_load_2d(smem_u32(sQ), &op->tmap_a, &S.att[0], h * 64, row0);
+      tma_load_2d(smem_u32(sK), &op->tmap_a, &S.att[0], HD + h * 64, row0);
+      tma_load_2d(smem_u32(sV), &op->tmap_a, &S.att[0], 2 * HD + h * 64, row0);
+    }
+    if (warp == 8 && lane == 0) {
+      mbar_wait(&S.att[0], ph);
+      tc_fence_after();
+      const uint32_t idesc = umma_idesc_bf16(128, 128);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        umma_bf16(tbase, umma_sdesc_sw128(smem_u32(sQ) + k * 32), umma_sdesc_sw128(smem_u32(sK) + k * 32), idesc,
+                  k > 0 ? 1u : 0u);
+      umma_commit(&S.att[1]);
+    }
+    if (warp >= 4 && warp < 8) {
+      const int q = warp - 4, r = q * 32 + lane;
+      mbar_wait(&S.att[1], ph);
+      tc_fence_after();
+      const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16);
+      float v[32];
+      float mx = -INFINITY;
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(ta + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v[i] * 0.125f);
+      }
+      float sum = 0.f;
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(ta + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sum += expf(v[i] * 0.125f - mx);
+      }
+      const float inv = 1.f / sum;
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(ta + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __align__(16) __nv_bfloat16 pb[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pb[e] = __float2bfloat16_rn(expf(v[j * 8 + e] * 0.125f - mx) * inv);
+          const int chunk = (c & 1) * 4 + j;   // 16-byte chunk (8 keys) within the 64-key block
+          *(uint4*)(sP + (c >> 1) * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4)) = *(const uint4*)pb;
+        }
+      }
+      fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (warp == 8 && lane == 0) {
+      tc_fence_after();
+      const uint32_t idesc = umma_idesc_bf16(128, 64) | (1u << 16);   // B (V) is MN-major
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16(tbase + 128, umma_sdesc_sw128(smem_u32(sP) + (kk >> 2) * 16384 + (kk & 3) * 32),
+                  umma_sdesc_sw128(smem_u32(sV) + kk * 2048), idesc, kk > 0 ? 1u : 0u);
+      umma_commit(&S.att[2]);
+    }
+    if (warp >= 4 && warp < 8) {
+      const int q = warp - 4, r = q * 32 + lane;
+      mbar_wait(&S.att[2], ph);
+      tc_fence_after();
+      float v[32];
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + 128 + c * 32, v);
+        __align__(16) __nv_bfloat16 ob[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ob[i] = __float2bfloat16_rn(v[i]);
+        uint4* dst = (uint4*)(ctx + (int64_t)(row0 + r) * HD + h * 64 + c * 32);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[k] = ((const uint4*)ob)[k];
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    ++P.att_phase;
+  }
+}
+
 // ------------------------------------------------------------------ row softmax (K11)
 __device__ void softmax_rows(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
@@ -696,7 +891,11 @@ __device__ void softmax_rows(const OpDesc* op, const Ctx& X) {
   }
 }
 
-__device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S) {
+__device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P) {
+  if (op->type == OP_ATTENTION && op->g.act_tmap) {   // qkv tensor map bound: tensor-core path
+    attention_tc(op, X, S, P);
+    return;
+  }
   switch (op->type) {
     case OP_DWCONV: dwconv(op, X); break;
     case OP_MAXPOOL: maxpool(op, X); break;
@@ -711,21 +910,25 @@ __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S) {
   }
 }
 
-__device__ void run_program(const WorkDesc& w, const Ctx& X, const Smem& S, Pipe& P, ExecState* st,
+__device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, ExecState* st,
                             uint64_t& epoch, uint64_t* trace, int trace_cap) {
   int i = 0, step = 0;
   const bool tr = trace && blockIdx.x == 0 && threadIdx.x == 0;
   if (tr && trace_cap > 0) trace[0] = globaltimer();
+  S.dbg = (trace && trace_cap >= 1024 + 8 * 1000) ? trace + 1024 : nullptr;
   while (i < w.n_ops) {
     int j = i;
     while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
+    S.step = step;
     if (w.prog[i].type == OP_GEMM) {
       gemm_step(w.prog + i, j - i + 1, X, S, P);
     } else {
-      for (int k = i; k <= j; ++k) run_misc(w.prog + k, X, S);
+      for (int k = i; k <= j; ++k) run_misc(w.prog + k, X, S, P);
     }
     fence_proxy_async_smem();
+    if (threadIdx.x == 0) dbg_mark(S, 6);
     gridsync(st, epoch, false);
+    if (threadIdx.x == 0) dbg_mark(S, 7);
     ++step;
     if (tr && step < trace_cap) trace[step] = globaltimer();
     i = j + 1;
@@ -747,8 +950,12 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.empty = bars + kStages;
   S.tfull = bars + 2 * kStages;
   S.tempty = bars + 2 * kStages + 2;
-  S.tmem_base = (uint32_t*)(bars + 2 * kStages + 4);
+  S.att = bars + 2 * kStages + 4;
+  S.tmem_base = (uint32_t*)(bars + 2 * kStages + 7);
+  S.epi_flag = (int*)(bars + 2 * kStages + 8);
   S.scratch = base;
+  S.dbg = nullptr;
+  S.step = 0;
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -760,6 +967,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
       mbar_init(&S.tfull[s], 1);
       mbar_init(&S.tempty[s], 128);
     }
+    for (int s = 0; s < 3; ++s) mbar_init(&S.att[s], 1);
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc(S.tmem_base, 512);

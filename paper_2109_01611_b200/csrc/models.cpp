@@ -162,7 +162,9 @@ struct Act {
 
 class Builder {
  public:
-  Builder(const ParamMap& P, DevWeights& dw, int batch, Program& prog) : P(P), dw(dw), b(batch), prog(prog) {}
+  Builder(const ParamMap& P, DevWeights& dw, int batch, Program& prog) : P(P), dw(dw), b(batch), prog(prog) {
+    alloc(64 * 1024);   // offset 0: split-K tile counters (zeroed with the workspace, self-resetting)
+  }
 
   const ParamMap& P;
   DevWeights& dw;
@@ -255,8 +257,20 @@ class Builder {
     g.BN = std::max(16, rup((g.N + nnb - 1) / nnb, 16));
     g.n_nblk = (g.N + g.BN - 1) / g.BN;
     g.n_mblk = (M + 127) / 128;
-    g.a_tma = 0;
-    g.b_tma = 1;
+    g.a_tma = SRC_GATHER;
+    g.b_tma = SRC_TMA;
+    // workspace activations are fetched by TMA (tensor map bound per workspace):
+    // 2-D tiles for 1x1/stride-1 convs and linears, im2col mode for KxK or
+    // strided convs with 64-channel-aligned inputs; the rest is gathered.
+    if (ga.x.kind == BUF_WS && ga.C % 8 == 0 && ga.lda % 8 == 0) {
+      if (ga.KH == 1 && ga.stride == 1 && ga.pad == 0) {
+        g.a_tma = SRC_TMA;
+        g.act_tmap = 1;
+      } else if (ga.C % 64 == 0 && ga.lda == ga.C) {
+        g.a_tma = SRC_IM2COL;
+        g.act_tmap = 1;
+      }
+    }
     g.ga = ga;
     g.ga.rows = M;
     ep.bias = abs_ref(bias);
@@ -281,8 +295,12 @@ class Builder {
     g.BN = std::max(16, rup(nrows, 16));
     g.n_nblk = 1;
     g.n_mblk = (g.M + 127) / 128;
-    g.a_tma = 1;
-    g.b_tma = 0;
+    g.a_tma = SRC_TMA;
+    g.b_tma = SRC_GATHER;
+    if (gb.x.kind == BUF_WS && gb.C % 8 == 0 && gb.lda % 8 == 0) {
+      g.b_tma = SRC_TMA;
+      g.act_tmap = 1;
+    }
     g.gb = gb;
     g.gb.rows = nrows;
     ep.bias = abs_ref(bias);
@@ -323,25 +341,18 @@ class Builder {
       PendingFinal f{g.ep, g.M, g.N, g.splits, ws};
       g.ep.splitk = g.splits;
       g.ep.ws = ws_ref(ws);
+      // per-tile arrival counters in the reserved zero region (tiles < 256 by choose_split)
+      g.ep.cnt = ws_ref((uint64_t)((n_split_ops++) % 64) * 256 * 4);
       finals.push_back(f);
     }
   }
+  int n_split_ops = 0;
 
-  // Emit finalize ops for split-K GEMMs of the previous step (call after step()).
+  // Split-K partial buffers die with their step: the last-arriving split of
+  // each tile reduces in-kernel (no finalize step).  Call after step().
   void flush_finals() {
-    if (finals.empty()) return;
-    for (auto& f : finals) {
-      OpDesc& op = add(OP_SPLITK_FINAL);
-      op.m.rows = f.M;
-      op.m.cols = f.N;
-      op.m.ep = f.ep;
-      op.m.ep.splitk = f.splits;
-      op.m.ep.ws = ws_ref(f.ws);
-      op.n_units = 1;
-      release_off(f.ws);
-    }
+    for (auto& f : finals) release_off(f.ws);
     finals.clear();
-    step();
   }
 
   static Gather conv_gather(const Act& x, int KH, int stride, int pad, int Ho, int Wo) {
@@ -765,6 +776,8 @@ static void build_bert(Builder& B, size_t& in_b, size_t& out_b) {
       op.m.seq = S;
       op.m.heads = 12;
       op.m.dh = 64;
+      op.m.rows = M;
+      op.g.act_tmap = 1;   // qkv [M, 2304] is workspace-resident: TMA + tcgen05 attention
       op.n_units = b * 12;
       B.prog.flops += 2.0 * 2 * b * 12 * S * S * 64;
     }
@@ -851,7 +864,7 @@ bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, in
 
 // ------------------------------------------------------------------ single-op test programs
 bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int out_fp32, const uint16_t* w_host,
-                     const uint16_t* b_host, int has_res, DevWeights& dw, Program& out, std::string& err) {
+                     const uint16_t* b_host, int in_ws, DevWeights& dw, Program& out, std::string& err) {
   out = Program();
   ParamMap P;
   Param w, bb;
@@ -864,18 +877,19 @@ bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int 
   Builder B(P, dw, M, out);
   WRef wr = fc_weight(dw, P, "t", B.e);
   void* bias = raw_param(dw, P, "t.b", B.e);
-  // input: BUF_IN [M, K] bf16; residual BUF_IN after it ([M, N]); output BUF_OUT [M, N]
+  // input: [M, K] bf16 (BUF_IN, or copied to workspace offset 0); output BUF_OUT [M, N]
+  BufRef x = in_ref(0);
+  if (in_ws) {
+    x = ws_ref(B.alloc((uint64_t)M * K * 2));
+    out.in_copy_bytes = (size_t)M * K * 2;
+  }
   Epilogue ep = Builder::plain_ep(out_ref(0), N, 0);
   ep.act = act;
   ep.out_fp32 = out_fp32;
-  if (has_res) ep.res = in_ref((uint64_t)M * K * 2);
   if (swap_ab) {
-    B.gemm_swap(Builder::mat_gather(in_ref(0), K, K), M, wr, bias, ep);
+    B.gemm_swap(Builder::mat_gather(x, K, K), M, wr, bias, ep);
   } else {
-    B.gemm_gather_a(Builder::mat_gather(in_ref(0), K, K), M, wr, bias, ep, splitk != 0);
-  }
-  if (!splitk && !swap_ab) {
-    // force no split
+    B.gemm_gather_a(Builder::mat_gather(x, K, K), M, wr, bias, ep, splitk != 0);
   }
   B.step();
   B.flush_finals();
@@ -887,7 +901,8 @@ bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int 
 }
 
 bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, int pad, int act,
-                     const uint16_t* w_host, const uint16_t* b_host, DevWeights& dw, Program& out, std::string& err) {
+                     const uint16_t* w_host, const uint16_t* b_host, int in_ws, DevWeights& dw, Program& out,
+                     std::string& err) {
   out = Program();
   ParamMap P;
   Param w, bb;
@@ -899,6 +914,10 @@ bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, i
   P["t.b"] = bb;
   Builder B(P, dw, N, out);
   Act x = input_act(N, H, W, C);
+  if (in_ws) {
+    out.in_copy_bytes = (size_t)N * H * W * C * 2;
+    x.ref = ws_ref(B.alloc(out.in_copy_bytes));
+  }
   const int Ho = (H + 2 * pad - KH) / stride + 1, Wo = (W + 2 * pad - KH) / stride + 1;
   Act y;
   y.ref = out_ref(0);
@@ -966,10 +985,19 @@ bool build_test_misc(int type, const int* ia, int n, const uint16_t* w_host, siz
     op.n_units = 1;
   } else if (type == OP_ATTENTION) {
     if (!need(1)) return false;
+    // iargs: nseq [, tensor_core]; the tensor-core path reads qkv from the workspace
+    const bool tc = n < 2 || ia[1] != 0;
+    const uint64_t qkv_bytes = (uint64_t)ia[0] * 128 * 2304 * 2;
     OpDesc& op = B.add(OP_ATTENTION);
     op.m.x = in_ref(0);
+    if (tc) {
+      op.m.x = ws_ref(B.alloc(qkv_bytes));
+      out.in_copy_bytes = qkv_bytes;
+      op.g.act_tmap = 1;
+    }
     op.m.y = out_ref(0);
     op.m.N = ia[0];
+    op.m.rows = ia[0] * 128;
     op.m.seq = 128;
     op.m.heads = 12;
     op.m.dh = 64;
@@ -997,6 +1025,73 @@ bool build_test_misc(int type, const int* ia, int n, const uint16_t* w_host, siz
 }  // namespace gl
 
 namespace gl {
+// Encode the tensor maps of workspace-resident activation operands for one
+// workspace (TMA descriptors hold absolute addresses).
+bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::string& err) {
+  out = p.ops;
+  Err e;
+  for (OpDesc& op : out) {
+    if (op.type == OP_ATTENTION && op.g.act_tmap) {
+      // qkv [rows, 3 * 768] bf16; box = one head's 64 columns x 128 tokens
+      if (op.m.x.kind != BUF_WS) {
+        err = "bind: attention qkv not in the workspace";
+        return false;
+      }
+      const int hd3 = 3 * op.m.heads * op.m.dh;
+      cuuint64_t dims[2] = {(cuuint64_t)hd3, (cuuint64_t)op.m.rows};
+      cuuint64_t strides[1] = {(cuuint64_t)hd3 * 2};
+      cuuint32_t box[2] = {64, 128};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = driver().tensorMapEncodeTiled(&op.tmap_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ws + op.m.x.off,
+                                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        err = "bind: attention tensor map encode failed";
+        return false;
+      }
+      continue;
+    }
+    if (op.type != OP_GEMM || !op.g.act_tmap) continue;
+    GemmArgs& g = op.g;
+    const bool swap = g.a_tma == SRC_TMA && g.b_tma == SRC_TMA && g.ep.transpose;
+    const Gather& x = swap ? g.gb : g.ga;
+    if (x.x.kind != BUF_WS) return e.fail("bind: activation operand not in the workspace"), err = e.msg, false;
+    char* base = ws + x.x.off;
+    CUtensorMap* map = swap ? &op.tmap_b : &op.tmap_a;
+    Driver& D = driver();
+    CUresult r;
+    if ((swap ? g.b_tma : g.a_tma) == SRC_TMA) {
+      // [rows, C] matrix with row stride lda; box 64 x (128 or BN)
+      cuuint64_t dims[2] = {(cuuint64_t)x.C, (cuuint64_t)x.rows};
+      cuuint64_t strides[1] = {(cuuint64_t)x.lda * 2};
+      cuuint32_t box[2] = {64, (cuuint32_t)(swap ? g.BN : 128)};
+      cuuint32_t es[2] = {1, 1};
+      r = D.tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      // NHWC im2col: dims {C, W, H, N}; window top-left positions of the
+      // output pixels span [-pad, -pad + (O-1) * stride] in W and H.
+      if (!D.tensorMapEncodeIm2col) return e.fail("cuTensorMapEncodeIm2col unavailable"), err = e.msg, false;
+      const int nimg = x.rows / (x.Ho * x.Wo);
+      cuuint64_t dims[4] = {(cuuint64_t)x.C, (cuuint64_t)x.W, (cuuint64_t)x.H, (cuuint64_t)nimg};
+      cuuint64_t strides[3] = {(cuuint64_t)x.C * 2, (cuuint64_t)x.W * x.C * 2, (cuuint64_t)x.H * x.W * x.C * 2};
+      int lower[2] = {-x.pad, -x.pad};
+      int upper[2] = {-x.pad + (x.Wo - 1) * x.stride - (x.W - 1), -x.pad + (x.Ho - 1) * x.stride - (x.H - 1)};
+      cuuint32_t es[4] = {1, (cuuint32_t)x.stride, (cuuint32_t)x.stride, 1};
+      r = D.tensorMapEncodeIm2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, lower, upper, 64, 128,
+                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) {
+      err = "bind: tensor map encode failed (" + std::to_string((int)r) + ")";
+      return false;
+    }
+  }
+  return true;
+}
+
 // Algorithmic cost of one op: FLOPs (2 x MACs of the contraction) and the bytes
 // it must move at minimum (weights + input activations + outputs, each once).
 void op_cost(const OpDesc& op, double& flops, double& bytes) {

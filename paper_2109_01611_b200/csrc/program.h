@@ -25,6 +25,9 @@ enum OpType : int32_t {
 };
 
 enum BufKind : int32_t { BUF_NONE = 0, BUF_WS = 1, BUF_IN = 2, BUF_OUT = 3, BUF_ABS = 4 };
+// GEMM operand sources: cp.async implicit-im2col gather by the producer warps,
+// 2-D tiled TMA, or TMA im2col mode (NHWC, 64 channels x 128 pixels per load).
+enum OperandSrc : int32_t { SRC_GATHER = 0, SRC_TMA = 1, SRC_IM2COL = 2 };
 enum Activation : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_GELU = 2, ACT_TANH = 3 };
 
 struct BufRef {
@@ -49,7 +52,8 @@ struct Epilogue {
   BufRef out;
   BufRef bias;                // bf16 [N] (or [M] when bias_on_m)
   BufRef res;                 // bf16 residual, same mapping as out
-  BufRef ws;                  // fp32 split-K workspace [M, N]
+  BufRef ws;                  // fp32 split-K partials [splits][M][N]
+  BufRef cnt;                 // int32 per-tile arrival counters (split-K last-arriver reduction)
   int64_t img_stride;         // out element index = (r / rows_per_img) * img_stride
   int32_t rows_per_img;       //   + (r % rows_per_img) * ldc + col_off + c
   int32_t ldc, col_off;
@@ -64,8 +68,8 @@ struct GemmArgs {
   int32_t M, N, K_real, K_pad;  // D[M,N] = A[M,K] B[N,K]^T
   int32_t BN;                   // UMMA N of this op (multiple of 16, <= 256)
   int32_t n_mblk, n_nblk, splits, kb_per_split;
-  int32_t a_tma, b_tma;         // operand source: 1 = TMA tensor map, 0 = gather
-  int32_t pad_;
+  int32_t a_tma, b_tma;         // operand source: SRC_GATHER / SRC_TMA / SRC_IM2COL
+  int32_t act_tmap;             // 1: the activation operand's tensor map is bound per workspace
   Gather ga, gb;                // gather geometry (used when *_tma == 0)
   Epilogue ep;
 };

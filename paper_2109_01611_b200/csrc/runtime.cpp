@@ -51,6 +51,7 @@ Driver& driver() {
     };
     bool ok = true;
     ok &= get("cuTensorMapEncodeTiled", (void**)&d.tensorMapEncodeTiled);
+    ok &= get("cuTensorMapEncodeIm2col", (void**)&d.tensorMapEncodeIm2col);
     ok &= get("cuDeviceGetDevResource", (void**)&d.deviceGetDevResource);
     ok &= get("cuDevSmResourceSplitByCount", (void**)&d.devSmResourceSplitByCount);
     ok &= get("cuDevResourceGenerateDesc", (void**)&d.devResourceGenerateDesc);
@@ -186,7 +187,33 @@ struct Gpulet {
   bool uses_rem = false;
 };
 
+// Upload a program bound to workspace `ws` (tensor maps of workspace operands).
+static OpDesc* upload_bound(const Program& p, char* ws, std::string& err) {
+  std::vector<OpDesc> ops;
+  if (!bind_program(p, ws, ops, err)) return nullptr;
+  OpDesc* d = nullptr;
+  if (cudaMalloc(&d, ops.size() * sizeof(OpDesc)) != cudaSuccess) {
+    err = "cudaMalloc(program)";
+    return nullptr;
+  }
+  cudaMemcpy(d, ops.data(), ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice);
+  return d;
+}
+
+// Resources of one gpu-let slot of a GPU, reused by successive gpu-lets.
+struct SlotRes {
+  bool ready = false;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  HostRing* ring = nullptr;
+  HostRing* ring_dev = nullptr;
+  ExecState* st = nullptr;
+  int* smid = nullptr;
+  std::map<int, std::vector<OpDesc*>> progs;  // model id -> [batch] programs bound to ws
+};
+
 struct GpuState {
+  SlotRes slot_res[2];
   int dev = 0;
   int nsm = 0;
   bool split = false;
@@ -205,6 +232,7 @@ struct gl_ctx {
   std::deque<gl_completion> stash;  // collected by gl_wait, handed out by gl_poll
   std::mutex mu;
   uint64_t next_ticket = 1;
+  uint64_t idle_polls = 0;
   bool poisoned = false;
 };
 
@@ -265,12 +293,13 @@ static gl_status launch_executor(gl_ctx* ctx, int dev, CUstream stream, int grid
 // One-shot run of a program on the whole GPU (kernel unit tests).
 static gl_status run_oneshot(gl_ctx* ctx, int gpu, Program& prog, const void* in, void* out) {
   CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
-  OpDesc* dprog = nullptr;
-  CK(cudaMalloc(&dprog, prog.ops.size() * sizeof(OpDesc)), "cudaMalloc(prog)");
-  CK(cudaMemcpy(dprog, prog.ops.data(), prog.ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice), "memcpy prog");
   char* ws = nullptr;
   CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
   CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
+  if (prog.in_copy_bytes) CK(cudaMemcpy(ws, in, prog.in_copy_bytes, cudaMemcpyDeviceToDevice), "copy input to ws");
+  std::string berr;
+  OpDesc* dprog = upload_bound(prog, ws, berr);
+  if (!dprog) return fail(GL_E_CUDA, berr);
   HostRing* ring = nullptr;
   CK(cudaHostAlloc((void**)&ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
   std::memset((void*)ring, 0, sizeof(HostRing));
@@ -346,6 +375,19 @@ gl_status gl_shutdown(gl_ctx* ctx) {
     for (int b = 1; b <= 32; ++b)
       if (m->prog[b].dev) release_device(m->prog[b].dev, false);
     m->w.reset();
+  }
+  for (auto& G : ctx->gpus) {
+    cudaSetDevice(G.dev);
+    for (auto& R : G.slot_res) {
+      if (!R.ready) continue;
+      for (auto& kv : R.progs)
+        for (OpDesc* p : kv.second) release_device(p, false);
+      release_device(R.ws, false);
+      release_device(R.st, false);
+      release_device(R.smid, false);
+      release_device(R.ring, true);
+      R = SlotRes();
+    }
   }
   delete ctx;
   return GL_OK;
@@ -460,22 +502,51 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     for (int i : g->groups) G.used_groups |= (1u << i);
     if (g->uses_rem) G.rem_used = true;
   }
-  // workspace: the largest program of any model loaded on this GPU
-  size_t ws = 256;
-  for (auto& m : ctx->models)
-    if (m && m->gpu == gpu)
-      for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
-  g->ws_bytes = ws;
-  CK(cudaMalloc(&g->ws, ws), "cudaMalloc(workspace)");
-  CK(cudaMemset(g->ws, 0, ws), "memset(workspace)");
-  CK(cudaHostAlloc((void**)&g->ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+  // Per-slot resources (workspace, bound programs, rings) are allocated for
+  // both slots the first time a gpu-let is created on this GPU, while no
+  // executor runs there: device allocations can synchronise the device and
+  // would block behind a persistent executor.
+  if (!G.slot_res[0].ready) {
+    size_t ws = 256;
+    for (auto& m : ctx->models)
+      if (m && m->gpu == gpu)
+        for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
+    for (int s = 0; s < 2; ++s) {
+      SlotRes& R = G.slot_res[s];
+      R.ws_bytes = ws;
+      CK(cudaMalloc(&R.ws, ws), "cudaMalloc(workspace)");
+      CK(cudaMemset(R.ws, 0, ws), "memset(workspace)");
+      for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+        auto& m = ctx->models[mi];
+        if (!m || m->gpu != gpu) continue;
+        std::vector<OpDesc*>& v = R.progs[(int)mi];
+        v.assign(33, nullptr);
+        for (int b = 1; b <= 32; ++b) {
+          std::string berr;
+          v[b] = upload_bound(m->prog[b], R.ws, berr);
+          if (!v[b]) return fail(GL_E_CUDA, "gl_create_gpulet: " + berr);
+        }
+      }
+      CK(cudaHostAlloc((void**)&R.ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+      CK(cudaHostGetDevicePointer((void**)&R.ring_dev, R.ring, 0), "cudaHostGetDevicePointer");
+      CK(cudaMalloc(&R.st, sizeof(ExecState)), "cudaMalloc(state)");
+      CK(cudaMalloc(&R.smid, 160 * sizeof(int)), "cudaMalloc(smid)");
+      R.ready = true;
+    }
+    CK(cudaDeviceSynchronize(), "slot resources");
+  }
+  SlotRes& R = G.slot_res[slot];
+  for (auto& old : ctx->gpulets)   // a previous gpu-let of this slot gives its ring back
+    if (old && old->gpu == gpu && old->slot == slot) old->ring = nullptr;
+  g->ws = R.ws;
+  g->ws_bytes = R.ws_bytes;
+  g->ring = R.ring;
+  g->ring_dev = R.ring_dev;
+  g->st = R.st;
+  g->smid = R.smid;
   std::memset((void*)g->ring, 0, sizeof(HostRing));
-  CK(cudaHostGetDevicePointer((void**)&g->ring_dev, g->ring, 0), "cudaHostGetDevicePointer");
-  CK(cudaMalloc(&g->st, sizeof(ExecState)), "cudaMalloc(state)");
-  CK(cudaMemset(g->st, 0, sizeof(ExecState)), "memset(state)");
-  CK(cudaMalloc(&g->smid, 160 * sizeof(int)), "cudaMalloc(smid)");
-  CK(cudaMemset(g->smid, 0xff, 160 * sizeof(int)), "memset(smid)");
-  CK(cudaStreamSynchronize(0), "sync before launch");   // legacy stream only: executors are non-blocking
+  CK(cudaMemsetAsync(g->st, 0, sizeof(ExecState), (cudaStream_t)g->stream), "reset state");
+  CK(cudaMemsetAsync(g->smid, 0xff, 160 * sizeof(int), (cudaStream_t)g->stream), "reset smid");
   g->id = (int)ctx->gpulets.size();
   ExecParams p;
   std::memset(&p, 0, sizeof(p));
@@ -540,11 +611,8 @@ gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t id) {
     driver().streamDestroy(g.stream);
   if (g.gctx) driver().greenCtxDestroy(g.gctx);
   --g_live_exec;
-  release_device(g.ws, false);
-  release_device(g.st, false);
-  release_device(g.smid, false);
-  release_device(g.ring, true);
-  g.ring = nullptr;
+  // workspace, programs and rings stay with the slot for the next gpu-let;
+  // completions still in the ring can be polled until the slot is reused
   flush_deferred();
   if (e != cudaSuccess) return cuda_check(ctx, e, "executor");
   return GL_OK;
@@ -570,13 +638,15 @@ gl_status gl_submit_batch(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_
   if (mid < 0 || mid >= (int)ctx->models.size() || ctx->models[mid]->gpu != g.gpu)
     return fail(GL_E_MODEL, "gl_submit_batch: model not loaded on this gpu-let's GPU");
   Model& m = *ctx->models[mid];
-  if (m.prog[batch].ws_bytes > g.ws_bytes)
-    return fail(GL_E_STATE, "gl_submit_batch: model loaded after the gpu-let was created (workspace too small)");
+  auto& progs = ctx->gpus[g.gpu].slot_res[g.slot].progs;
+  auto pit = progs.find(mid);
+  if (pit == progs.end() || m.prog[batch].ws_bytes > g.ws_bytes)
+    return fail(GL_E_STATE, "gl_submit_batch: model loaded after the gpu-let was created");
   if (g.tail - g.comp_seen >= (uint64_t)kRing - 1) return fail(GL_E_QUEUE_FULL, "gl_submit_batch: ring full");
   WorkDesc& w = g.ring->items[g.tail % kRing];
   const uint64_t t = ctx->next_ticket++;
   w.ticket = t;
-  w.prog = m.prog[batch].dev;
+  w.prog = pit->second[batch];
   w.in = in_dev;
   w.out = out_dev;
   w.n_ops = (int)m.prog[batch].ops.size();
@@ -625,8 +695,18 @@ gl_status gl_poll(gl_ctx* ctx, gl_completion* out, int32_t max, int32_t* n_out) 
   }
   n += collect(ctx, out + n, max - n);
   *n_out = n;
-  for (auto& gp : ctx->gpulets)
-    if (gp && gp->alive && gp->ring->error) return fail(GL_E_CUDA, "executor reported a device fault");
+  // an executor that exited while alive (device fault / trap) can never
+  // complete its queued work: report it instead of letting callers spin
+  if (n == 0 && (++ctx->idle_polls & 1023) == 0) {
+    for (auto& gp : ctx->gpulets) {
+      if (!gp || !gp->alive) continue;
+      cudaError_t e = cudaStreamQuery((cudaStream_t)gp->stream);
+      if (e != cudaErrorNotReady) {
+        gp->alive = false;
+        return cuda_check(ctx, e == cudaSuccess ? cudaErrorLaunchFailure : e, "executor exited");
+      }
+    }
+  }
   return GL_OK;
 }
 
@@ -711,32 +791,32 @@ gl_status gl_profile(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32
   return GL_OK;
 }
 
-gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A, const uint16_t* W, const uint16_t* bias, const void* res,
-                       void* out, int32_t M, int32_t N, int32_t K, int32_t act, int32_t swap_ab, int32_t splitk,
-                       int32_t out_fp32) {
+gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A, const uint16_t* W, const uint16_t* bias, void* out,
+                       int32_t M, int32_t N, int32_t K, int32_t act, int32_t swap_ab, int32_t splitk, int32_t out_fp32,
+                       int32_t a_in_ws) {
   if (!ctx || !A || !W || !bias || !out || gpu < 0 || gpu >= (int)ctx->gpus.size() || M < 1 || N < 1 || K < 8 ||
       K % 8)
     return fail(GL_E_ARG, "gl_test_gemm: bad arguments");
-  if (res) return fail(GL_E_ARG, "gl_test_gemm: residual must be passed via the input buffer layout");
   CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
   DevWeights dw;
   Program prog;
   std::string err;
-  if (!build_test_gemm(M, N, K, act, swap_ab, splitk, out_fp32, W, bias, 0, dw, prog, err))
+  if (!build_test_gemm(M, N, K, act, swap_ab, splitk, out_fp32, W, bias, a_in_ws, dw, prog, err))
     return fail(GL_E_ARG, err);
   return run_oneshot(ctx, gpu, prog, A, out);
 }
 
 gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x, const uint16_t* W, const uint16_t* bias, void* y,
                        int32_t N, int32_t H, int32_t Wd, int32_t C, int32_t Cout, int32_t KH, int32_t stride,
-                       int32_t pad, int32_t act) {
+                       int32_t pad, int32_t act, int32_t x_in_ws) {
   if (!ctx || !x || !W || !bias || !y || gpu < 0 || gpu >= (int)ctx->gpus.size() || C % 8)
     return fail(GL_E_ARG, "gl_test_conv: bad arguments");
   CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
   DevWeights dw;
   Program prog;
   std::string err;
-  if (!build_test_conv(N, H, Wd, C, Cout, KH, stride, pad, act, W, bias, dw, prog, err)) return fail(GL_E_ARG, err);
+  if (!build_test_conv(N, H, Wd, C, Cout, KH, stride, pad, act, W, bias, x_in_ws, dw, prog, err))
+    return fail(GL_E_ARG, err);
   return run_oneshot(ctx, gpu, prog, x, y);
 }
 
@@ -765,6 +845,9 @@ extern "C" gl_status gl_run_once(gl_ctx* ctx, int32_t mid, int32_t batch, const 
   char* ws = nullptr;
   CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
   CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
+  std::string berr;
+  OpDesc* bound = upload_bound(prog, ws, berr);
+  if (!bound) return fail(GL_E_CUDA, "gl_run_once: " + berr);
   HostRing* ring = nullptr;
   CK(cudaHostAlloc((void**)&ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
   std::memset((void*)ring, 0, sizeof(HostRing));
@@ -774,12 +857,12 @@ extern "C" gl_status gl_run_once(gl_ctx* ctx, int32_t mid, int32_t batch, const 
   CK(cudaMalloc(&st, sizeof(ExecState)), "cudaMalloc(st)");
   CK(cudaMemset(st, 0, sizeof(ExecState)), "memset st");
   uint64_t* tr = nullptr;
-  const int tcap = 1024;
+  const int tcap = 1024 + 8 * 1000;   // step stamps + CTA-0 role stamps (executor dbg_mark)
   CK(cudaMalloc(&tr, tcap * sizeof(uint64_t)), "cudaMalloc(trace)");
   CK(cudaMemset(tr, 0, tcap * sizeof(uint64_t)), "memset trace");
   WorkDesc& w = ring->items[0];
   w.ticket = 0;
-  w.prog = prog.dev;
+  w.prog = bound;
   w.in = in_dev;
   w.out = out_dev;
   w.n_ops = (int)prog.ops.size();
@@ -807,10 +890,13 @@ extern "C" gl_status gl_run_once(gl_ctx* ctx, int32_t mid, int32_t batch, const 
     std::vector<uint64_t> h(tcap);
     cudaMemcpy(h.data(), tr, tcap * sizeof(uint64_t), cudaMemcpyDeviceToHost);
     for (int i = 0; i < std::min(cap, std::min(steps + 1, tcap)); ++i) trace_ns[i] = h[i];
+    // role stamps follow at trace_ns[1024 + 8 * step + k] when the caller's buffer is large enough
+    for (int i = 1024; i < std::min(cap, tcap); ++i) trace_ns[i] = h[i];
   }
   if (n_steps) *n_steps = steps;
   cudaStreamDestroy(s);
   release_device(tr, false);
+  release_device(bound, false);
   release_device(st, false);
   release_device(ring, true);
   release_device(ws, false);

@@ -16,6 +16,7 @@ namespace gl {
 // ---- driver entry points (resolved through cudart; no link-time libcuda) ----
 struct Driver {
   decltype(&::cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
+  decltype(&::cuTensorMapEncodeIm2col) tensorMapEncodeIm2col = nullptr;
   decltype(&::cuDeviceGetDevResource) deviceGetDevResource = nullptr;
   decltype(&::cuDevSmResourceSplitByCount) devSmResourceSplitByCount = nullptr;
   decltype(&::cuDevResourceGenerateDesc) devResourceGenerateDesc = nullptr;
@@ -56,6 +57,7 @@ struct DevWeights {
 // ---- programs -------------------------------------------------------------------
 struct Program {
   std::vector<OpDesc> ops;
+  size_t in_copy_bytes = 0; // tests: bytes of the input copied to workspace offset 0 before launch
   OpDesc* dev = nullptr;   // device copy
   size_t ws_bytes = 0;     // activation workspace needed
   double flops = 0;        // algorithmic FLOPs of one batch (2 * MACs)
@@ -76,10 +78,15 @@ bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, in
                    size_t& in_bytes, size_t& out_bytes, std::string& err);
 
 // Single-op programs for kernel unit tests (models.cpp).
+// in_ws: the input is first copied into the workspace so the TMA operand paths run.
 bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int out_fp32, const uint16_t* w_host,
-                     const uint16_t* b_host, int has_res, DevWeights& dw, Program& out, std::string& err);
+                     const uint16_t* b_host, int in_ws, DevWeights& dw, Program& out, std::string& err);
 bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, int pad, int act,
-                     const uint16_t* w_host, const uint16_t* b_host, DevWeights& dw, Program& out, std::string& err);
+                     const uint16_t* w_host, const uint16_t* b_host, int in_ws, DevWeights& dw, Program& out,
+                     std::string& err);
+// Bind a program to a workspace: encode the tensor maps of workspace-resident
+// activation operands (their addresses are only known per workspace).
+bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::string& err);
 bool build_test_misc(int type, const int* iargs, int n_iargs, const uint16_t* w_host, size_t w_len, DevWeights& dw,
                      Program& out, std::string& err);
 

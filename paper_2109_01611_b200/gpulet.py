@@ -83,8 +83,8 @@ def lib():
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
-            "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, P, I32, I32, I32, I32, I32, I32, I32],
-            "gl_test_conv": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32],
+            "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32],
+            "gl_test_conv": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32],
             "gl_test_misc": [P, ctypes.c_int, I32, ctypes.POINTER(I32), I32, P, I64, P, P],
         }
         for name, args in sig.items():
@@ -193,9 +193,11 @@ class Context:
         _check(lib().gl_profile(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d)))
         return d.value
 
-    def run_once(self, mid, batch, x, y, n_sm=0, trace=True):
-        """One-shot executor launch; returns per-step durations (ns) when trace."""
-        cap = 1024
+    def run_once(self, mid, batch, x, y, n_sm=0, trace=True, roles=False):
+        """One-shot executor launch; returns per-step durations (ns) when trace
+        (and, with roles, CTA 0's per-step role stamps relative to step start:
+        producer start/end, MMA first/last, epilogue first/end, barrier in/out)."""
+        cap = 1024 + 8 * 1000 if roles else 1024
         tr = (ctypes.c_uint64 * cap)()
         n = ctypes.c_int32()
         _check(lib().gl_run_once(self.h, mid, batch, _ptr(x), _ptr(y), n_sm, tr if trace else None, cap,
@@ -203,7 +205,14 @@ class Context:
         if not trace:
             return None
         ts = list(tr[: n.value + 1])
-        return [ts[i + 1] - ts[i] for i in range(n.value)]
+        durs = [ts[i + 1] - ts[i] for i in range(n.value)]
+        if not roles:
+            return durs
+        rl = []
+        for s in range(n.value):
+            st = list(tr[1024 + 8 * s: 1024 + 8 * s + 8])
+            rl.append([(v - ts[s]) if v else None for v in st])
+        return durs, rl
 
     def serve(self, lanes, n_models, arr_us, arr_model, slo_us):
         """gl_serve: lanes = list of dicts (gpulet, model_id, model_slot, batch, duty_us,
@@ -234,13 +243,13 @@ class Context:
         return [(t[i], o[i], f[i], b[i]) for i in range(n.value)]
 
     # ---- kernel unit entry points -------------------------------------------
-    def test_gemm(self, gpu, A, W_bits, b_bits, out, M, N, K, act=0, swap_ab=0, splitk=1, out_fp32=0):
-        _check(lib().gl_test_gemm(self.h, gpu, _ptr(A), _ptr(W_bits), _ptr(b_bits), None, _ptr(out), M, N, K, act,
-                                  swap_ab, splitk, out_fp32))
+    def test_gemm(self, gpu, A, W_bits, b_bits, out, M, N, K, act=0, swap_ab=0, splitk=1, out_fp32=0, in_ws=0):
+        _check(lib().gl_test_gemm(self.h, gpu, _ptr(A), _ptr(W_bits), _ptr(b_bits), _ptr(out), M, N, K, act,
+                                  swap_ab, splitk, out_fp32, in_ws))
 
-    def test_conv(self, gpu, x, W_bits, b_bits, y, N, H, W, C, Cout, KH, stride, pad, act=1):
+    def test_conv(self, gpu, x, W_bits, b_bits, y, N, H, W, C, Cout, KH, stride, pad, act=1, in_ws=0):
         _check(lib().gl_test_conv(self.h, gpu, _ptr(x), _ptr(W_bits), _ptr(b_bits), _ptr(y), N, H, W, C, Cout, KH,
-                                  stride, pad, act))
+                                  stride, pad, act, in_ws))
 
     def test_misc(self, gpu, op, iargs, params, x, y):
         ia = (ctypes.c_int32 * len(iargs))(*iargs)

@@ -28,15 +28,17 @@ GEMM_CASES = [(128, 64, 64, 1), (200, 96, 320, 1), (1000, 256, 768, 0), (77, 48,
               (300, 1000, 512, 3), (513, 2304, 768, 0)]
 
 
+@pytest.mark.parametrize("in_ws", [0, 1])
 @pytest.mark.parametrize("M,N,K,act", GEMM_CASES)
-def test_gemm_vs_oracle(ctx, M, N, K, act):
+def test_gemm_vs_oracle(ctx, M, N, K, act, in_ws):
+    """in_ws=0: activation operand gathered by cp.async; in_ws=1: 2-D TMA."""
     import torch
     r = np.random.default_rng(M + N + K)
     A = _bf16(r, (M, K))
     W = _bf16(r, (N, K), 1 / np.sqrt(K))
     b = _bf16(r, (N,), 0.1)
     out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
-    ctx.test_gemm(0, to_dev_bf16(A), W, b, out, M, N, K, act=act)
+    ctx.test_gemm(0, to_dev_bf16(A), W, b, out, M, N, K, act=act, in_ws=in_ws)
     torch.cuda.synchronize()
     y = nn.linear(bits_to_f64(A), bits_to_f64(W), bits_to_f64(b))
     y = {0: y, 1: nn.relu(y), 2: nn.gelu(y), 3: np.tanh(y)}[act]
@@ -47,15 +49,16 @@ def test_gemm_vs_oracle(ctx, M, N, K, act):
     assert np.mean(got == ref) > 0.9
 
 
+@pytest.mark.parametrize("in_ws", [0, 1])
 @pytest.mark.parametrize("M,N,K", [(1, 1000, 2048), (7, 4096, 25088), (32, 1000, 4096), (16, 2, 768), (3, 768, 768)])
-def test_gemm_swap_ab_splitk_vs_oracle(ctx, M, N, K):
+def test_gemm_swap_ab_splitk_vs_oracle(ctx, M, N, K, in_ws):
     import torch
     r = np.random.default_rng(M * 7 + N)
     A = _bf16(r, (M, K))
     W = _bf16(r, (N, K), 1 / np.sqrt(K))
     b = _bf16(r, (N,), 0.1)
     out = torch.empty((M, N), dtype=torch.float32, device="cuda")
-    ctx.test_gemm(0, to_dev_bf16(A), W, b, out, M, N, K, act=0, swap_ab=1, out_fp32=1)
+    ctx.test_gemm(0, to_dev_bf16(A), W, b, out, M, N, K, act=0, swap_ab=1, out_fp32=1, in_ws=in_ws)
     torch.cuda.synchronize()
     ref = nn.linear(bits_to_f64(A), bits_to_f64(W), bits_to_f64(b))
     assert rel_err(out.cpu().numpy(), ref) < 1e-4
@@ -63,11 +66,15 @@ def test_gemm_swap_ab_splitk_vs_oracle(ctx, M, N, K):
 
 CONV_CASES = [(2, 14, 14, 64, 128, 3, 1, 1), (1, 30, 30, 8, 64, 7, 2, 3), (2, 9, 9, 32, 24, 3, 2, 1),
               (3, 15, 15, 256, 512, 1, 2, 0), (1, 12, 12, 16, 48, 5, 1, 2), (2, 19, 19, 512, 126, 3, 1, 1),
-              (1, 56, 56, 64, 64, 3, 1, 1)]
+              (1, 56, 56, 64, 64, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1), (2, 10, 10, 256, 512, 3, 2, 1),
+              (3, 7, 7, 512, 256, 1, 1, 0), (2, 5, 5, 128, 64, 5, 1, 2)]
 
 
+@pytest.mark.parametrize("in_ws", [0, 1])
 @pytest.mark.parametrize("N,H,W,C,Co,k,s,p", CONV_CASES)
-def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p):
+def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p, in_ws):
+    """in_ws=0: cp.async implicit-im2col gather; in_ws=1: TMA (2-D for 1x1/s1,
+    im2col mode for KxK / strided convs with C % 64 == 0, gather otherwise)."""
     import torch
     r = np.random.default_rng(H * C + Co)
     x = _bf16(r, (N, H, W, C))
@@ -75,7 +82,7 @@ def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p):
     b = _bf16(r, (Co,), 0.05)
     Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
     y = torch.empty((N, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
-    ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1)
+    ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1, in_ws=in_ws)
     torch.cuda.synchronize()
     ref = nn.rbf16(nn.relu(nn.conv2d(bits_to_f64(x), bits_to_f64(w), bits_to_f64(b), s, p)))
     got = bits_to_f64(from_dev_bf16(y))
@@ -136,13 +143,14 @@ def test_layernorm(ctx):
     assert rel_err(bits_to_f64(from_dev_bf16(y)), ref) < 1e-2
 
 
-def test_attention(ctx):
+@pytest.mark.parametrize("tensor_core", [1, 0])
+def test_attention(ctx, tensor_core):
     import torch
     r = np.random.default_rng(11)
     nseq = 3
     qkv = _bf16(r, (nseq * 128, 3 * 768))
     y = torch.empty((nseq * 128, 768), dtype=torch.bfloat16, device="cuda")
-    ctx.test_misc(0, 8, [nseq], None, to_dev_bf16(qkv), y)
+    ctx.test_misc(0, 8, [nseq, tensor_core], None, to_dev_bf16(qkv), y)
     torch.cuda.synchronize()
     q = bits_to_f64(qkv).reshape(nseq, 128, 3, 12, 64)
     s = np.einsum("bqhd,bkhd->bhqk", q[:, :, 0], q[:, :, 1]) * 0.125

@@ -29,7 +29,9 @@ def main():
     mid = ctx.load_model(0, a.model, synthgen.weight_file(a.model))
     x = common.device_input(a.model, a.batch)
     y = torch.empty(ctx.model_io(mid, a.batch)[1] // 4, device="cuda")
-    runs = [ctx.run_once(mid, a.batch, x, y, a.n_sm, True) for _ in range(a.reps)]
+    runs = [ctx.run_once(mid, a.batch, x, y, a.n_sm, True, roles=True) for _ in range(a.reps)]
+    roles = runs[-1][1]
+    runs = [r[0] for r in runs]
     info = ctx.program_info(mid, a.batch)
     best = [min(r[i] for r in runs) for i in range(len(info))]
     tot = sum(best)
@@ -37,7 +39,9 @@ def main():
     for i, (t, n, f, b) in enumerate(info):
         rows.append({"step": i, "op": OPS.get(t, t), "ops": n, "us": round(best[i] / 1e3, 2), "gflop": round(f / 1e9, 3),
                      "mb": round(b / 1e6, 2), "tflops": round(f / max(best[i], 1) / 1e3, 1),
-                     "gbs": round(b / max(best[i], 1), 1)})
+                     "gbs": round(b / max(best[i], 1), 1),
+                     # CTA 0 role stamps (us from step start): prod start/end, mma first/last, epi first/end, bar in/out
+                     "roles_us": [None if v is None else round(v / 1e3, 2) for v in roles[i]]})
     fl = sum(r[2] for r in info)
     summary = {"model": a.model, "batch": a.batch, "steps": len(info), "total_us": round(tot / 1e3, 1),
                "tflops": round(fl / tot / 1e3, 1), "rows": rows}

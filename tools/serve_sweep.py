@@ -44,7 +44,11 @@ def poisson_trace(rates, secs, seed):
 class Server:
     def __init__(self, ctx, mids, lat_env, l2, mem, slo, coeffs):
         self.ctx, self.mids, self.lat, self.l2, self.mem, self.slo, self.c = ctx, mids, lat_env, l2, mem, slo, coeffs
+        import torch
+        # device buffers exist before any executor starts (allocations can synchronise the device)
         self.inputs = {m: common.device_input(m, 32) for m in common.MODELS}
+        self.outputs = {m: torch.empty(ctx.model_io(mids[m], 32)[1] // 4, device="cuda") for m in common.MODELS}
+        torch.cuda.current_stream().synchronize()
 
     def run(self, rates, mode, secs, seed):
         import torch
@@ -63,7 +67,7 @@ class Server:
                 for ln in g["lanes"]:
                     m = ln["model"]
                     mi = common.MODELS.index(m)
-                    y = torch.empty(self.ctx.model_io(self.mids[m], 32)[1] // 4, device="cuda")
+                    y = self.outputs[m]
                     drop = (self.lat[mi][0][common.GRID.index(g["size"])] * ln["F"] + 999) // 1000
                     lanes.append(dict(gpulet=gid, model_id=self.mids[m], model_slot=mi, batch=ln["batch"],
                                       duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.inputs[m], y=y))
