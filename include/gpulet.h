@@ -88,6 +88,12 @@ gl_status gl_model_cost(gl_ctx* ctx, int32_t model_id, int32_t batch, double* fl
  * Out: *gpulet_id, *sm_count (actual SMs).  Errors: GL_E_GRID, GL_E_PARTITION,
  * GL_E_NOT_CONCURRENT, GL_E_CUDA. */
 gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int sm_pct, int32_t* gpulet_id, int32_t* sm_count);
+/* Create a whole GPU partition of n (1 or 2) gpu-lets, sizes pcts[] summing to <= 100,
+ * in slot order.  All green contexts are created before the first executor starts
+ * (green-context creation can block behind a running persistent kernel, so this is
+ * the way to (re)partition a GPU).  The GPU must have no live gpu-let (GL_E_STATE).
+ * Out: ids[n], sm_counts[n] (optional). */
+gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids, int32_t* sm_counts);
 /* Drain and stop a gpu-let's executor; its slot becomes free. */
 gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t gpulet_id);
 /* %smid of every executor CTA (confinement audit); *n = number written. */

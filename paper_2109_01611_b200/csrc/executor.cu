@@ -51,6 +51,7 @@ struct Smem {
   uint8_t* scratch;  // non-GEMM ops reuse the stage area
   uint64_t* att;     // attention barriers: [0] Q/K/V landed, [1] S = QK^T done, [2] O = PV done
   int* epi_flag;     // epilogue broadcast word (split-K last arriver)
+  uint8_t* estage;   // epilogue staging: 4 warps x 32 rows x kEpiRowBytes (coalesced stores)
   uint64_t* dbg;     // optional per-step role stamps of CTA 0 (one-shot trace mode)
   int step;          // current step index (for dbg)
 };
@@ -113,7 +114,7 @@ __device__ __forceinline__ int64_t out_index(const Epilogue& e, int r, int c) {
 
 // Apply bias / residual / activation to an fp32 value of output element (m, n)
 // of D[M,N] and store it.  (r, c) = (m, n), or (n, m) for swap-AB.
-__device__ __forceinline__ void store_one(const Epilogue& e, const Ctx& X, int m, int n, float v) {
+__device__ __noinline__ void store_one(const Epilogue& e, const Ctx& X, int m, int n, float v) {
   const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
   if (bias) v += __bfloat162float(bias[e.bias_on_m ? m : n]);
   const int r = e.transpose ? n : m, c = e.transpose ? m : n;
@@ -125,6 +126,92 @@ __device__ __forceinline__ void store_one(const Epilogue& e, const Ctx& X, int m
     ((float*)res(e.out, X))[idx] = v;
   else
     ((__nv_bfloat16*)res(e.out, X))[idx] = __float2bfloat16_rn(v);
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_t(float v) {
+  if (ACT == ACT_RELU) return fmaxf(v, 0.f);
+  if (ACT == ACT_GELU) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));
+  if (ACT == ACT_TANH) return tanhf(v);
+  return v;
+}
+
+__device__ __forceinline__ void add_bf16x8(float* v, const uint4& u) {
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] += f.x;
+    v[2 * i + 1] += f.y;
+  }
+}
+
+// Warp-collective epilogue of the 32 rows [row0, row0 + 32) of one tile, for
+// its first `nfull` full 32-column chunks (bf16 row-major output): TMEM ->
+// registers, + bias (+ residual) -> ACT -> bf16.  Rows are staged in shared
+// memory so that residual loads and output stores move 16 B per lane with four
+// lanes per 64-B row segment; the residual of chunk j + 1 is prefetched by
+// cp.async while chunk j is computed (two staging buffers per warp).
+template <int ACT, bool RES>
+__device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, const Ctx& X, uint32_t taddr,
+                                         int row0, int n00, int nfull, uint8_t* stg, int lane) {
+  const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+  const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
+  __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
+  const int sr = lane >> 2, seg = lane & 3;
+  const int64_t ldc = e.ldc;
+  const int64_t coff = e.col_off;
+  auto prefetch = [&](int j) {
+    uint8_t* b = stg + (j & 1) * 32 * kEpiRowBytes;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int r = it * 8 + sr;
+      const bool ok = row0 + r < g.M;
+      const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n00 + j * 32 + seg * 8 : rsd;
+      cp_async16(smem_u32(b + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
+    }
+    cp_async_commit();
+  };
+  if (RES && nfull > 0) prefetch(0);
+  for (int j = 0; j < nfull; ++j) {
+    uint8_t* b = stg + (j & 1) * 32 * kEpiRowBytes;
+    if (RES) {
+      if (j + 1 < nfull) {
+        prefetch(j + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+    }
+    float v[32];
+    tmem_ld32(taddr + j * 32, v);
+    const int n0 = n00 + j * 32;
+    if (bias) {
+      const uint4* bp = (const uint4*)(bias + n0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, __ldg(bp + k));
+    }
+    if (RES) {
+      const uint4* rp = (const uint4*)(b + lane * kEpiRowBytes);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, rp[k]);
+    }
+    __align__(16) __nv_bfloat16 o[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) o[c] = __float2bfloat16_rn(act_t<ACT>(v[c]));
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ((uint4*)(b + lane * kEpiRowBytes))[k] = ((const uint4*)o)[k];
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int r = it * 8 + sr;
+      if (row0 + r < g.M)
+        *(uint4*)(outp + (row0 + r) * ldc + coff + n0 + seg * 8) = *(const uint4*)(b + r * kEpiRowBytes + seg * 16);
+    }
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------------ operand gather
@@ -322,95 +409,66 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       if (tile == (int)blockIdx.x && q == 0 && lane == 0) dbg_mark(S, 4);
       const int m = mb * 128 + q * 32 + lane;
       const int nend = min(g.N, (nb + 1) * g.BN);
-      float* ws = (float*)res(e.ws, X);
-      const bool vec = !e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 &&
-                       (e.col_off % 8) == 0;
-      const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
-      const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
-      __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
-      // bias / residual / activation / store of 32 consecutive output columns
-      auto finish_chunk = [&](int n0, const float* v) {
-        if (vec && n0 + 32 <= nend) {
-          const int64_t o0 = (int64_t)m * e.ldc + e.col_off + n0;
-          __align__(16) __nv_bfloat16 r[32];
-          if (rsd) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) ((uint4*)r)[c] = ((const uint4*)(rsd + o0))[c];
-          }
-          __align__(16) __nv_bfloat16 o[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            float x = v[c] + (bias ? __bfloat162float(bias[n0 + c]) : 0.f);
-            if (rsd) x += __bfloat162float(r[c]);
-            o[c] = __float2bfloat16_rn(act_f(x, e.act));
-          }
-          uint4* dst = (uint4*)(outp + o0);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) dst[c] = ((const uint4*)o)[c];
-        } else {
-          for (int c = 0; c < 32 && n0 + c < nend; ++c) store_one(e, X, m, n0 + c, v[c]);
-        }
-      };
-      if (e.splitk <= 1) {
+      const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * 256;
+      int j0 = 0;   // first column (within the tile) not yet stored
+      if (e.splitk > 1) {
+        // split-K: this split's fp32 partial tile -> ws[split][M][N] (L2-only
+        // stores); an OP_SPLITK_FINAL step reduces the splits in order.
+        float* wp = (float*)res(e.ws, X) + ((int64_t)(kb0 / g.kb_per_split) * g.M + m) * g.N;
         for (int j = 0; j < g.BN; j += 32) {
           float v[32];
-          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
+          tmem_ld32(taddr + j, v);
           const int n0 = nb * g.BN + j;
-          if (m < g.M && n0 < nend) finish_chunk(n0, v);
-        }
-        tc_fence_before();
-        mbar_arrive(&S.tempty[acc]);
-        ++P.acc;
-      } else {
-        // split-K: store this split's fp32 partial tile; the last split of the
-        // tile to arrive sums all partials in split order and runs the epilogue
-        // (no separate reduction step).
-        const int split = kb0 / g.kb_per_split;
-        float* wp = ws + ((int64_t)split * g.M + m) * g.N;
-        for (int j = 0; j < g.BN; j += 32) {
-          float v[32];
-          tmem_ld32(tbase + ((uint32_t)(q * 32) << 16) + acc * 256 + j, v);
-          const int n0 = nb * g.BN + j;
-          if (m < g.M && n0 < nend)
-            for (int c = 0; c < 32 && n0 + c < nend; ++c) wp[n0 + c] = v[c];
-        }
-        tc_fence_before();
-        mbar_arrive(&S.tempty[acc]);
-        ++P.acc;
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) {
-          int* cnt = (int*)res(e.cnt, X) + mb + nb * g.n_mblk;
-          const int old = atomicAdd(cnt, 1);
-          const bool last = old == g.splits - 1;
-          if (last) *cnt = 0;   // self-reset for the next run of the program
-          *S.epi_flag = last ? 1 : 0;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (*(volatile int*)S.epi_flag) {
-          __threadfence();
-          for (int j = 0; j < g.BN; j += 32) {
-            const int n0 = nb * g.BN + j;
-            if (m >= g.M || n0 >= nend) continue;
-            float v[32];
+          if (m < g.M && n0 < nend) {
+            if (n0 + 32 <= nend && (g.N & 3) == 0) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = 0.f;
-            for (int s = 0; s < g.splits; ++s) {
-              const volatile float* pp = ws + ((int64_t)s * g.M + m) * g.N + n0;
-              for (int c = 0; c < 32 && n0 + c < nend; ++c) v[c] += pp[c];
+              for (int c = 0; c < 8; ++c)
+                __stcg((float4*)(wp + n0) + c, make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+            } else {
+              for (int c = 0; c < 32 && n0 + c < nend; ++c) __stcg(wp + n0 + c, v[c]);
             }
-            finish_chunk(n0, v);
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        j0 = g.BN;
+      } else if (!e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 &&
+                 (e.col_off % 8) == 0) {
+        // bf16 row-major output: warp-collective staged epilogue on the full
+        // 32-column chunks (residual prefetched by cp.async one chunk ahead)
+        const int nfull = (nend - nb * g.BN) / 32;
+        const bool rs = e.res.kind != BUF_NONE;
+        uint8_t* stg = S.estage + q * 2 * 32 * kEpiRowBytes;
+        const int row0 = mb * 128 + q * 32, n00 = nb * g.BN;
+        switch (e.act * 2 + (rs ? 1 : 0)) {
+          case 0: epi_rows<ACT_NONE, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 1: epi_rows<ACT_NONE, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 2: epi_rows<ACT_RELU, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 3: epi_rows<ACT_RELU, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 4: epi_rows<ACT_GELU, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 5: epi_rows<ACT_GELU, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          case 6: epi_rows<ACT_TANH, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+          default: epi_rows<ACT_TANH, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
+        }
+        j0 = nfull * 32;
       }
+      // remaining (partial / fp32 / transposed / strided) columns, element-wise
+      for (int j = j0; j < g.BN; j += 32) {
+        const int n0 = nb * g.BN + j;
+        if (n0 >= nend) break;
+        float v[32];
+        tmem_ld32(taddr + j, v);
+        if (m < g.M)
+          for (int c = 0; c < 32 && n0 + c < nend; ++c) store_one(e, X, m, n0 + c, v[c]);
+      }
+      tc_fence_before();
+      mbar_arrive(&S.tempty[acc]);
+      ++P.acc;
     }
     if (q == 0 && lane == 0) dbg_mark(S, 5);
   }
 }
 
 // ------------------------------------------------------------------ split-K final
-__device__ void splitk_final(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void splitk_final(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const Epilogue& e = a.ep;
   const float* ws = (const float*)res(e.ws, X);
@@ -418,13 +476,13 @@ __device__ void splitk_final(const OpDesc* op, const Ctx& X) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / a.cols), n = (int)(i - (int64_t)m * a.cols);
     float v = 0.f;
-    for (int s = 0; s < e.splitk; ++s) v += ws[(int64_t)s * total + i];
+    for (int s = 0; s < e.splitk; ++s) v += __ldcg(ws + (int64_t)s * total + i);
     store_one(e, X, m, n, v);
   }
 }
 
 // ------------------------------------------------------------------ depthwise 3x3 (K5)
-__device__ void dwconv(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void dwconv(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   const __nv_bfloat16* w = (const __nv_bfloat16*)res(a.w, X);   // [9][C] tap-major
@@ -468,7 +526,7 @@ __device__ void dwconv(const OpDesc* op, const Ctx& X) {
 }
 
 // ------------------------------------------------------------------ max pool (K6)
-__device__ void maxpool(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void maxpool(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
@@ -504,7 +562,7 @@ __device__ void maxpool(const OpDesc* op, const Ctx& X) {
 }
 
 // ------------------------------------------------------------------ global avg pool (K6)
-__device__ void avgpool(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void avgpool(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
@@ -529,7 +587,7 @@ __device__ void avgpool(const OpDesc* op, const Ctx& X) {
 // ------------------------------------------------------------------ LeNet-5 fused (K7)
 __device__ __forceinline__ float bfr(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
-__device__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+__device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   const __nv_bfloat16* W = (const __nv_bfloat16*)res(a.w, X);  // packed params in manifest order
@@ -646,7 +704,7 @@ __device__ __forceinline__ void ln_row_store(float* v, const __nv_bfloat16* g, c
   }
 }
 
-__device__ void layernorm(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void layernorm(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
@@ -666,7 +724,7 @@ __device__ void layernorm(const OpDesc* op, const Ctx& X) {
   }
 }
 
-__device__ void embed_ln(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void embed_ln(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const int32_t* ids = (const int32_t*)res(a.x, X);
   const __nv_bfloat16* word = (const __nv_bfloat16*)res(a.w, X);   // [vocab, 768]
@@ -698,7 +756,7 @@ __device__ void embed_ln(const OpDesc* op, const Ctx& X) {
 // ------------------------------------------------------------------ attention (K9)
 // Unit = (sequence, head): S = Q K^T / 8 (fp32), softmax fp32, P -> bf16,
 // O = P V (fp32) -> bf16.  qkv [b*seq, 3*768]; ctx [b*seq, 768].
-__device__ void attention(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+__device__ __noinline__ void attention(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* qkv = (const __nv_bfloat16*)res(a.x, X);
   __nv_bfloat16* ctx = (__nv_bfloat16*)res(a.y, X);
@@ -787,7 +845,7 @@ __device__ void attention(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
 // P = softmax(S/8) as bf16 into smem in the UMMA K-major layout; O = P V is a
 // 128x64x128 UMMA with V as an MN-major B operand into TMEM columns [128,192);
 // O is rounded to bf16 and stored.  Rounding points match the oracle (C1.4).
-__device__ void attention_tc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P) {
+__device__ __noinline__ void attention_tc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P) {
   const MiscArgs& a = op->m;
   __nv_bfloat16* ctx = (__nv_bfloat16*)res(a.y, X);
   const int H = a.heads, units = a.N * H, HD = H * 64;
@@ -877,7 +935,7 @@ __device__ void attention_tc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe
 }
 
 // ------------------------------------------------------------------ row softmax (K11)
-__device__ void softmax_rows(const OpDesc* op, const Ctx& X) {
+__device__ __noinline__ void softmax_rows(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   float* x = (float*)res(a.x, X);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.rows; r += gridDim.x * blockDim.x) {
@@ -953,6 +1011,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.att = bars + 2 * kStages + 4;
   S.tmem_base = (uint32_t*)(bars + 2 * kStages + 7);
   S.epi_flag = (int*)(bars + 2 * kStages + 8);
+  S.estage = base + kStages * (kStageBytesA + kStageBytesB) + 1024;
   S.scratch = base;
   S.dbg = nullptr;
   S.step = 0;

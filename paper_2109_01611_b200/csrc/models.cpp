@@ -341,18 +341,30 @@ class Builder {
       PendingFinal f{g.ep, g.M, g.N, g.splits, ws};
       g.ep.splitk = g.splits;
       g.ep.ws = ws_ref(ws);
-      // per-tile arrival counters in the reserved zero region (tiles < 256 by choose_split)
-      g.ep.cnt = ws_ref((uint64_t)((n_split_ops++) % 64) * 256 * 4);
+      // In-kernel last-arriver reduction (e.cnt = per-tile counters in the
+      // reserved zero region) leaves one CTA reducing a whole tile and was
+      // measured slower than a separate all-CTA reduction step for the deep
+      // splits used at small batch; the finalize op is used instead.
+      g.ep.cnt = BufRef{0, BUF_NONE, 0};
       finals.push_back(f);
     }
   }
-  int n_split_ops = 0;
 
-  // Split-K partial buffers die with their step: the last-arriving split of
-  // each tile reduces in-kernel (no finalize step).  Call after step().
+  // Emit the split-K reduction ops of the previous step (call after step()).
   void flush_finals() {
-    for (auto& f : finals) release_off(f.ws);
+    if (finals.empty()) return;
+    for (auto& f : finals) {
+      OpDesc& op = add(OP_SPLITK_FINAL);
+      op.m.rows = f.M;
+      op.m.cols = f.N;
+      op.m.ep = f.ep;
+      op.m.ep.splitk = f.splits;
+      op.m.ep.ws = ws_ref(f.ws);
+      op.n_units = 1;
+      release_off(f.ws);
+    }
     finals.clear();
+    step();
   }
 
   static Gather conv_gather(const Act& x, int KH, int stride, int pad, int Ho, int Wo) {
@@ -882,6 +894,7 @@ bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int 
   if (in_ws) {
     x = ws_ref(B.alloc((uint64_t)M * K * 2));
     out.in_copy_bytes = (size_t)M * K * 2;
+    out.in_copy_off = x.off;
   }
   Epilogue ep = Builder::plain_ep(out_ref(0), N, 0);
   ep.act = act;
@@ -917,6 +930,7 @@ bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, i
   if (in_ws) {
     out.in_copy_bytes = (size_t)N * H * W * C * 2;
     x.ref = ws_ref(B.alloc(out.in_copy_bytes));
+    out.in_copy_off = x.ref.off;
   }
   const int Ho = (H + 2 * pad - KH) / stride + 1, Wo = (W + 2 * pad - KH) / stride + 1;
   Act y;
@@ -993,6 +1007,7 @@ bool build_test_misc(int type, const int* ia, int n, const uint16_t* w_host, siz
     if (tc) {
       op.m.x = ws_ref(B.alloc(qkv_bytes));
       out.in_copy_bytes = qkv_bytes;
+      out.in_copy_off = op.m.x.off;
       op.g.act_tmap = 1;
     }
     op.m.y = out_ref(0);

@@ -162,6 +162,8 @@ constexpr int kThreads = 288;   // 4 producer warps, 4 epilogue warps, 1 MMA war
 constexpr int kStages = 4;
 constexpr int kStageBytesA = 128 * 128;       // 128 rows x 64 bf16
 constexpr int kStageBytesB = 256 * 128;       // up to 256 rows x 64 bf16
-constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 2048;  // + barriers, alignment
+constexpr int kEpiRowBytes = 80;                   // 32 bf16 + 16 B pad per staged row
+constexpr int kEpiStageBytes = 4 * 2 * 32 * kEpiRowBytes;  // per epilogue warp: 2 x (32 rows x 32 columns)
+constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 + kEpiStageBytes;  // + barriers
 
 }  // namespace gl

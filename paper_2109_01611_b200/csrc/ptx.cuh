@@ -55,9 +55,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 // Wait until the phase with the given parity has completed; trap on a hang so a
 // bad descriptor fails loudly instead of wedging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint64_t n = 0;
+  if (mbar_try_wait(bar, parity)) return;
+  uint64_t t0 = 0;
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++n > (GL_SPIN_LIMIT >> 6)) __trap();
+    if ((++n & 1023) == 0) {   // a pipeline stage never lands: fail loudly after ~4 s
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
   }
 }
 

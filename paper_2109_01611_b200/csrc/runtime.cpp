@@ -98,6 +98,15 @@ static void flush_deferred() {
   g_deferred.clear();
 }
 
+// GL_DEBUG=1: progress messages on stderr (host-side hang diagnosis).
+static void dbg_log(const char* what) {
+  static const bool on = getenv("GL_DEBUG") != nullptr;
+  if (on) {
+    fprintf(stderr, "[libgpulet] %s\n", what);
+    fflush(stderr);
+  }
+}
+
 static uint64_t now_ns() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -214,6 +223,11 @@ struct SlotRes {
 
 struct GpuState {
   SlotRes slot_res[2];
+  bool green_ready = false;
+  CUgreenCtx gctx[2][5] = {};      // [slot][size index of 20,40,50,60,80]
+  CUstream gstream[2][5] = {};
+  int gnsm[2][5] = {};
+  CUstream full_stream = nullptr;  // 100 %: a non-blocking stream of the primary context
   int dev = 0;
   int nsm = 0;
   bool split = false;
@@ -266,6 +280,92 @@ static int sm_for_pct(int pct) {
 
 static size_t exec_smem_bytes() { return (size_t)kSmemBytes + 1024; }
 
+static int grid_index(int pct) {
+  switch (pct) {
+    case 20: return 0;
+    case 40: return 1;
+    case 50: return 2;
+    case 60: return 3;
+    case 80: return 4;
+    default: return -1;
+  }
+}
+
+// One SM split per GPU (8-SM groups + remainder), then one green context and
+// stream per (slot, size): slot 0 uses groups from the front, slot 1 from the back.
+static gl_status prepare_green(gl_ctx* ctx, GpuState& G) {
+  Driver& D = driver();
+  CUdevice cud;
+  gl_status rc = cu_check(ctx, D.deviceGet(&cud, G.dev), "cuDeviceGet");
+  if (rc) return rc;
+  CUdevResource all;
+  rc = cu_check(ctx, D.deviceGetDevResource(cud, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+  if (rc) return rc;
+  G.ngroups = 32;
+  rc = cu_check(ctx, D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem, 0, 8),
+                "cuDevSmResourceSplitByCount");
+  if (rc) return rc;
+  G.split = true;
+  cudaStream_t s;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return fail(GL_E_CUDA, "stream");
+  G.full_stream = (CUstream)s;
+  G.green_ready = true;
+  return GL_OK;
+}
+
+// Green context + stream of (slot, size index), created on first use.
+static gl_status ensure_green(gl_ctx* ctx, GpuState& G, int slot, int gi) {
+  if (G.gctx[slot][gi]) return GL_OK;
+  static const int pcts[5] = {20, 40, 50, 60, 80};
+  Driver& D = driver();
+  CUdevice cud;
+  gl_status rc = cu_check(ctx, D.deviceGet(&cud, G.dev), "cuDeviceGet");
+  if (rc) return rc;
+  const int want = sm_for_pct(pcts[gi]);
+  std::vector<CUdevResource> res;
+  int have = 0;
+  // The split yields `ngroups` co-schedulable 8-SM groups plus a remainder
+  // whose size depends on the physical GPU's floorsweeping (measured: 15
+  // groups + 28 SMs on this pool's B200s, not 18 + 4).  Slot 0 takes
+  // k = floor(p * ngroups / 100) groups from the front; slot 1 takes the
+  // remainder + floor(q * ngroups / 100) groups from the back, so any pair with
+  // p + q <= 100 is disjoint (scripts/diag_pairs.py audits the SM ids).
+  (void)want;
+  const int k_groups = pcts[gi] * (int)G.ngroups / 100;
+  if (slot == 1 && G.rem.sm.smCount > 0) {
+    res.push_back(G.rem);
+    have += (int)G.rem.sm.smCount;
+  }
+  for (int k = 0; k < k_groups && k < (int)G.ngroups; ++k) {
+    const unsigned i = slot == 0 ? (unsigned)k : G.ngroups - 1 - (unsigned)k;
+    res.push_back(G.groups[i]);
+    have += (int)G.groups[i].sm.smCount;
+  }
+  if (have < 8 * k_groups) return fail(GL_E_PARTITION, "ensure_green: not enough SM groups");
+  CUdevResourceDesc desc;
+  rc = cu_check(ctx, D.devResourceGenerateDesc(&desc, res.data(), (unsigned)res.size()), "cuDevResourceGenerateDesc");
+  if (rc) return rc;
+  dbg_log("ensure_green: cuGreenCtxCreate");
+  rc = cu_check(ctx, D.greenCtxCreate(&G.gctx[slot][gi], desc, cud, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+  if (rc) return rc;
+  rc = cu_check(ctx, D.greenCtxStreamCreate(&G.gstream[slot][gi], G.gctx[slot][gi], CU_STREAM_NON_BLOCKING, 0),
+                "cuGreenCtxStreamCreate");
+  if (rc) return rc;
+  G.gnsm[slot][gi] = have;
+  return GL_OK;
+}
+
+// Drop every cached green context of a GPU (only while none of its executors run).
+static void drop_green(GpuState& G) {
+  for (int s = 0; s < 2; ++s)
+    for (int gi = 0; gi < 5; ++gi) {
+      if (G.gstream[s][gi]) driver().streamDestroy(G.gstream[s][gi]);
+      if (G.gctx[s][gi]) driver().greenCtxDestroy(G.gctx[s][gi]);
+      G.gstream[s][gi] = nullptr;
+      G.gctx[s][gi] = nullptr;
+    }
+}
+
 static gl_status launch_executor(gl_ctx* ctx, int dev, CUstream stream, int grid, const ExecParams& p) {
   Driver& D = driver();
   if (!D.ok) return fail(GL_E_CUDA, "CUDA driver entry points unavailable");
@@ -296,7 +396,8 @@ static gl_status run_oneshot(gl_ctx* ctx, int gpu, Program& prog, const void* in
   char* ws = nullptr;
   CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
   CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
-  if (prog.in_copy_bytes) CK(cudaMemcpy(ws, in, prog.in_copy_bytes, cudaMemcpyDeviceToDevice), "copy input to ws");
+  if (prog.in_copy_bytes)
+    CK(cudaMemcpy(ws + prog.in_copy_off, in, prog.in_copy_bytes, cudaMemcpyDeviceToDevice), "copy input to ws");
   std::string berr;
   OpDesc* dprog = upload_bound(prog, ws, berr);
   if (!dprog) return fail(GL_E_CUDA, berr);
@@ -378,6 +479,11 @@ gl_status gl_shutdown(gl_ctx* ctx) {
   }
   for (auto& G : ctx->gpus) {
     cudaSetDevice(G.dev);
+    if (G.green_ready) {
+      drop_green(G);
+      if (G.full_stream) cudaStreamDestroy((cudaStream_t)G.full_stream);
+      G.green_ready = false;
+    }
     for (auto& R : G.slot_res) {
       if (!R.ready) continue;
       for (auto& kv : R.progs)
@@ -451,56 +557,32 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
   const int slot = G.slots[0] < 0 ? 0 : 1;
   Driver& D = driver();
   CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  dbg_log("create_gpulet: begin");
   auto g = std::make_unique<Gpulet>();
   g->gpu = gpu;
   g->slot = slot;
   g->pct = pct;
+  // Green contexts are cached per (slot, size).  cuGreenCtxCreate can block
+  // behind a running persistent kernel, so gl_create_gpulets creates a whole
+  // GPU partition's contexts before launching any executor.  Slot 0 takes
+  // 8-SM groups from the front, slot 1 from the back; shares >= 60 % add the
+  // 4-SM remainder, so any pair with sizes summing to <= 100 is disjoint
+  // (k(20)=4, k(40)=7, k(50)=9, k(60)=11, k(80)=14 of 18 groups).
+  if (!G.green_ready) {
+    gl_status rc = prepare_green(ctx, G);
+    if (rc) return rc;
+  }
   if (pct == 100) {
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    g->stream = (CUstream)s;
+    g->stream = G.full_stream;
     g->own_primary_stream = true;
     g->nsm = G.nsm;
   } else {
-    CUdevice cud;
-    gl_status rc = cu_check(ctx, D.deviceGet(&cud, G.dev), "cuDeviceGet");
+    const int gi = grid_index(pct);
+    gl_status rc = ensure_green(ctx, G, slot, gi);
     if (rc) return rc;
-    if (!G.split) {
-      CUdevResource all;
-      rc = cu_check(ctx, D.deviceGetDevResource(cud, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
-      if (rc) return rc;
-      G.ngroups = 32;
-      rc = cu_check(ctx, D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem, 0, 8),
-                    "cuDevSmResourceSplitByCount");
-      if (rc) return rc;
-      G.split = true;
-    }
-    const int want = sm_for_pct(pct);
-    std::vector<CUdevResource> res;
-    int have = 0;
-    // larger shares also take the remainder group (148 = 18 x 8 + 4)
-    if (pct >= 60 && !G.rem_used && G.rem.sm.smCount > 0) {
-      res.push_back(G.rem);
-      have += (int)G.rem.sm.smCount;
-      g->uses_rem = true;
-    }
-    for (unsigned i = 0; i < G.ngroups && have < want; ++i) {
-      if (G.used_groups & (1u << i)) continue;
-      res.push_back(G.groups[i]);
-      have += (int)G.groups[i].sm.smCount;
-      g->groups.push_back((int)i);
-    }
-    if (have < want) return fail(GL_E_PARTITION, "gl_create_gpulet: not enough free SM groups");
-    CUdevResourceDesc desc;
-    rc = cu_check(ctx, D.devResourceGenerateDesc(&desc, res.data(), (unsigned)res.size()), "cuDevResourceGenerateDesc");
-    if (rc) return rc;
-    rc = cu_check(ctx, D.greenCtxCreate(&g->gctx, desc, cud, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
-    if (rc) return rc;
-    rc = cu_check(ctx, D.greenCtxStreamCreate(&g->stream, g->gctx, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
-    if (rc) return rc;
-    g->nsm = have;
-    for (int i : g->groups) G.used_groups |= (1u << i);
-    if (g->uses_rem) G.rem_used = true;
+    g->gctx = G.gctx[slot][gi];
+    g->stream = G.gstream[slot][gi];
+    g->nsm = G.gnsm[slot][gi];
   }
   // Per-slot resources (workspace, bound programs, rings) are allocated for
   // both slots the first time a gpu-let is created on this GPU, while no
@@ -535,6 +617,7 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     }
     CK(cudaDeviceSynchronize(), "slot resources");
   }
+  dbg_log("create_gpulet: slot resources ready");
   SlotRes& R = G.slot_res[slot];
   for (auto& old : ctx->gpulets)   // a previous gpu-let of this slot gives its ring back
     if (old && old->gpu == gpu && old->slot == slot) old->ring = nullptr;
@@ -545,8 +628,12 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
   g->st = R.st;
   g->smid = R.smid;
   std::memset((void*)g->ring, 0, sizeof(HostRing));
-  CK(cudaMemsetAsync(g->st, 0, sizeof(ExecState), (cudaStream_t)g->stream), "reset state");
-  CK(cudaMemsetAsync(g->smid, 0xff, 160 * sizeof(int), (cudaStream_t)g->stream), "reset smid");
+  // legacy-stream memsets: they do not wait for the (non-blocking) executor
+  // streams; runtime calls on a green-context stream are avoided on purpose
+  CK(cudaMemset(g->st, 0, sizeof(ExecState)), "reset state");
+  CK(cudaMemset(g->smid, 0xff, 160 * sizeof(int)), "reset smid");
+  CK(cudaStreamSynchronize(0), "reset sync");
+  dbg_log("create_gpulet: state reset");
   g->id = (int)ctx->gpulets.size();
   ExecParams p;
   std::memset(&p, 0, sizeof(p));
@@ -558,6 +645,7 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
   p.smid_log = g->smid;
   ++g_live_exec;
   gl_status rc = launch_executor(ctx, G.dev, g->stream, g->nsm, p);
+  dbg_log("create_gpulet: launched");
   if (rc) {
     --g_live_exec;
     return rc;
@@ -571,8 +659,13 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     if (n == g->nsm) break;
     if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
       g->ring->quit = 1;
+      std::vector<int> sm(160, -1);
+      cudaMemcpy(sm.data(), g->smid, 160 * sizeof(int), cudaMemcpyDeviceToHost);
+      std::string ids;
+      for (int i = 0; i < g->nsm; ++i) ids += (g->ring->resident[i] ? std::to_string(sm[i]) : std::string("-")) + " ";
       return fail(GL_E_NOT_CONCURRENT, "gl_create_gpulet: executor CTAs not co-resident (" + std::to_string(n) + "/" +
-                                            std::to_string(g->nsm) + ")");
+                                            std::to_string(g->nsm) + ") slot " + std::to_string(slot) + " pct " +
+                                            std::to_string(pct) + " smids: " + ids);
     }
     cudaError_t e = cudaStreamQuery((cudaStream_t)g->stream);
     if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_check(ctx, e, "executor launch");
@@ -603,13 +696,7 @@ gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t id) {
   g.alive = false;
   GpuState& G = ctx->gpus[g.gpu];
   G.slots[g.slot] = -1;
-  for (int i : g.groups) G.used_groups &= ~(1u << i);
-  if (g.uses_rem) G.rem_used = false;
-  if (g.own_primary_stream)
-    cudaStreamDestroy((cudaStream_t)g.stream);
-  else if (g.stream)
-    driver().streamDestroy(g.stream);
-  if (g.gctx) driver().greenCtxDestroy(g.gctx);
+  // the (slot, size) green context and its stream stay for the next gpu-let
   --g_live_exec;
   // workspace, programs and rings stay with the slot for the next gpu-let;
   // completions still in the ring can be polled until the slot is reused
@@ -931,5 +1018,40 @@ extern "C" gl_status gl_program_info(gl_ctx* ctx, int32_t mid, int32_t batch, in
     }
   }
   if (n_steps) *n_steps = s;
+  return GL_OK;
+}
+
+// Create a whole GPU partition (1 or 2 gpu-lets) at once: every green context it
+// needs is created before the first executor is launched (cuGreenCtxCreate can
+// block behind a running persistent kernel).  The GPU must have no live gpu-let.
+extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids,
+                                       int32_t* sm_counts) {
+  if (!ctx || !pcts || !ids || n < 1 || n > 2 || gpu < 0 || gpu >= (int)ctx->gpus.size())
+    return fail(GL_E_ARG, "gl_create_gpulets: bad arguments");
+  GpuState& G = ctx->gpus[gpu];
+  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_create_gpulets: GPU has live gpu-lets");
+  int sum = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sm_for_pct(pcts[i]) < 0) return fail(GL_E_GRID, "gl_create_gpulets: sm_pct not in the grid");
+    sum += pcts[i];
+  }
+  if (sum > 100) return fail(GL_E_PARTITION, "gl_create_gpulets: sizes sum to more than 100");
+  CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  if (!G.green_ready) {
+    gl_status rc = prepare_green(ctx, G);
+    if (rc) return rc;
+  }
+  drop_green(G);
+  for (int i = 0; i < n; ++i)
+    if (pcts[i] < 100) {
+      gl_status rc = ensure_green(ctx, G, i, grid_index(pcts[i]));
+      if (rc) return rc;
+    }
+  for (int i = 0; i < n; ++i) {
+    int32_t sm = 0;
+    gl_status rc = gl_create_gpulet(ctx, gpu, pcts[i], &ids[i], &sm);
+    if (rc) return rc;
+    if (sm_counts) sm_counts[i] = sm;
+  }
   return GL_OK;
 }

@@ -57,7 +57,8 @@ struct DevWeights {
 // ---- programs -------------------------------------------------------------------
 struct Program {
   std::vector<OpDesc> ops;
-  size_t in_copy_bytes = 0; // tests: bytes of the input copied to workspace offset 0 before launch
+  size_t in_copy_bytes = 0; // tests: bytes of the input copied into the workspace before launch
+  size_t in_copy_off = 0;   //   ... at this workspace offset
   OpDesc* dev = nullptr;   // device copy
   size_t ws_bytes = 0;     // activation workspace needed
   double flops = 0;        // algorithmic FLOPs of one batch (2 * MACs)

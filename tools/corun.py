@@ -1,0 +1,139 @@
+"""Co-run interference harness + model fit (PAPER.md
+§4.4).  For each gpu-let split (p, 100-p) two gpu-lets run pairs of
+(model, batch) back to back for `--ms` milliseconds each way; the factor of a
+side is its median co-run device latency over its median solo latency (sibling
+idle, same gpu-let).  Features are the solo L2/DRAM utilisations of both sides
+at their (model, batch, size) from profiles/profile_b200.csv.  The native OLS
+(gl_fit_interference, Householder QR) fits c1..c5 on a seeded 70 % split; the
+prediction error |max(1, f_hat) - f| / f is reported on the held-out 30 %
+(paper: 90 % of cases <= 10.26 %) and on the cfg3 cases (ResNet-50 +
+VGG-16 on 50:50).  Writes profiles/coeffs_b200.json and profiles/corun_b200.csv.
+
+    python tools/corun.py [--batches 2,8,32] [--splits 20,50,80] [--ms 150]
+"""
+import argparse
+import csv
+import itertools
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import synthgen  # noqa: E402
+from tools import common  # noqa: E402
+
+
+def run_loop(ctx, jobs, ms):
+    """jobs: list of (gid, mid, batch, x, y); keep each gpu-let's ring busy for
+    `ms`; return per-job device latencies (us) of batches that started inside the
+    window where all jobs were active."""
+    lat = [[] for _ in jobs]
+    starts = [[] for _ in jobs]
+    ends = [[] for _ in jobs]
+    inflight = {}
+    depth = 3
+    t_end = time.perf_counter() + ms / 1000.0
+    for j, (gid, mid, b, x, y) in enumerate(jobs):
+        for _ in range(depth):
+            inflight[ctx.submit_batch(gid, mid, x, y, b)] = j
+    while inflight:
+        for r in ctx.poll():
+            j = inflight.pop(r.ticket)
+            lat[j].append((r.t_end_ns - r.t_start_ns) / 1e3)
+            starts[j].append(r.t_start_ns)
+            ends[j].append(r.t_end_ns)
+            if time.perf_counter() < t_end:
+                gid, mid, b, x, y = jobs[j]
+                inflight[ctx.submit_batch(gid, mid, x, y, b)] = j
+    if len(jobs) > 1:   # keep batches inside the common busy window
+        lo = max(min(s) for s in starts)
+        hi = min(max(e) for e in ends)
+        out = []
+        for j in range(len(jobs)):
+            sel = [l for l, s, e in zip(lat[j], starts[j], ends[j]) if s >= lo and e <= hi]
+            out.append(sel if len(sel) >= 3 else lat[j])
+        return out
+    return lat
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batches", default="2,8,32")
+    ap.add_argument("--splits", default="20,50,80")
+    ap.add_argument("--ms", type=float, default=150)
+    ap.add_argument("--models", default=",".join(common.MODELS[1:]))
+    ap.add_argument("--seed", type=int, default=0)
+    a = ap.parse_args()
+    import torch
+    from paper_2109_01611_b200 import gpulet
+    batches = [int(b) for b in a.batches.split(",")]
+    splits = [int(s) for s in a.splits.split(",")]
+    models = a.models.split(",")
+    ctx = gpulet.Context(1)
+    mids = {m: ctx.load_model(0, m, synthgen.weight_file(m)) for m in common.MODELS}
+    xs = {m: common.device_input(m, 32) for m in models}
+    ys = {(m, s): torch.empty(ctx.model_io(mids[m], 32)[1] // 4, device="cuda") for m in models for s in (0, 1)}
+    torch.cuda.current_stream().synchronize()
+    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
+    si = {b: common.STAT_B.index(min(sb for sb in common.STAT_B if sb >= b)) for b in batches}
+    rows = []
+    t0 = time.time()
+    for p in splits:
+        q = 100 - p
+        (ga, _), (gb, _) = ctx.create_gpulets(0, [p, q])
+        solo = {}
+        for (side, gid, pp) in ((0, ga, p), (1, gb, q)):
+            for m in models:
+                for b in batches:
+                    L = run_loop(ctx, [(gid, mids[m], b, xs[m], ys[(m, side)])], a.ms / 3)[0]
+                    solo[(side, m, b)] = float(np.median(L))
+        for m1, m2 in itertools.combinations(models, 2):
+            for b1, b2 in itertools.product(batches, batches):
+                for (mA, bA, mB, bB) in ((m1, b1, m2, b2), (m2, b2, m1, b1)):
+                    LA, LB = run_loop(ctx, [(ga, mids[mA], bA, xs[mA], ys[(mA, 0)]),
+                                            (gb, mids[mB], bB, xs[mB], ys[(mB, 1)])], a.ms)
+                    fA = float(np.median(LA)) / solo[(0, mA, bA)]
+                    fB = float(np.median(LB)) / solo[(1, mB, bB)]
+                    iA, iB = common.MODELS.index(mA), common.MODELS.index(mB)
+                    gA, gB = common.GRID.index(p), common.GRID.index(q)
+                    fa = [l2[iA][si[bA]][gA], l2[iB][si[bB]][gB], mem[iA][si[bA]][gA], mem[iB][si[bB]][gB]]
+                    fb = [l2[iB][si[bB]][gB], l2[iA][si[bA]][gA], mem[iB][si[bB]][gB], mem[iA][si[bA]][gA]]
+                    rows.append(dict(victim=mA, vb=bA, vp=p, partner=mB, pb=bB, pp=q, factor=fA,
+                                     l2_v=fa[0], l2_u=fa[1], mem_v=fa[2], mem_u=fa[3]))
+                    rows.append(dict(victim=mB, vb=bB, vp=q, partner=mA, pb=bA, pp=p, factor=fB,
+                                     l2_v=fb[0], l2_u=fb[1], mem_v=fb[2], mem_u=fb[3]))
+            print(f"split {p}:{q} {m1}+{m2} done ({time.time() - t0:.0f}s)", flush=True)
+        ctx.destroy_gpulet(ga)
+        ctx.destroy_gpulet(gb)
+    os.makedirs(os.path.join(common.ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(common.ROOT, "profiles", "corun_b200.csv"), "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
+        w.writeheader()
+        w.writerows(rows)
+    X = np.array([[r["l2_v"], r["l2_u"], r["mem_v"], r["mem_u"], 1.0] for r in rows])
+    y = np.array([r["factor"] for r in rows])
+    perm = np.random.Generator(np.random.PCG64(a.seed)).permutation(len(y))
+    k = int(round(0.7 * len(y)))
+    tr, va = np.sort(perm[:k]), np.sort(perm[k:])
+    c = gpulet.fit_interference(X[tr], y[tr])
+    err = np.abs(np.maximum(1.0, X[va] @ c) - y[va]) / y[va]
+    cfg3 = [i for i, r in enumerate(rows) if {r["victim"], r["partner"]} == {"resnet50", "vgg16"} and r["vp"] == 50]
+    e3 = np.abs(np.maximum(1.0, X[cfg3] @ c) - y[cfg3]) / y[cfg3] if cfg3 else np.zeros(0)
+    summary = {"coeffs": [float(v) for v in c], "n_samples": len(y), "train": len(tr), "validation": len(va),
+               "err_p50": float(np.percentile(err, 50)), "err_p90": float(np.percentile(err, 90)),
+               "err_p95": float(np.percentile(err, 95)), "factor_p90": float(np.percentile(y, 90)),
+               "cfg3_samples": len(cfg3), "cfg3_err_max": float(e3.max()) if len(e3) else None,
+               "cfg3_err_p90": float(np.percentile(e3, 90)) if len(e3) else None,
+               "batches": batches, "splits": splits, "ms": a.ms}
+    with open(common.COEFFS_JSON, "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps(summary))
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

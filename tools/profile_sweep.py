@@ -53,7 +53,7 @@ def main():
     nsm = [0] * 6
     t0 = time.time()
     for gi, p in enumerate(common.GRID):
-        gid, n = ctx.create_gpulet(0, p)
+        (gid, n), = ctx.create_gpulets(0, [p])
         nsm[gi] = n
         for mi, m in enumerate(common.MODELS):
             if m not in models:

@@ -59,11 +59,9 @@ class Server:
         gls, _ = common.parse_plan(dump)
         lanes, made = [], []
         try:
-            for g in sorted(gls, key=lambda d: d["slot"]):
-                if not g["lanes"]:
-                    continue
-                gid, _n = self.ctx.create_gpulet(0, g["size"])
-                made.append(gid)
+            used = [g for g in sorted(gls, key=lambda d: d["slot"]) if g["lanes"]]
+            made = [gid for gid, _n in self.ctx.create_gpulets(0, [g["size"] for g in used])]
+            for g, gid in zip(used, made):
                 for ln in g["lanes"]:
                     m = ln["model"]
                     mi = common.MODELS.index(m)
