@@ -192,6 +192,23 @@ gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x_dev, const uint16_t* 
 gl_status gl_test_misc(gl_ctx* ctx, int gpu, int32_t type, const int32_t* iargs, int32_t n_iargs,
                        const uint16_t* params_host, int64_t n_params, const void* x_dev, void* y_dev);
 
+/* Statistics of the last kernel-unit test run (gl_test_gemm/conv/misc launch the
+ * one-op program once, after gl_set_tuning(3, n) warm-up launches): *ns = measured device duration
+ * (%globaltimer, program start -> final barrier); timeline (host buffer, `cap`
+ * uint64) = per-CTA tile stamps of the GEMM step, `*tl_per_cta` entries per CTA,
+ * entry 4*i+k of CTA c at [c * tl_per_cta + 4*i + k], k = 0 MMA start, 1 MMA last
+ * commit, 2 epilogue start, 3 epilogue end, ns from program start (0 = unused).
+ * Any pointer may be NULL.  Process-global; not thread-safe (a tuning tool). */
+gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* tl_per_cta);
+
+/* Program-builder tuning overrides for models loaded / tests built afterwards
+ * (process-global; 0 = automatic).  key 0: GEMM UMMA N tile (BN, multiple of 16,
+ * <= 256); key 1: split-K factor (1 = off); key 2: executor debug flags (tuning
+ * experiments, see ExecParams::dbg_flags); key 3: warm-up launches of the kernel-unit
+ * tests; key 4: 1 = gather every activation operand with cp.async (no TMA), to
+ * test that path.  GL_E_ARG for an unknown key. */
+gl_status gl_set_tuning(int32_t key, int32_t value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,8 +41,9 @@ __device__ __forceinline__ char* res(const BufRef& b, const Ctx& c) {
 }
 
 struct Smem {
-  uint8_t* a[kStages];
+  uint8_t* a[kStages];   // fixed 4-stage layout (scratch for the non-GEMM ops)
   uint8_t* b[kStages];
+  uint8_t* ring;         // GEMM ring: stage s at ring + s * stage_bytes (A 16 KB, then B)
   uint64_t* full;
   uint64_t* empty;
   uint64_t* tfull;
@@ -54,7 +55,14 @@ struct Smem {
   uint8_t* estage;   // epilogue staging: 4 warps x 32 rows x kEpiRowBytes (coalesced stores)
   uint64_t* dbg;     // optional per-step role stamps of CTA 0 (one-shot trace mode)
   int step;          // current step index (for dbg)
+  uint64_t* tl;      // optional per-tile timeline of step 0 for this CTA (tuning tool)
+  int tl_cap;
+  int flags;         // ExecParams::dbg_flags
 };
+
+__device__ __forceinline__ void tl_mark(const Smem& S, int i, int k) {
+  if (S.tl && S.step == 0 && 4 * i + k < S.tl_cap) S.tl[4 * i + k] = globaltimer();
+}
 
 // CTA 0 role stamps: [0] producer first tile start, [1] producer all issued,
 // [2] MMA first stage acquired, [3] MMA last commit, [4] epilogue first tfull,
@@ -64,18 +72,19 @@ __device__ __forceinline__ void dbg_mark(const Smem& S, int k) {
 }
 
 struct Pipe {
-  uint32_t stage = 0, phase = 0;  // smem ring position (producer / MMA each keep their own)
+  uint32_t stage = 0, nst = kStages;  // smem ring position and depth of the current GEMM step
+  uint32_t bits = 0;              // parity of each ring stage's barrier uses (producer / MMA each keep their own)
   uint32_t acc = 0;               // accumulator uses (MMA / epilogue each keep their own)
   uint32_t att_phase = 0;         // attention barrier parity (every thread tracks it)
   int npend = 0;
   uint32_t pend[kLag];
 };
 
+__device__ __forceinline__ uint32_t par(const Pipe& p) { return (p.bits >> p.stage) & 1u; }
+
 __device__ __forceinline__ void advance(Pipe& p) {
-  if (++p.stage == kStages) {
-    p.stage = 0;
-    p.phase ^= 1;
-  }
+  p.bits ^= 1u << p.stage;
+  if (++p.stage == p.nst) p.stage = 0;
 }
 
 // ------------------------------------------------------------------ gpu-let barrier
@@ -147,53 +156,42 @@ __device__ __forceinline__ void add_bf16x8(float* v, const uint4& u) {
 }
 
 // Warp-collective epilogue of the 32 rows [row0, row0 + 32) of one tile, for
-// its first `nfull` full 32-column chunks (bf16 row-major output): TMEM ->
-// registers, + bias (+ residual) -> ACT -> bf16.  Rows are staged in shared
-// memory so that residual loads and output stores move 16 B per lane with four
-// lanes per 64-B row segment; the residual of chunk j + 1 is prefetched by
-// cp.async while chunk j is computed (two staging buffers per warp).
+// `nfull` full 32-column chunks starting at output column n00 (bf16 row-major
+// output): TMEM -> registers, + bias (+ residual) -> ACT -> bf16.  Rows are
+// staged in shared memory so that residual loads and output stores move 16 B
+// per lane with four lanes per 64-B row segment.
 template <int ACT, bool RES>
 __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, const Ctx& X, uint32_t taddr,
-                                         int row0, int n00, int nfull, uint8_t* stg, int lane) {
+                                         int row0, int n00, int nfull, uint8_t* stg, int lane, bool nostore) {
   const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
   const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
   __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
   const int sr = lane >> 2, seg = lane & 3;
   const int64_t ldc = e.ldc;
   const int64_t coff = e.col_off;
-  auto prefetch = [&](int j) {
-    uint8_t* b = stg + (j & 1) * 32 * kEpiRowBytes;
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int r = it * 8 + sr;
-      const bool ok = row0 + r < g.M;
-      const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n00 + j * 32 + seg * 8 : rsd;
-      cp_async16(smem_u32(b + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
-    }
-    cp_async_commit();
-  };
-  if (RES && nfull > 0) prefetch(0);
   for (int j = 0; j < nfull; ++j) {
-    uint8_t* b = stg + (j & 1) * 32 * kEpiRowBytes;
+    const int n0 = n00 + j * 32;
     if (RES) {
-      if (j + 1 < nfull) {
-        prefetch(j + 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int r = it * 8 + sr;
+        const bool ok = row0 + r < g.M;
+        const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n0 + seg * 8 : rsd;
+        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
       }
-      __syncwarp();
+      cp_async_commit();
     }
     float v[32];
     tmem_ld32(taddr + j * 32, v);
-    const int n0 = n00 + j * 32;
     if (bias) {
       const uint4* bp = (const uint4*)(bias + n0);
 #pragma unroll
       for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, __ldg(bp + k));
     }
     if (RES) {
-      const uint4* rp = (const uint4*)(b + lane * kEpiRowBytes);
+      cp_async_wait<0>();
+      __syncwarp();
+      const uint4* rp = (const uint4*)(stg + lane * kEpiRowBytes);
 #pragma unroll
       for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, rp[k]);
     }
@@ -202,13 +200,13 @@ __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, c
     for (int c = 0; c < 32; ++c) o[c] = __float2bfloat16_rn(act_t<ACT>(v[c]));
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ((uint4*)(b + lane * kEpiRowBytes))[k] = ((const uint4*)o)[k];
+    for (int k = 0; k < 4; ++k) ((uint4*)(stg + lane * kEpiRowBytes))[k] = ((const uint4*)o)[k];
     __syncwarp();
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int r = it * 8 + sr;
-      if (row0 + r < g.M)
-        *(uint4*)(outp + (row0 + r) * ldc + coff + n0 + seg * 8) = *(const uint4*)(b + r * kEpiRowBytes + seg * 16);
+      if (row0 + r < g.M && !nostore)
+        *(uint4*)(outp + (row0 + r) * ldc + coff + n0 + seg * 8) = *(const uint4*)(stg + r * kEpiRowBytes + seg * 16);
     }
     __syncwarp();
   }
@@ -282,13 +280,147 @@ __device__ __forceinline__ int locate(const OpDesc* ops, int nops, int t, int& l
 }
 
 // ------------------------------------------------------------------ GEMM step (K1-K4)
-__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& S, Pipe& P) {
-  int total = 0;
-  for (int i = 0; i < nops; ++i) total += ops[i].n_units;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Roles.  Steps whose operands all come by TMA: warp 9 (one thread) produces,
+// warp 8 (one thread) issues tcgen05.mma, warps 0-7 run the epilogue (warp w
+// owns TMEM lanes 32*(w%4).. and one half of the tile's columns).  Steps with
+// a gathered operand: warps 0-3 gather (cp.async) and issue the TMA half,
+// warps 4-7 run the epilogue over all columns.  The smem ring depth follows
+// the step's widest N tile: 192 KB / (16 KB + BN x 128 B), at most 8 stages.
+// One 64-wide K block of the im2col A operand: 64 / cb TMA im2col loads of
+// [128 pixels x cb channels], box j at sa + j * 128 * cb * 2.  k = (tap, c) with
+// c fastest, so a box never straddles a tap (cb divides C).  Taps past the
+// filter (K padding; the weights there are zero) re-read tap (0, 0) so the smem
+// operand stays finite.
+__device__ __forceinline__ void im2col_kblock(const GemmArgs& g, const void* tmap, uint64_t* bar, uint32_t sa, int kb,
+                                              int icw, int ich, int icn) {
+  const int cb = g.a_cb ? g.a_cb : 64;
+  const int ntaps = g.ga.KH * g.ga.KW;
+  for (int j = 0; j < 64 / cb; ++j) {
+    const int k0 = kb * 64 + j * cb;
+    int tap = k0 / g.ga.C, c0 = k0 - tap * g.ga.C;
+    if (tap >= ntaps) tap = 0, c0 = 0;
+    const int kh = tap / g.ga.KW, kw = tap - kh * g.ga.KW;
+    tma_load_im2col_4d(sa + j * 128 * cb * 2, tmap, bar, c0, icw, ich, icn, (uint16_t)kw, (uint16_t)kh);
+  }
+}
 
-  if (warp < 4) {
-    // ---------------- producers
+// UMMA smem descriptor of the A operand for the K=16 step k (0..3) of a stage.
+__device__ __forceinline__ uint64_t a_desc(const GemmArgs& g, uint32_t a0, int k) {
+  if (g.a_tma != SRC_IM2COL || g.a_cb == 0 || g.a_cb == 64) return umma_sdesc_sw128(a0 + k * 32);
+  switch (g.a_cb) {
+    case 32: return umma_sdesc(a0 + (k >> 1) * 8192 + (k & 1) * 32, 4, 512, 16);       // SW64, 64-B rows
+    case 16: return umma_sdesc(a0 + k * 4096, 6, 256, 16);                            // SW32, 32-B rows
+    default: return umma_sdesc(a0 + k * 4096, 0, 128, 2048);                         // no swizzle, 16-B rows
+  }
+}
+
+__device__ __forceinline__ uint32_t stage_bytes_for(int bn) {
+  return (uint32_t)kStageBytesA + (uint32_t)((bn * 128 + 1023) & ~1023);
+}
+
+// Epilogue of one warp over the tile columns [c0, c1) (relative to the tile).
+__device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, const Smem& S, uint32_t taddr, int mb,
+                                              int nb, int kb0, int q, int c0, int c1, uint8_t* stg, int lane) {
+  const Epilogue& e = g.ep;
+  const int m = mb * 128 + q * 32 + lane;
+  const int nend = min(g.N, (nb + 1) * g.BN);
+  c1 = min(c1, nend - nb * g.BN);
+  if (c1 <= c0) return;
+  int j0 = c0;   // first column (within the tile) not yet stored
+  if (S.flags & 1) {
+    for (int j = c0; j < c1; j += 32) {
+      float v[32];
+      tmem_ld32(taddr + j, v);
+      if (v[0] == 1234.5f && v[31] == -1.f) store_one(e, X, m, 0, v[1]);
+    }
+    return;
+  }
+  if (e.splitk > 1) {
+    // split-K: this split's fp32 partial tile -> ws[split][R][Cc] in OUTPUT
+    // order (R x Cc = M x N, or N x M for swap-AB), L2-only stores; an
+    // OP_SPLITK_FINAL step reduces the splits in order.
+    const int split = kb0 / g.kb_per_split;
+    for (int j = c0; j < c1; j += 32) {
+      float v[32];
+      tmem_ld32(taddr + j, v);
+      const int n0 = nb * g.BN + j;
+      const int nn = min(32, c1 - j);
+      if (m < g.M) {
+        if (e.transpose) {
+          float* wp = (float*)res(e.ws, X) + (int64_t)split * g.M * g.N + m;
+          for (int c = 0; c < nn; ++c) __stcg(wp + (int64_t)(n0 + c) * g.M, v[c]);
+        } else {
+          float* wp = (float*)res(e.ws, X) + ((int64_t)split * g.M + m) * g.N;
+          if (nn == 32 && (g.N & 3) == 0) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              __stcg((float4*)(wp + n0) + c, make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+          } else {
+            for (int c = 0; c < nn; ++c) __stcg(wp + n0 + c, v[c]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (!e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 && (e.col_off % 8) == 0) {
+    // bf16 row-major output: warp-collective staged epilogue on the full 32-column chunks
+    const int nfull = (c1 - c0) / 32;
+    const bool rs = e.res.kind != BUF_NONE;
+    const int row0 = mb * 128 + q * 32, n00 = nb * g.BN + c0;
+    const uint32_t ta = taddr + c0;
+    const bool ns = (S.flags & 2) != 0;
+    switch (e.act * 2 + (rs ? 1 : 0)) {
+      case 0: epi_rows<ACT_NONE, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 1: epi_rows<ACT_NONE, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 2: epi_rows<ACT_RELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 3: epi_rows<ACT_RELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 4: epi_rows<ACT_GELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 5: epi_rows<ACT_GELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 6: epi_rows<ACT_TANH, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      default: epi_rows<ACT_TANH, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+    }
+    j0 = c0 + nfull * 32;
+  }
+  // remaining (partial / fp32 / transposed / strided) columns, element-wise
+  for (int j = j0; j < c1; j += 32) {
+    const int n0 = nb * g.BN + j;
+    float v[32];
+    tmem_ld32(taddr + j, v);
+    if (m < g.M)
+      for (int c = 0; c < 32 && j + c < c1; ++c) store_one(e, X, m, n0 + c, v[c]);
+  }
+}
+
+__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& S, Pipe& P) {
+  int total = 0, maxbn = 16;
+  bool gstep = false;
+  for (int i = 0; i < nops; ++i) {
+    total += ops[i].n_units;
+    maxbn = max(maxbn, ops[i].g.BN);
+    gstep |= ops[i].g.a_tma == SRC_GATHER || ops[i].g.b_tma == SRC_GATHER;
+  }
+  const uint32_t sbytes = stage_bytes_for(maxbn);
+  P.nst = min((uint32_t)kMaxStages, (uint32_t)kRingBytes / sbytes);
+  P.stage = 0;
+  const uint32_t ring = smem_u32(S.ring);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // The producer / epilogue roles move between warps from step to step, so
+  // every thread ends the step with the ring and accumulator state the
+  // participating threads reached: this CTA's tile and k-block counts.
+  const uint32_t bits0 = P.bits, acc0 = P.acc;
+  int my_tiles = 0, my_kb = 0;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    int lt;
+    const OpDesc* op = ops + locate(ops, nops, tile, lt);
+    int mb, nb, kb0, kb1;
+    decode_tile(op->g, lt, mb, nb, kb0, kb1);
+    ++my_tiles;
+    my_kb += kb1 - kb0;
+  }
+
+  if (gstep && warp < 4) {
+    // ---------------- gather producers (128 threads; thread 0 also issues the TMA half)
     const int t = threadIdx.x;
     if (t == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -311,7 +443,6 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const __nv_bfloat16* gx = (const __nv_bfloat16*)res(gg.x, X);
       RowCache rc;
       if (gather) rowcache_init(rc, gg, grow0, grows, t);
-      // im2col traversal start: window top-left of the tile's first output pixel
       int icw = 0, ich = 0, icn = 0;
       if (g.a_tma == SRC_IM2COL && t == 0) {
         const int m0 = mb * 128, HoWo = g.ga.Ho * g.ga.Wo;
@@ -322,25 +453,23 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       }
       const uint32_t tx = (g.a_tma ? 128 * 128 : 0) + (g.b_tma ? g.BN * 128 : 0);
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&S.empty[P.stage], P.phase ^ 1);
+        mbar_wait(&S.empty[P.stage], par(P) ^ 1);   // empty[stage]
+        const uint32_t sa = ring + P.stage * sbytes, sbb = sa + kStageBytesA;
         if (t == 0) {
           mbar_arrive_expect_tx(&S.full[P.stage], tx);
           if (g.a_tma == SRC_TMA) {
-            tma_load_2d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+            tma_load_2d(sa, &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
           } else if (g.a_tma == SRC_IM2COL) {
-            const int k0 = kb * 64, tap = k0 / g.ga.C, c0 = k0 - tap * g.ga.C;
-            const int kh = tap / g.ga.KW, kw = tap - kh * g.ga.KW;
-            tma_load_im2col_4d(smem_u32(S.a[P.stage]), &op->tmap_a, &S.full[P.stage], c0, icw, ich, icn,
-                               (uint16_t)kw, (uint16_t)kh);
+            im2col_kblock(g, &op->tmap_a, &S.full[P.stage], sa, kb, icw, ich, icn);
           }
-          if (g.b_tma) tma_load_2d(smem_u32(S.b[P.stage]), &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
+          if (g.b_tma) tma_load_2d(sbb, &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
         }
         if (!gather) {
           mbar_arrive(&S.full[P.stage]);
           advance(P);
           continue;
         }
-        gather_kblock(gg, gx, rc, grows, kb, g.K_real, smem_u32(g.a_tma ? S.b[P.stage] : S.a[P.stage]), t);
+        gather_kblock(gg, gx, rc, grows, kb, g.K_real, g.a_tma ? sbb : sa, t);
         cp_async_commit();
         if (P.npend == kLag) {
           cp_async_wait<kLag>();
@@ -359,10 +488,52 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     for (int i = 0; i < P.npend; ++i) mbar_arrive(&S.full[P.pend[i]]);
     P.npend = 0;
     if (t == 0) dbg_mark(S, 1);
+  } else if (!gstep && warp == 9) {
+    // ---------------- TMA producer (one thread)
+    if (lane == 0) {
+      dbg_mark(S, 0);
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int lt;
+        const OpDesc* op = ops + locate(ops, nops, tile, lt);
+        const GemmArgs& g = op->g;
+        int mb, nb, kb0, kb1;
+        decode_tile(g, lt, mb, nb, kb0, kb1);
+        int icw = 0, ich = 0, icn = 0;
+        if (g.a_tma == SRC_IM2COL) {
+          const int m0 = mb * 128, HoWo = g.ga.Ho * g.ga.Wo;
+          icn = m0 / HoWo;
+          const int rem = m0 - icn * HoWo, ho = rem / g.ga.Wo, wo = rem - ho * g.ga.Wo;
+          ich = ho * g.ga.stride - g.ga.pad;
+          icw = wo * g.ga.stride - g.ga.pad;
+        }
+        const uint32_t tx = 128 * 128 + g.BN * 128;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&S.empty[P.stage], par(P) ^ 1);   // empty[stage]
+          if (S.flags & 8) {
+            mbar_arrive_cnt(&S.full[P.stage], 129);
+            advance(P);
+            continue;
+          }
+          const uint32_t sa = ring + P.stage * sbytes, sbb = sa + kStageBytesA;
+          mbar_arrive_expect_tx(&S.full[P.stage], tx);
+          if (g.a_tma == SRC_TMA) {
+            tma_load_2d(sa, &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+          } else {
+            im2col_kblock(g, &op->tmap_a, &S.full[P.stage], sa, kb, icw, ich, icn);
+          }
+          tma_load_2d(sbb, &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
+          mbar_arrive_cnt(&S.full[P.stage], 128);
+          advance(P);
+        }
+      }
+      dbg_mark(S, 1);
+    }
+    __syncwarp();
   } else if (warp == 8) {
     // ---------------- MMA issuer
     if (lane == 0) {
       const uint32_t tbase = *S.tmem_base;
+      int ntile = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         int lt;
         const OpDesc* op = ops + locate(ops, nops, tile, lt);
@@ -372,193 +543,276 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         const uint32_t acc = P.acc & 1, use = P.acc >> 1;
         mbar_wait(&S.tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
+        tl_mark(S, ntile, 0);
         const uint32_t d = tbase + acc * 256;
         const uint32_t idesc = umma_idesc_bf16(128, g.BN);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&S.full[P.stage], P.phase);
+          mbar_wait(&S.full[P.stage], par(P));
           tc_fence_after();
           if (tile == (int)blockIdx.x && kb == kb0) dbg_mark(S, 2);
-          const uint32_t a0 = smem_u32(S.a[P.stage]), b0 = smem_u32(S.b[P.stage]);
+          const uint32_t a0 = ring + P.stage * sbytes, b0 = a0 + kStageBytesA;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(d, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&S.empty[P.stage]);
+            if (!(S.flags & 4))
+              umma_bf16(d, a_desc(g, a0, k), umma_sdesc_sw128(b0 + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit(&S.empty[P.stage]);   // empty[stage]
           advance(P);
         }
         umma_commit(&S.tfull[acc]);
+        tl_mark(S, ntile++, 1);
         ++P.acc;
       }
       dbg_mark(S, 3);
     }
     __syncwarp();
-  } else {
-    // ---------------- epilogue (warps 4-7 -> TMEM lanes 0-127)
-    const int q = warp - 4;
+  } else if (warp < 8) {
+    // ---------------- epilogue: warps 4-7 (all columns) or 0-7 (column halves)
+    const int q = warp & 3, half = warp < 4 ? 1 : 0;
     const uint32_t tbase = *S.tmem_base;
+    uint8_t* stg = S.estage + warp * 32 * kEpiRowBytes;
+    const uint32_t arrive_n = gstep ? 2u : 1u;
+    int ntile = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const OpDesc* op = ops + locate(ops, nops, tile, lt);
       const GemmArgs& g = op->g;
-      const Epilogue& e = g.ep;
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
       const uint32_t acc = P.acc & 1, use = P.acc >> 1;
       mbar_wait(&S.tfull[acc], use & 1);
       tc_fence_after();
-      if (tile == (int)blockIdx.x && q == 0 && lane == 0) dbg_mark(S, 4);
-      const int m = mb * 128 + q * 32 + lane;
-      const int nend = min(g.N, (nb + 1) * g.BN);
+      const bool lead = q == 0 && half == 0 && lane == 0;
+      if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
+      if (lead) tl_mark(S, ntile, 2);
       const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * 256;
-      int j0 = 0;   // first column (within the tile) not yet stored
-      if (e.splitk > 1) {
-        // split-K: this split's fp32 partial tile -> ws[split][M][N] (L2-only
-        // stores); an OP_SPLITK_FINAL step reduces the splits in order.
-        float* wp = (float*)res(e.ws, X) + ((int64_t)(kb0 / g.kb_per_split) * g.M + m) * g.N;
-        for (int j = 0; j < g.BN; j += 32) {
-          float v[32];
-          tmem_ld32(taddr + j, v);
-          const int n0 = nb * g.BN + j;
-          if (m < g.M && n0 < nend) {
-            if (n0 + 32 <= nend && (g.N & 3) == 0) {
-#pragma unroll
-              for (int c = 0; c < 8; ++c)
-                __stcg((float4*)(wp + n0) + c, make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
-            } else {
-              for (int c = 0; c < 32 && n0 + c < nend; ++c) __stcg(wp + n0 + c, v[c]);
-            }
-          }
-        }
-        j0 = g.BN;
-      } else if (!e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 &&
-                 (e.col_off % 8) == 0) {
-        // bf16 row-major output: warp-collective staged epilogue on the full
-        // 32-column chunks (residual prefetched by cp.async one chunk ahead)
-        const int nfull = (nend - nb * g.BN) / 32;
-        const bool rs = e.res.kind != BUF_NONE;
-        uint8_t* stg = S.estage + q * 2 * 32 * kEpiRowBytes;
-        const int row0 = mb * 128 + q * 32, n00 = nb * g.BN;
-        switch (e.act * 2 + (rs ? 1 : 0)) {
-          case 0: epi_rows<ACT_NONE, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 1: epi_rows<ACT_NONE, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 2: epi_rows<ACT_RELU, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 3: epi_rows<ACT_RELU, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 4: epi_rows<ACT_GELU, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 5: epi_rows<ACT_GELU, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          case 6: epi_rows<ACT_TANH, false>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-          default: epi_rows<ACT_TANH, true>(e, g, X, taddr, row0, n00, nfull, stg, lane); break;
-        }
-        j0 = nfull * 32;
+      int c0 = 0, c1 = g.BN;
+      if (!gstep) {
+        const int split = min(g.BN, ((g.BN / 2) + 31) & ~31);
+        c0 = half ? split : 0;
+        c1 = half ? g.BN : split;
       }
-      // remaining (partial / fp32 / transposed / strided) columns, element-wise
-      for (int j = j0; j < g.BN; j += 32) {
-        const int n0 = nb * g.BN + j;
-        if (n0 >= nend) break;
-        float v[32];
-        tmem_ld32(taddr + j, v);
-        if (m < g.M)
-          for (int c = 0; c < 32 && n0 + c < nend; ++c) store_one(e, X, m, n0 + c, v[c]);
-      }
+      epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane);
       tc_fence_before();
-      mbar_arrive(&S.tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cnt(&S.tempty[acc], arrive_n);
+      if (lead) tl_mark(S, ntile, 3);
+      ++ntile;
       ++P.acc;
     }
-    if (q == 0 && lane == 0) dbg_mark(S, 5);
+    if (q == 0 && half == 0 && lane == 0) dbg_mark(S, 5);
   }
+  uint32_t flips = 0;
+  for (uint32_t st = 0; st < P.nst; ++st) {
+    const uint32_t uses = my_kb / P.nst + (st < my_kb % P.nst ? 1u : 0u);
+    flips |= (uses & 1u) << st;
+  }
+  P.bits = bits0 ^ flips;
+  P.stage = 0;
+  P.acc = acc0 + my_tiles;
 }
 
 // ------------------------------------------------------------------ split-K final
+// Sums the fp32 partials ws[s][R][Cc] (output order, see the split-K epilogue)
+// over s in order, then + bias (+ residual) -> activation -> store.  8 output
+// columns per thread (16-B bf16 stores) when the output mapping allows it.
 __device__ __noinline__ void splitk_final(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const Epilogue& e = a.ep;
   const float* ws = (const float*)res(e.ws, X);
-  const int64_t total = (int64_t)a.rows * a.cols;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int m = (int)(i / a.cols), n = (int)(i - (int64_t)m * a.cols);
+  const int R = e.transpose ? a.cols : a.rows, Cc = e.transpose ? a.rows : a.cols;
+  const int64_t total = (int64_t)R * Cc;
+  const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+  const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
+  const bool bias_on_c = (e.bias_on_m != 0) == (e.transpose != 0);
+  const bool vec = (Cc % 8) == 0 && (e.ldc % 8) == 0 && (e.col_off % 8) == 0 && (e.img_stride % 8) == 0 &&
+                   !e.out_fp32 && bias_on_c;
+  const int tstride = gridDim.x * blockDim.x;
+  if (vec) {
+    const int64_t nv = total / 8;
+    const int cv = Cc / 8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += tstride) {
+      const int r = (int)(i / cv), c = (int)(i - (int64_t)r * cv) * 8;
+      float v[8];
+      const float4* p = (const float4*)(ws + (int64_t)r * Cc + c);
+      float4 u0 = __ldcg(p), u1 = __ldcg(p + 1);
+      v[0] = u0.x, v[1] = u0.y, v[2] = u0.z, v[3] = u0.w, v[4] = u1.x, v[5] = u1.y, v[6] = u1.z, v[7] = u1.w;
+      for (int sp = 1; sp < e.splitk; ++sp) {
+        p = (const float4*)(ws + (int64_t)sp * total + (int64_t)r * Cc + c);
+        u0 = __ldcg(p), u1 = __ldcg(p + 1);
+        v[0] += u0.x, v[1] += u0.y, v[2] += u0.z, v[3] += u0.w, v[4] += u1.x, v[5] += u1.y, v[6] += u1.z,
+            v[7] += u1.w;
+      }
+      if (bias) add_bf16x8(v, *(const uint4*)(bias + c));
+      const int64_t idx = out_index(e, r, c);
+      if (rsd) add_bf16x8(v, *(const uint4*)(rsd + idx));
+      __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = __float2bfloat16_rn(act_f(v[k], e.act));
+      *(uint4*)((__nv_bfloat16*)res(e.out, X) + idx) = *(const uint4*)o;
+    }
+    return;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += tstride) {
+    const int r = (int)(i / Cc), c = (int)(i - (int64_t)r * Cc);
     float v = 0.f;
-    for (int s = 0; s < e.splitk; ++s) v += __ldcg(ws + (int64_t)s * total + i);
-    store_one(e, X, m, n, v);
+    for (int sp = 0; sp < e.splitk; ++sp) v += __ldcg(ws + (int64_t)sp * total + i);
+    // store_one takes GEMM coordinates (m, n)
+    if (e.transpose)
+      store_one(e, X, c, r, v);
+    else
+      store_one(e, X, r, c, v);
   }
 }
 
 // ------------------------------------------------------------------ depthwise 3x3 (K5)
+// Thread item = (image, output row, strip of STRIP output columns, 8-channel
+// group); consecutive threads take consecutive channel groups (16-B coalesced).
+// All input vectors of an item are loaded (zero outside the image) before any
+// arithmetic so the loads overlap; the strip shares its input columns across
+// outputs.  32-bit index math (every tensor here is < 2^31 elements).
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+template <int STRIDE, int STRIP>
+__device__ __forceinline__ void dw_item(const MiscArgs& a, const __nv_bfloat16* __restrict__ x, const uint4 (&wv)[9],
+                                        const uint4& bv, __nv_bfloat16* __restrict__ y, int n, int ho, int wo0,
+                                        int cg) {
+  constexpr int NCOL = (STRIP - 1) * STRIDE + 3;
+  uint4 xin[3][NCOL];
+  const int wi0 = wo0 * STRIDE - a.pad;
+#pragma unroll
+  for (int kh = 0; kh < 3; ++kh) {
+    const int hi = ho * STRIDE - a.pad + kh;
+    const bool hok = hi >= 0 && hi < a.H;
+    const __nv_bfloat16* row = x + ((n * a.H + (hok ? hi : 0)) * a.W) * a.C + cg * 8;
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) {
+      const int wi = wi0 + j;
+      const bool ok = hok && wi >= 0 && wi < a.W;
+      xin[kh][j] = ok ? __ldg((const uint4*)(row + wi * a.C)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  float acc[STRIP][8];
+  const uint32_t* bw = (const uint32_t*)&bv;
+#pragma unroll
+  for (int o = 0; o < STRIP; ++o)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc[o][2 * c] = bf_lo(bw[c]);
+      acc[o][2 * c + 1] = bf_hi(bw[c]);
+    }
+#pragma unroll
+  for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+    for (int kw = 0; kw < 3; ++kw) {
+      const uint32_t* ww = (const uint32_t*)&wv[kh * 3 + kw];
+#pragma unroll
+      for (int o = 0; o < STRIP; ++o) {
+        const uint32_t* xx = (const uint32_t*)&xin[kh][o * STRIDE + kw];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[o][2 * c] = fmaf(bf_lo(xx[c]), bf_lo(ww[c]), acc[o][2 * c]);
+          acc[o][2 * c + 1] = fmaf(bf_hi(xx[c]), bf_hi(ww[c]), acc[o][2 * c + 1]);
+        }
+      }
+    }
+#pragma unroll
+  for (int o = 0; o < STRIP; ++o) {
+    if (wo0 + o >= a.Wo) break;
+    __align__(16) __nv_bfloat16 ob[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) ob[c] = __float2bfloat16_rn(act_f(acc[o][c], a.act));
+    *(uint4*)(y + ((n * a.Ho + ho) * a.Wo + wo0 + o) * a.C + cg * 8) = *(const uint4*)ob;
+  }
+}
+
+template <int STRIDE, int STRIP>
+__device__ __forceinline__ void dw_loop(const MiscArgs& a, const __nv_bfloat16* x, const __nv_bfloat16* w,
+                                        const __nv_bfloat16* b, __nv_bfloat16* y) {
+  const int CG = a.C / 8, WS = (a.Wo + STRIP - 1) / STRIP;
+  const int total = a.N * a.Ho * WS * CG;
+  const int stride_t = gridDim.x * blockDim.x;
+  int cg_cached = -1;
+  uint4 wv[9], bv = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride_t) {
+    const int cg = i % CG;
+    int p = i / CG;
+    const int ws = p % WS;
+    p /= WS;
+    const int ho = p % a.Ho, n = p / a.Ho;
+    if (cg != cg_cached) {
+      cg_cached = cg;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) wv[t] = __ldg((const uint4*)(w + t * a.C + cg * 8));
+      bv = __ldg((const uint4*)(b + cg * 8));
+    }
+    dw_item<STRIDE, STRIP>(a, x, wv, bv, y, n, ho, ws * STRIP, cg);
+  }
+}
+
 __device__ __noinline__ void dwconv(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   const __nv_bfloat16* w = (const __nv_bfloat16*)res(a.w, X);   // [9][C] tap-major
   const __nv_bfloat16* b = (const __nv_bfloat16*)res(a.b, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
-  const int CG = a.C / 8;
-  const int64_t total = (int64_t)a.N * a.Ho * a.Wo * CG;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i % CG);
-    int64_t p = i / CG;
-    const int wo = (int)(p % a.Wo);
-    p /= a.Wo;
-    const int ho = (int)(p % a.Ho);
-    const int n = (int)(p / a.Ho);
-    float acc[8];
-    const uint4 bv = *(const uint4*)(b + cg * 8);
-    const __nv_bfloat16* bb = (const __nv_bfloat16*)&bv;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = __bfloat162float(bb[c]);
-#pragma unroll
-    for (int kh = 0; kh < 3; ++kh) {
-      const int hi = ho * a.stride - a.pad + kh;
-      if (hi < 0 || hi >= a.H) continue;
-#pragma unroll
-      for (int kw = 0; kw < 3; ++kw) {
-        const int wi = wo * a.stride - a.pad + kw;
-        if (wi < 0 || wi >= a.W) continue;
-        const uint4 xv = *(const uint4*)(x + (((int64_t)n * a.H + hi) * a.W + wi) * a.C + cg * 8);
-        const uint4 wv = *(const uint4*)(w + (kh * 3 + kw) * a.C + cg * 8);
-        const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
-        const __nv_bfloat16* ww = (const __nv_bfloat16*)&wv;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = fmaf(__bfloat162float(xx[c]), __bfloat162float(ww[c]), acc[c]);
-      }
-    }
-    __align__(16) __nv_bfloat16 o[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(act_f(acc[c], a.act));
-    *(uint4*)(y + (((int64_t)n * a.Ho + ho) * a.Wo + wo) * a.C + cg * 8) = *(const uint4*)o;
-  }
+  if (a.stride == 1)
+    dw_loop<1, 4>(a, x, w, b, y);
+  else
+    dw_loop<2, 2>(a, x, w, b, y);
 }
 
 // ------------------------------------------------------------------ max pool (K6)
+// One output pixel x 8 channels per thread item; the K x K window's vectors are
+// all loaded (predicated) before the max so the loads overlap.  Max commutes
+// with bf16 rounding, so bf16 max is exact.
+template <int K>
+__device__ __forceinline__ void maxpool_k(const MiscArgs& a, const __nv_bfloat16* __restrict__ x,
+                                          __nv_bfloat16* __restrict__ y) {
+  const int CG = a.C / 8;
+  const int total = a.N * a.Ho * a.Wo * CG;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int cg = i % CG;
+    int p = i / CG;
+    const int wo = p % a.Wo;
+    p /= a.Wo;
+    const int ho = p % a.Ho, n = p / a.Ho;
+    const int h0 = ho * a.stride - a.pad, w0 = wo * a.stride - a.pad;
+    uint4 v[K * K];
+    bool ok[K * K];
+#pragma unroll
+    for (int kh = 0; kh < K; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < K; ++kw) {
+        const int hi = h0 + kh, wi = w0 + kw;
+        ok[kh * K + kw] = hi >= 0 && hi < a.H && wi >= 0 && wi < a.W;
+        v[kh * K + kw] = ok[kh * K + kw] ? __ldg((const uint4*)(x + ((n * a.H + hi) * a.W + wi) * a.C + cg * 8))
+                                         : make_uint4(0u, 0u, 0u, 0u);
+      }
+    __nv_bfloat162 mx[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) mx[c] = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll
+    for (int t = 0; t < K * K; ++t) {
+      if (!ok[t]) continue;
+      const __nv_bfloat162* xx = (const __nv_bfloat162*)&v[t];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mx[c] = __hmax2(mx[c], xx[c]);
+    }
+    *(uint4*)(y + ((n * a.Ho + ho) * a.Wo + wo) * a.C + cg * 8) = *(const uint4*)mx;
+  }
+}
+
 __device__ __noinline__ void maxpool(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
-  const int CG = a.C / 8;
-  const int64_t total = (int64_t)a.N * a.Ho * a.Wo * CG;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int cg = (int)(i % CG);
-    int64_t p = i / CG;
-    const int wo = (int)(p % a.Wo);
-    p /= a.Wo;
-    const int ho = (int)(p % a.Ho);
-    const int n = (int)(p / a.Ho);
-    float mx[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) mx[c] = -INFINITY;
-    for (int kh = 0; kh < a.k; ++kh) {
-      const int hi = ho * a.stride - a.pad + kh;
-      if (hi < 0 || hi >= a.H) continue;
-      for (int kw = 0; kw < a.k; ++kw) {
-        const int wi = wo * a.stride - a.pad + kw;
-        if (wi < 0 || wi >= a.W) continue;
-        const uint4 xv = *(const uint4*)(x + (((int64_t)n * a.H + hi) * a.W + wi) * a.C + cg * 8);
-        const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) mx[c] = fmaxf(mx[c], __bfloat162float(xx[c]));
-      }
-    }
-    __align__(16) __nv_bfloat16 o[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(mx[c]);
-    *(uint4*)(y + (((int64_t)n * a.Ho + ho) * a.Wo + wo) * a.C + cg * 8) = *(const uint4*)o;
-  }
+  if (a.k == 2)
+    maxpool_k<2>(a, x, y);
+  else if (a.k == 3)
+    maxpool_k<3>(a, x, y);
+  else
+    __trap();
 }
 
 // ------------------------------------------------------------------ global avg pool (K6)
@@ -949,6 +1203,20 @@ __device__ __noinline__ void softmax_rows(const OpDesc* op, const Ctx& X) {
   }
 }
 
+// ------------------------------------------------------------------ 16-B vector copy
+__device__ __noinline__ void copy_vec(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const uint4* x = (const uint4*)res(a.x, X);
+  uint4* y = (uint4*)res(a.y, X);
+  const int n = a.rows, st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * st < n; i += 4 * st) {
+    const uint4 v0 = __ldcs(x + i), v1 = __ldcs(x + i + st), v2 = __ldcs(x + i + 2 * st), v3 = __ldcs(x + i + 3 * st);
+    y[i] = v0, y[i + st] = v1, y[i + 2 * st] = v2, y[i + 3 * st] = v3;
+  }
+  for (; i < n; i += st) y[i] = __ldcs(x + i);
+}
+
 __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P) {
   if (op->type == OP_ATTENTION && op->g.act_tmap) {   // qkv tensor map bound: tensor-core path
     attention_tc(op, X, S, P);
@@ -964,6 +1232,7 @@ __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P)
     case OP_ATTENTION: attention(op, X, S.scratch); break;
     case OP_SOFTMAX: softmax_rows(op, X); break;
     case OP_SPLITK_FINAL: splitk_final(op, X); break;
+    case OP_COPY: copy_vec(op, X); break;
     default: __trap();
   }
 }
@@ -1003,28 +1272,32 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
     S.a[s] = base + s * kStageBytesA;
     S.b[s] = base + kStages * kStageBytesA + s * kStageBytesB;
   }
-  uint64_t* bars = (uint64_t*)(base + kStages * (kStageBytesA + kStageBytesB));
-  S.full = bars;
-  S.empty = bars + kStages;
-  S.tfull = bars + 2 * kStages;
-  S.tempty = bars + 2 * kStages + 2;
-  S.att = bars + 2 * kStages + 4;
-  S.tmem_base = (uint32_t*)(bars + 2 * kStages + 7);
-  S.epi_flag = (int*)(bars + 2 * kStages + 8);
-  S.estage = base + kStages * (kStageBytesA + kStageBytesB) + 1024;
+  S.ring = base;
+  uint64_t* bars = (uint64_t*)(base + kRingBytes);
+  S.full = bars;                          // [kMaxStages] full, then [kMaxStages] empty
+  S.empty = bars + kMaxStages;
+  S.tfull = bars + 2 * kMaxStages;
+  S.tempty = bars + 2 * kMaxStages + 2;
+  S.att = bars + 2 * kMaxStages + 4;
+  S.tmem_base = (uint32_t*)(bars + 2 * kMaxStages + 7);
+  S.epi_flag = (int*)(bars + 2 * kMaxStages + 8);
+  S.estage = base + kRingBytes + 1024;
   S.scratch = base;
   S.dbg = nullptr;
   S.step = 0;
+  S.tl = p.tl ? p.tl + (size_t)blockIdx.x * p.tl_cap : nullptr;
+  S.tl_cap = p.tl_cap;
+  S.flags = p.dbg_flags;
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&S.full[s], 128 + 1);
       mbar_init(&S.empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&S.tfull[s], 1);
-      mbar_init(&S.tempty[s], 128);
+      mbar_init(&S.tempty[s], 8);   // one arrival per epilogue warp (count 2 each when only 4 run)
     }
     for (int s = 0; s < 3; ++s) mbar_init(&S.att[s], 1);
     fence_mbar_init();

@@ -15,6 +15,8 @@
 
 namespace gl {
 
+int g_tune[kTuneKeys] = {0};
+
 static const char* kNames[6] = {"lenet5", "googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"};
 int model_kind_count() { return 6; }
 const char* model_name(int kind) { return (kind >= 0 && kind < 6) ? kNames[kind] : "?"; }
@@ -253,22 +255,23 @@ class Builder {
     g.N = w.rows;
     g.K_real = w.K_real;
     g.K_pad = w.K_pad;
-    const int nnb = (g.N + 255) / 256;
-    g.BN = std::max(16, rup((g.N + nnb - 1) / nnb, 16));
-    g.n_nblk = (g.N + g.BN - 1) / g.BN;
     g.n_mblk = (M + 127) / 128;
+    g.BN = pick_bn(g.N, g.n_mblk);
+    g.n_nblk = (g.N + g.BN - 1) / g.BN;
     g.a_tma = SRC_GATHER;
     g.b_tma = SRC_TMA;
     // workspace activations are fetched by TMA (tensor map bound per workspace):
     // 2-D tiles for 1x1/stride-1 convs and linears, im2col mode for KxK or
     // strided convs with 64-channel-aligned inputs; the rest is gathered.
-    if (ga.x.kind == BUF_WS && ga.C % 8 == 0 && ga.lda % 8 == 0) {
+    if (ga.x.kind == BUF_WS && ga.C % 8 == 0 && ga.lda % 8 == 0 && !g_tune[TUNE_GATHER]) {
       if (ga.KH == 1 && ga.stride == 1 && ga.pad == 0) {
         g.a_tma = SRC_TMA;
         g.act_tmap = 1;
-      } else if (ga.C % 64 == 0 && ga.lda == ga.C) {
+      } else if (ga.lda == ga.C) {
+        // im2col boxes of cb channels: the largest power of two <= 64 dividing C
         g.a_tma = SRC_IM2COL;
         g.act_tmap = 1;
+        g.a_cb = std::min(64, ga.C & -ga.C);
       }
     }
     g.ga = ga;
@@ -314,12 +317,28 @@ class Builder {
     prog.weight_bytes += (double)w.rows * w.K_real * 2;
   }
 
+  // UMMA N tile: the widest balanced tile (<= 256 columns) that still gives
+  // about one wave of tiles over a whole B200 (148 SMs); narrower tiles are
+  // preferred to split-K, which costs an extra reduction step (measured:
+  // tools/gemm_micro.py, ResNet-50 b=32 layer3/4 shapes).
+  static int pick_bn(int N, int n_mblk) {
+    if (g_tune[TUNE_BN] >= 16 && g_tune[TUNE_BN] <= 256) return std::min(rup(N, 16), rup(g_tune[TUNE_BN], 16));
+    int bn = 0;
+    for (int cap = 256; cap >= 64; cap /= 2) {
+      const int nnb = (N + cap - 1) / cap;
+      bn = std::max(16, rup((N + nnb - 1) / nnb, 16));
+      if (n_mblk * ((N + bn - 1) / bn) >= 96) break;
+    }
+    return bn;
+  }
+
   void choose_split(OpDesc& op, bool allow) {
     GemmArgs& g = op.g;
     const int nkb = g.K_pad / 64;
     const int tiles = g.n_mblk * g.n_nblk;
     int splits = 1;
     if (allow && tiles < 74 && nkb >= 8) splits = std::min(nkb / 4, std::max(1, 148 / tiles));
+    if (allow && g_tune[TUNE_SPLIT] > 0) splits = std::min(nkb, g_tune[TUNE_SPLIT]);
     splits = std::max(1, splits);
     g.kb_per_split = (nkb + splits - 1) / splits;
     g.splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;
@@ -389,6 +408,14 @@ class Builder {
   // conv + bias (+ residual) + act -> NHWC bf16; `out` may be a channel-offset view.
   Act conv(const Act& x, const std::string& name, int k, int stride, int pad, int act, const Act* resid = nullptr,
            const Act* out = nullptr, int col_off = 0) {
+    if (x.ref.kind == BUF_IN && x.C % 8 == 0 && !g_tune[TUNE_GATHER]) {
+      // the request input is not at a fixed address: stage it in the workspace
+      // (one copy step) so the conv reads it by TMA instead of a cp.async gather
+      const Act xs = stage_input(x);
+      const Act y = conv(xs, name, k, stride, pad, act, resid, out, col_off);
+      release_off(xs.ref.off);
+      return y;
+    }
     WRef w = conv_weight(dw, P, name, x.C, e);
     void* bias = raw_param(dw, P, name + ".b", e);
     const int Ho = (x.H + 2 * pad - k) / stride + 1, Wo = (x.W + 2 * pad - k) / stride + 1;
@@ -402,6 +429,17 @@ class Builder {
     ep.act = act;
     if (resid) ep.res = resid->ref;
     gemm_gather_a(conv_gather(x, k, stride, pad, Ho, Wo), x.N * Ho * Wo, w, bias, ep);
+    return y;
+  }
+
+  Act stage_input(const Act& x) {
+    Act y = tensor(x.N, x.H, x.W, x.C);
+    OpDesc& op = add(OP_COPY);
+    MiscArgs& a = op.m;
+    a.x = x.ref, a.y = y.ref;
+    a.rows = (int)((uint64_t)x.N * x.H * x.W * x.C * 2 / 16);   // 16-B vectors
+    op.n_units = 1;
+    step();
     return y;
   }
 
@@ -1095,8 +1133,13 @@ bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::str
       int lower[2] = {-x.pad, -x.pad};
       int upper[2] = {-x.pad + (x.Wo - 1) * x.stride - (x.W - 1), -x.pad + (x.Ho - 1) * x.stride - (x.H - 1)};
       cuuint32_t es[4] = {1, (cuuint32_t)x.stride, (cuuint32_t)x.stride, 1};
-      r = D.tensorMapEncodeIm2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, lower, upper, 64, 128,
-                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      const int cb = g.a_cb ? g.a_cb : 64;
+      const CUtensorMapSwizzle sw = cb == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                    : cb == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : cb == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+      r = D.tensorMapEncodeIm2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, lower, upper,
+                                  (cuuint32_t)cb, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) {
@@ -1151,6 +1194,9 @@ void op_cost(const OpDesc& op, double& flops, double& bytes) {
       break;
     case OP_SPLITK_FINAL:
       bytes = (4.0 * op.m.ep.splitk + 2) * op.m.rows * op.m.cols;
+      break;
+    case OP_COPY:
+      bytes = 32.0 * op.m.rows;
       break;
     default: break;
   }

@@ -21,7 +21,8 @@ enum OpType : int32_t {
   OP_LAYERNORM = 7,    // LayerNorm over rows (K10)
   OP_ATTENTION = 8,    // per (sequence, head) softmax(QK^T/8) V (K9)
   OP_SOFTMAX = 9,      // in-place fp32 row softmax (K11)
-  OP_SPLITK_FINAL = 10 // split-K reduction epilogue
+  OP_SPLITK_FINAL = 10, // split-K reduction epilogue
+  OP_COPY = 11         // 16-B vector copy (request input -> workspace, so TMA can read it)
 };
 
 enum BufKind : int32_t { BUF_NONE = 0, BUF_WS = 1, BUF_IN = 2, BUF_OUT = 3, BUF_ABS = 4 };
@@ -70,6 +71,8 @@ struct GemmArgs {
   int32_t n_mblk, n_nblk, splits, kb_per_split;
   int32_t a_tma, b_tma;         // operand source: SRC_GATHER / SRC_TMA / SRC_IM2COL
   int32_t act_tmap;             // 1: the activation operand's tensor map is bound per workspace
+  int32_t a_cb;                 // SRC_IM2COL channel box (64 / 32 / 16 / 8 channels per load; swizzle 128 / 64 / 32 / none)
+  int32_t pad0_;
   Gather ga, gb;                // gather geometry (used when *_tma == 0)
   Epilogue ep;
 };
@@ -155,15 +158,20 @@ struct ExecParams {
   int32_t* smid_log;            // optional: %smid per CTA (confinement audit)
   uint64_t* trace;              // optional: %globaltimer at program start and after every step
   int32_t trace_cap;
-  int32_t pad_;
+  int32_t dbg_flags;            // tuning experiments only (0 in production): 1 epilogue skips bias/act/stores,
+                                //   2 epilogue skips global stores, 4 MMA issues no UMMA, 8 producer issues no loads
+  int32_t tl_cap;               // optional per-CTA tile timeline of step 0 (tuning tool): tl[cta * tl_cap + 4 * i + k]
+  uint64_t* tl;                 //   k = 0 MMA start (accumulator acquired), 1 MMA last commit, 2 epilogue start, 3 epilogue end
 };
 
-constexpr int kThreads = 288;   // 4 producer warps, 4 epilogue warps, 1 MMA warp
-constexpr int kStages = 4;
+constexpr int kThreads = 320;   // warps 0-3 gather producers / epilogue, 4-7 epilogue, 8 MMA, 9 TMA producer
+constexpr int kStages = 4;      // fixed stage layout used as scratch by the non-GEMM ops
 constexpr int kStageBytesA = 128 * 128;       // 128 rows x 64 bf16
 constexpr int kStageBytesB = 256 * 128;       // up to 256 rows x 64 bf16
+constexpr int kRingBytes = kStages * (kStageBytesA + kStageBytesB);  // GEMM smem ring (192 KB)
+constexpr int kMaxStages = 8;   // GEMM ring depth: kRingBytes / (A + B stage bytes), at most 8
 constexpr int kEpiRowBytes = 80;                   // 32 bf16 + 16 B pad per staged row
-constexpr int kEpiStageBytes = 4 * 2 * 32 * kEpiRowBytes;  // per epilogue warp: 2 x (32 rows x 32 columns)
-constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 + kEpiStageBytes;  // + barriers
+constexpr int kEpiStageBytes = 8 * 32 * kEpiRowBytes;  // 8 epilogue warps x (32 rows x 32 columns)
+constexpr int kSmemBytes = kRingBytes + 1024 + kEpiStageBytes;  // + barriers
 
 }  // namespace gl

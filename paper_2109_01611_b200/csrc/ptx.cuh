@@ -36,6 +36,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
@@ -151,6 +154,19 @@ __device__ __forceinline__ uint64_t umma_sdesc_sw128(uint32_t smem_addr) {
   d |= (uint64_t)(1024 >> 4) << 32;  // SBO
   d |= (uint64_t)1 << 46;            // version
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// General K-major descriptor: layout 0 none / 2 SW128 / 4 SW64 / 6 SW32; sbo =
+// byte distance between 8-row core groups; lbo = byte distance between the two
+// 16-B K chunks of a K=16 step (used by the no-swizzle layout only).
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t smem_addr, uint32_t layout, uint32_t sbo, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 

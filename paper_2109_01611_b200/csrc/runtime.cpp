@@ -390,9 +390,18 @@ static gl_status launch_executor(gl_ctx* ctx, int dev, CUstream stream, int grid
   return cu_check(ctx, r, "cuLaunchKernelEx(gl_executor)");
 }
 
-// One-shot run of a program on the whole GPU (kernel unit tests).
+// One-shot run of a program on the whole GPU (kernel unit tests): optional
+// warm-up launches (gl_set_tuning key 3; 0 by default since some test ops run
+// in place), then a measured launch whose duration (program start -> last step
+// barrier, %globaltimer) and per-CTA tile timeline are kept for gl_test_stats.
+static std::vector<uint64_t> g_test_tl;
+static uint64_t g_test_ns = 0;
+static int g_test_tl_cap = 0;
+static const int kTestTlCap = 4 * 64;
+
 static gl_status run_oneshot(gl_ctx* ctx, int gpu, Program& prog, const void* in, void* out) {
   CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  const int nsm = ctx->gpus[gpu].nsm;
   char* ws = nullptr;
   CK(cudaMalloc(&ws, std::max<size_t>(prog.ws_bytes, 256)), "cudaMalloc(ws)");
   CK(cudaMemset(ws, 0, std::max<size_t>(prog.ws_bytes, 256)), "memset ws");
@@ -403,34 +412,64 @@ static gl_status run_oneshot(gl_ctx* ctx, int gpu, Program& prog, const void* in
   if (!dprog) return fail(GL_E_CUDA, berr);
   HostRing* ring = nullptr;
   CK(cudaHostAlloc((void**)&ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
-  std::memset((void*)ring, 0, sizeof(HostRing));
   HostRing* ring_dev = nullptr;
   CK(cudaHostGetDevicePointer((void**)&ring_dev, ring, 0), "cudaHostGetDevicePointer");
   ExecState* st = nullptr;
   CK(cudaMalloc(&st, sizeof(ExecState)), "cudaMalloc(st)");
-  CK(cudaMemset(st, 0, sizeof(ExecState)), "memset st");
-  WorkDesc& w = ring->items[0];
-  w.ticket = 1;
-  w.prog = dprog;
-  w.in = in;
-  w.out = out;
-  w.n_ops = (int)prog.ops.size();
-  w.batch = 1;
-  ring->tail = 1;
-  ExecParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.ring = ring_dev;
-  p.st = st;
-  p.ws = ws;
-  p.one_shot = 1;
+  uint64_t* tr = nullptr;
+  CK(cudaMalloc(&tr, 1024 * sizeof(uint64_t)), "cudaMalloc(trace)");
+  uint64_t* tl = nullptr;
+  const size_t tl_n = (size_t)nsm * kTestTlCap;
+  CK(cudaMalloc(&tl, tl_n * sizeof(uint64_t)), "cudaMalloc(timeline)");
   cudaStream_t s;
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  gl_status rc = launch_executor(ctx, ctx->gpus[gpu].dev, (CUstream)s, ctx->gpus[gpu].nsm, p);
+  gl_status rc = GL_OK;
+  const int runs = 1 + std::max(0, std::min(g_tune[TUNE_WARM], 8));   // warm-up runs first (tuning tool)
+  for (int rep = 0; rep < runs && rc == GL_OK; ++rep) {
+    std::memset((void*)ring, 0, sizeof(HostRing));
+    CK(cudaMemset(st, 0, sizeof(ExecState)), "memset st");
+    CK(cudaMemset(tr, 0, 1024 * sizeof(uint64_t)), "memset trace");
+    CK(cudaMemset(tl, 0, tl_n * sizeof(uint64_t)), "memset timeline");
+    WorkDesc& w = ring->items[0];
+    w.ticket = 1;
+    w.prog = dprog;
+    w.in = in;
+    w.out = out;
+    w.n_ops = (int)prog.ops.size();
+    w.batch = 1;
+    ring->tail = 1;
+    ExecParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.ring = ring_dev;
+    p.st = st;
+    p.ws = ws;
+    p.one_shot = 1;
+    p.trace = tr;
+    p.trace_cap = 1024;
+    p.tl = tl;
+    p.tl_cap = kTestTlCap;
+    p.dbg_flags = g_tune[TUNE_MISC];
+    rc = launch_executor(ctx, ctx->gpus[gpu].dev, (CUstream)s, nsm, p);
+    if (rc == GL_OK) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_check(ctx, e, "executor (one-shot)");
+    }
+  }
   if (rc == GL_OK) {
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) rc = cuda_check(ctx, e, "executor (one-shot)");
+    int steps = 0;
+    for (auto& op : prog.ops) steps += op.step_end ? 1 : 0;
+    std::vector<uint64_t> h(1024);
+    cudaMemcpy(h.data(), tr, 1024 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    g_test_ns = h[std::min(steps, 1023)] - h[0];
+    g_test_tl.assign(tl_n, 0);
+    cudaMemcpy(g_test_tl.data(), tl, tl_n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    for (auto& v : g_test_tl)
+      if (v) v -= h[0];
+    g_test_tl_cap = kTestTlCap;
   }
   cudaStreamDestroy(s);
+  release_device(tl, false);
+  release_device(tr, false);
   release_device(st, false);
   release_device(ring, true);
   release_device(ws, false);
@@ -905,6 +944,20 @@ gl_status gl_test_conv(gl_ctx* ctx, int gpu, const void* x, const uint16_t* W, c
   if (!build_test_conv(N, H, Wd, C, Cout, KH, stride, pad, act, W, bias, x_in_ws, dw, prog, err))
     return fail(GL_E_ARG, err);
   return run_oneshot(ctx, gpu, prog, x, y);
+}
+
+gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* tl_per_cta) {
+  if (ns) *ns = g_test_ns;
+  if (tl_per_cta) *tl_per_cta = g_test_tl_cap;
+  if (timeline)
+    for (int i = 0; i < cap && i < (int)g_test_tl.size(); ++i) timeline[i] = g_test_tl[i];
+  return GL_OK;
+}
+
+gl_status gl_set_tuning(int32_t key, int32_t value) {
+  if (key < 0 || key >= kTuneKeys) return fail(GL_E_ARG, "gl_set_tuning: bad key");
+  g_tune[key] = value;
+  return GL_OK;
 }
 
 gl_status gl_test_misc(gl_ctx* ctx, int gpu, int32_t type, const int32_t* ia, int32_t n, const uint16_t* params,

@@ -74,6 +74,10 @@ struct Model {
   size_t in_bytes[33] = {0}, out_bytes[33] = {0};
 };
 
+// Program-builder tuning overrides (gl_set_tuning; 0 = automatic choice).
+enum TuneKey { TUNE_BN = 0, TUNE_SPLIT = 1, TUNE_MISC = 2, TUNE_WARM = 3, TUNE_GATHER = 4, kTuneKeys = 8 };
+extern int g_tune[kTuneKeys];
+
 // Build the layer program of model `kind` at batch b (models.cpp).
 bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
                    size_t& in_bytes, size_t& out_bytes, std::string& err);

@@ -21,7 +21,8 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3}
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
-           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc"]
+           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
+           "gl_test_stats", "gl_set_tuning"]
 
 
 class GpuletError(RuntimeError):
@@ -87,6 +88,8 @@ def lib():
             "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32],
             "gl_test_conv": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32],
             "gl_test_misc": [P, ctypes.c_int, I32, ctypes.POINTER(I32), I32, P, I64, P, P],
+            "gl_test_stats": [ctypes.POINTER(U64), ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
+            "gl_set_tuning": [I32, I32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -260,6 +263,21 @@ class Context:
     def test_conv(self, gpu, x, W_bits, b_bits, y, N, H, W, C, Cout, KH, stride, pad, act=1, in_ws=0):
         _check(lib().gl_test_conv(self.h, gpu, _ptr(x), _ptr(W_bits), _ptr(b_bits), _ptr(y), N, H, W, C, Cout, KH,
                                   stride, pad, act, in_ws))
+
+    @staticmethod
+    def test_stats(n_cta=148):
+        """(device ns of the last test run, timeline[n_cta][tiles][4] ns or 0)."""
+        import numpy as np
+        ns = ctypes.c_uint64()
+        per = ctypes.c_int32()
+        _check(lib().gl_test_stats(ctypes.byref(ns), None, 0, ctypes.byref(per)))
+        tl = np.zeros(n_cta * per.value, dtype=np.uint64)
+        _check(lib().gl_test_stats(None, tl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), tl.size, None))
+        return ns.value, tl.reshape(n_cta, per.value // 4, 4)
+
+    @staticmethod
+    def set_tuning(key, value):
+        _check(lib().gl_set_tuning(int(key), int(value)))
 
     def test_misc(self, gpu, op, iargs, params, x, y):
         ia = (ctypes.c_int32 * len(iargs))(*iargs)

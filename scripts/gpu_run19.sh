@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gputests19.log 2>&1; echo "rc=$?" >> gpurun_out/gputests19.log
+timeout 600 python tools/gemm_micro.py --json gpurun_out/micro19.json > gpurun_out/micro19.log 2>&1
+for mb in resnet50:32 vgg16:32 bert_base:32 googlenet:32 ssd_mobilenet_v1:32 resnet50:1 lenet5:32; do m=${mb%:*}; b=${mb#*:}
+  timeout 120 python tools/oneshot.py --model $m --batch $b --json gpurun_out/trace19_${m}_b${b}.json >> gpurun_out/oneshot19.log 2>&1
+done

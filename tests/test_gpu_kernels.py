@@ -67,22 +67,29 @@ def test_gemm_swap_ab_splitk_vs_oracle(ctx, M, N, K, in_ws):
 CONV_CASES = [(2, 14, 14, 64, 128, 3, 1, 1), (1, 30, 30, 8, 64, 7, 2, 3), (2, 9, 9, 32, 24, 3, 2, 1),
               (3, 15, 15, 256, 512, 1, 2, 0), (1, 12, 12, 16, 48, 5, 1, 2), (2, 19, 19, 512, 126, 3, 1, 1),
               (1, 56, 56, 64, 64, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1), (2, 10, 10, 256, 512, 3, 2, 1),
-              (3, 7, 7, 512, 256, 1, 1, 0), (2, 5, 5, 128, 64, 5, 1, 2)]
+              (3, 7, 7, 512, 256, 1, 1, 0), (2, 5, 5, 128, 64, 5, 1, 2), (2, 14, 14, 96, 128, 3, 1, 1),
+              (1, 14, 14, 24, 64, 5, 1, 2), (2, 7, 7, 160, 320, 3, 1, 1), (2, 28, 28, 48, 128, 5, 1, 2),
+              (4, 32, 32, 8, 64, 3, 1, 1)]
 
 
 @pytest.mark.parametrize("in_ws", [0, 1])
 @pytest.mark.parametrize("N,H,W,C,Co,k,s,p", CONV_CASES)
 def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p, in_ws):
-    """in_ws=0: cp.async implicit-im2col gather; in_ws=1: TMA (2-D for 1x1/s1,
-    im2col mode for KxK / strided convs with C % 64 == 0, gather otherwise)."""
+    """in_ws=0: cp.async implicit-im2col gather (forced by tuning key 4);
+    in_ws=1: TMA (2-D for 1x1/s1, im2col boxes of 64/32/16/8 channels otherwise)."""
     import torch
+    from paper_2109_01611_b200 import gpulet
     r = np.random.default_rng(H * C + Co)
     x = _bf16(r, (N, H, W, C))
     w = _bf16(r, (Co, k, k, C), np.sqrt(2 / (k * k * C)))
     b = _bf16(r, (Co,), 0.05)
     Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
     y = torch.empty((N, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
-    ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1, in_ws=in_ws)
+    gpulet.Context.set_tuning(4, 1 - in_ws)
+    try:
+        ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1, in_ws=in_ws)
+    finally:
+        gpulet.Context.set_tuning(4, 0)
     torch.cuda.synchronize()
     ref = nn.rbf16(nn.relu(nn.conv2d(bits_to_f64(x), bits_to_f64(w), bits_to_f64(b), s, p)))
     got = bits_to_f64(from_dev_bf16(y))
