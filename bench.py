@@ -1,36 +1,39 @@
 #!/usr/bin/env python
-"""bench.py — SLO-satisfying req/s of mixed-model serving on gpu-lets (B200).
+"""bench.py — maximum SLO-satisfying req/s of mixed-model serving on gpu-lets (B200).
 
 Workload (BASELINE.json configs[3], the metric's 1-GPU configuration).  The
-config text names the paper's `game` scenario but lists six models; SURVEY D2
+config text names the paper's `game` scenario and lists six models; SURVEY D2
 keeps both readings, so one run measures both:
-  * headline `game`: app request = 6 LeNet-5 + 1 ResNet-50 (the paper's
-    definition of game), on gpu-lets planned by the native scheduler;
-  * `mix6`: the six models (LeNet-5, GoogLeNet, ResNet-50, SSD-MobileNet-V1,
-    VGG-16, BERT-base) at equal rates (Table tab:particular-scenarios P:800-806
-    extended with BERT), reported under "mix6";
-  * the whole-GPU temporal-sharing baseline (SBP) built from the same
-    kernels, on the same scenario, reported under "baseline_sbp".
-SLOs follow the paper's rule SLO = 2 x solo latency at batch 32
-applied to the measured B200 profile (profiles/profile_b200.csv); rates are the
-paper's rates scaled to B200 (C4.3) times the largest multiplier for which the
-scheduler (Alg. 1, gpulet+int by default) returns Schedulable.  The plan's
-gpu-lets are created (green contexts + persistent executors) and every step
-replays one duty-cycle round: each lane submits one batch of its planned batch
-size, gpu-lets run concurrently, lanes on a gpu-let run FIFO.  A request counts
-as SLO-satisfying when D (its lane's batch-building window) + (its batch's
-completion - round start, device %globaltimer) <= its model's SLO.
+  * headline `game`: an app request = 6 LeNet-5 + 1 ResNet-50 requests;
+  * `mix6`: LeNet-5, GoogLeNet, ResNet-50, SSD-MobileNet-V1, VGG-16, BERT-base at
+    equal rates (Table tab:particular-scenarios P:800-806 extended with BERT);
+  * the whole-GPU temporal-sharing baseline (SBP) and gpulet without
+    the interference model, on the same kernels.
+SLOs follow the paper's rule SLO = 2 x solo latency at batch 32 on
+the measured B200 profile (profiles/profile_b200.csv); scenario rates are the
+paper's, scaled to B200, times a multiplier x.
 
-  value    = SLO-satisfying requests of the K timed rounds / device time of the
-             K rounds (first dequeue -> last completion), summed over ranks /
-             max over ranks
-  e2e      = the same through the public API with pinned host inputs copied
-             H2D and outputs copied D2H inside every step (host wall clock)
-  roofline = the dominant lane's program at its batch, one executor launch on
-             the whole GPU, FLOPs / launch time vs the measured bf16 peak
-Multi-GPU: one process per GPU (torchrun); each GPU serves its own copy of the
-1-GPU plan (requests are independent: no collective on the data path), weak
-scaling.  --impl reference times the CPU oracle (oracle/) on a bounded sample.
+Method ("maximum achievable throughput"): x starts at the largest
+multiplier the native scheduler (Alg. 1, mode gpulet+int) accepts for N GPUs;
+the plan's gpu-lets are created (green contexts + persistent executors) and
+Poisson traffic is replayed in real time through the native frontend
+(gl_serve: smooth-WRR routing, duty-cycle batching, drops); x is bisected
+down until violations (late + dropped) are <= 1 % of arrivals.
+
+A step = one serving window of --window seconds of Poisson arrivals at that x.
+  value    = SLO-satisfying requests of the K timed windows, summed over ranks /
+             device time of those windows (first dequeue -> last completion,
+             %globaltimer), max over ranks
+  e2e      = the same windows with every batch's inputs copied H2D from pinned
+             host memory before submit and outputs copied D2H on completion
+  roofline = the dominant lane's model program at its planned batch, one
+             executor launch on the whole GPU (device %globaltimer), algorithmic
+             FLOPs (or bytes) / launch time vs MEASURED_PEAKS.json
+Multi-GPU: one process per GPU (torchrun); the scheduler places gpu-lets on N
+GPUs; rank r serves the gpu-lets of GPU r with its own Poisson streams (the
+per-model arrival process split by the lanes' rates).  Requests are
+independent: no collective on the data path; the control path (rate search,
+final sums) uses torch.distributed.  --impl reference times the CPU oracle.
 """
 import argparse
 import json
@@ -120,6 +123,27 @@ def init_dist(world, backend):
     return None
 
 
+def allsum(dist, vals):
+    """Control-path reduction (sum) over ranks."""
+    if dist is None:
+        return list(vals)
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def allmax(dist, vals):
+    if dist is None:
+        return list(vals)
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 # ----------------------------------------------------------------------------- oracle arm
 def reference_arm(a, world, rank):
     """The CPU oracle (fp64 numpy forward) as it stands, one request per step,
@@ -164,203 +188,284 @@ def cpu_baseline_sample():
 
 
 # ----------------------------------------------------------------------------- our arm
-def plan_for(lat_env, l2, mem, slo, coeffs, mode, scenario):
-    """Largest rate multiplier (bisection, 0.5 %) the native scheduler accepts."""
-    from paper_2109_01611_b200 import gpulet
+def poisson_trace(rates, secs, seed, lead_us=20_000):
+    """Merged Poisson arrivals (PCG64 inverse-CDF exponentials) of all models."""
+    import numpy as np
+    ts, ms = [], []
+    for m, r in enumerate(rates):
+        if r <= 0:
+            continue
+        rng = np.random.Generator(np.random.PCG64(seed * 131 + m))
+        n = int(r * secs * 1.3) + 20
+        t = np.cumsum(-np.log(1.0 - rng.random(n)) / r * 1e6)
+        t = t[t < secs * 1e6]
+        ts.append(t.astype(np.int64))
+        ms.append(np.full(len(t), m, np.int32))
+    if not ts:
+        return np.zeros(0, np.int64), np.zeros(0, np.int32)
+    t = np.concatenate(ts)
+    m = np.concatenate(ms)
+    o = np.argsort(t, kind="stable")
+    return t[o] + lead_us, m[o]
+
+
+class Server:
+    """One rank's serving state: loaded models, per-(model, slot) device and
+    pinned host buffers (all allocated before any executor runs), and the live
+    gpu-lets of the current plan."""
+
+    HOST_SLOTS = 64
+
+    def __init__(self, ctx, gpu, prof, e2e):
+        import torch
+        from tools import common
+        self.ctx, self.gpu = ctx, gpu
+        self.lat, self.l2, self.mem, self.slo, self.coeffs = prof
+        self.mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
+        self.x, self.y, self.xh, self.yh, self.req_bytes = {}, {}, {}, {}, {}
+        for m in common.MODELS:
+            inb, outb = ctx.model_io(self.mids[m], 32)
+            self.req_bytes[m] = (inb // 32, outb // 32)
+            for slot in (0, 1):
+                self.x[m, slot] = common.device_input(m, 32)
+                self.y[m, slot] = torch.empty(outb // 4, device="cuda")
+            if e2e:
+                h = common.host_input(m, 32)
+                reps = [h] * (self.HOST_SLOTS // 32)
+                self.xh[m] = torch.cat(reps).pin_memory()
+                self.yh[m] = torch.empty(self.HOST_SLOTS * (outb // 32) // 4, dtype=torch.float32).pin_memory()
+        torch.cuda.current_stream().synchronize()
+        self.made, self.lanes = [], []
+
+    def plan(self, scen, mode, n_gpus, x):
+        from paper_2109_01611_b200 import gpulet
+        from tools import common
+        rates = [r * n_gpus for r in common.scenario_rates(scen, self.slo, x)]
+        dump, ok = gpulet.schedule(common.MODELS, self.lat, self.l2, self.mem, self.slo, rates, n_gpus, mode,
+                                   self.coeffs)
+        return rates, dump, ok
+
+    def max_sched_x(self, scen, mode, n_gpus):
+        lo, hi = 0.0, 0.25
+        while self.plan(scen, mode, n_gpus, hi)[2] and hi < 1e6:
+            lo, hi = hi, hi * 2
+        for _ in range(40):
+            mid = (lo + hi) / 2
+            lo, hi = (mid, hi) if self.plan(scen, mode, n_gpus, mid)[2] else (lo, mid)
+            if hi - lo < 0.002 * max(lo, 1e-9):
+                break
+        return lo
+
+    def setup(self, dump, rank):
+        """Create this GPU's gpu-lets of the plan and build its lanes; returns
+        the per-model arrival rates this rank must serve."""
+        from tools import common
+        self.teardown()
+        gls, _ = common.parse_plan(dump)
+        used = [g for g in sorted(gls, key=lambda d: d["slot"]) if g["lanes"] and g["gpu"] == rank]
+        my_rates = [0] * len(common.MODELS)
+        if not used:
+            return my_rates
+        made = self.ctx.create_gpulets(self.gpu, [g["size"] for g in used])
+        self.made = [gid for gid, _n in made]
+        for g, (gid, nsm) in zip(used, made):
+            for ln in g["lanes"]:
+                m = ln["model"]
+                mi = common.MODELS.index(m)
+                drop = (self.lat[mi][0][common.GRID.index(g["size"])] * ln["F"] + 999) // 1000
+                ib, ob = self.req_bytes[m]
+                self.lanes.append(dict(gpulet=gid, model_id=self.mids[m], model_slot=mi, batch=ln["batch"],
+                                       duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.x[m, g["slot"]],
+                                       y=self.y[m, g["slot"]], x_host=self.xh.get(m), y_host=self.yh.get(m),
+                                       in_req_bytes=ib, out_req_bytes=ob, host_slots=self.HOST_SLOTS,
+                                       size=g["size"], sm=nsm, model=m))
+                my_rates[mi] += ln["rate"]
+        return my_rates
+
+    def teardown(self):
+        for gid in self.made:
+            self.ctx.destroy_gpulet(gid)
+        self.made, self.lanes = [], []
+
+    def window(self, rates, secs, seed, e2e=False):
+        """One serving window of Poisson traffic at `rates` through gl_serve."""
+        import numpy as np
+        from tools import common
+        t, m = poisson_trace(rates, secs, seed)
+        if len(t) == 0 or not self.lanes:
+            return dict(arrivals=0, sat=0, viol=0, dev_s=0.0, wall_s=0.0, h2d=0, d2h=0, per={})
+        lanes = self.lanes if e2e else [{k: v for k, v in ln.items() if k not in ("x_host", "y_host")}
+                                         for ln in self.lanes]
+        w0 = time.perf_counter()
+        lat, st = self.ctx.serve(lanes, len(common.MODELS), t, m, self.slo, stats=True)
+        wall = time.perf_counter() - w0
+        slo = np.asarray(self.slo)[m]
+        viol = (lat < 0) | (lat > slo)
+        per = {}
+        for mi, name in enumerate(common.MODELS):
+            sel = m == mi
+            if sel.any():
+                ok_l = lat[sel & (lat >= 0)]
+                per[name] = {"arrivals": int(sel.sum()), "viol": int(viol[sel].sum()),
+                             "p99_us": float(np.percentile(ok_l, 99)) if len(ok_l) else None,
+                             "slo_us": int(self.slo[mi])}
+        d0, d1 = st["dev_ns"]
+        return dict(arrivals=int(len(lat)), sat=int((~viol).sum()), viol=int(viol.sum()),
+                    dev_s=max(d1 - d0, 0) * 1e-9, wall_s=wall, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], per=per)
+
+
+def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
+    """Rate search + timed windows for one (scenario, mode).  Returns a dict."""
     from tools import common
-    lo, hi = 0.0, 1.0
-    while True:
-        _d, ok = gpulet.schedule(common.MODELS, lat_env, l2, mem, slo, common.scenario_rates(scenario, slo, hi), 1,
-                                 mode, coeffs)
-        if not ok or hi > 1e6:
+    xs = srv.max_sched_x(scen, mode, world)
+    if sum(srv.plan(scen, mode, world, xs)[0]) == 0:
+        # no positive rate vector of this scenario is schedulable on `world` GPU(s)
+        return {"value": 0.0, "x_sched": xs, "x": 0.0, "probes": [], "rates": [0] * len(common.MODELS),
+                "note": f"not schedulable on {world} GPU(s) at any positive rate"}
+    lo, hi, best = 0.0, xs, None
+    x = xs
+    probes = []
+    for it in range(a.probes + 1):
+        rates, dump, ok = srv.plan(scen, mode, world, x)
+        w = None
+        if ok and sum(rates) > 0:
+            my = srv.setup(dump, rank)
+            w = srv.window(my, a.probe_window, 1000 + it)
+            srv.teardown()
+            arr, viol = allsum(dist, [w["arrivals"], w["viol"]])
+        else:
+            arr, viol = 0, 1
+        frac = viol / arr if arr else 1.0
+        probes.append({"x": round(x, 4), "viol_frac": round(frac, 4),
+                       "viol_by_model": {k: v["viol"] for k, v in (w["per"] if w else {}).items() if v["viol"]}})
+        log(f"[{scen}/{mode}] probe x={x:.4f} viol={frac:.4f}")
+        if arr and frac <= 0.01:
+            lo, best = x, x
+            if it == 0:
+                break
+        else:
+            hi = x
+        x = (lo + hi) / 2
+        if best is not None and hi - lo < 0.02 * hi:
             break
-        lo, hi = hi, hi * 2
-    for _ in range(40):
-        mid = (lo + hi) / 2
-        _d, ok = gpulet.schedule(common.MODELS, lat_env, l2, mem, slo, common.scenario_rates(scenario, slo, mid), 1,
-                                 mode, coeffs)
-        lo, hi = (mid, hi) if ok else (lo, mid)
-        if hi - lo < 0.005 * max(lo, 1e-9):
-            break
-    rates = common.scenario_rates(scenario, slo, lo)
-    dump, ok = gpulet.schedule(common.MODELS, lat_env, l2, mem, slo, rates, 1, mode, coeffs)
-    return lo, rates, dump, ok
-
-
-def run_scenario(ctx, gpu, mids, prof, scenario, mode, steps, warmup, e2e_leg, dist=None, clocks=False):
-    import torch
-    from tools import common
-    lat_env, l2, mem, slo, coeffs = prof
-    x, rates, dump, ok = plan_for(lat_env, l2, mem, slo, coeffs, mode, scenario)
-    gls, _verdict = common.parse_plan(dump)
-    log(f"[{scenario}/{mode}] x={x:.4f} rates={rates}\n{dump}")
-    # every device buffer exists before any executor starts (a device allocation
-    # can synchronise the device and would wait behind a persistent kernel)
-    lanes, made = [], {}
-    used = [g for g in sorted(gls, key=lambda d: d["slot"]) if g["lanes"]]
-    for g in used:
-        for ln in g["lanes"]:
-            m = ln["model"]
-            mi = common.MODELS.index(m)
-            lanes.append(dict(gid=None, slot=g["slot"], model=m, mid=mids[m], batch=ln["batch"], D=g["D_us"],
-                              x=common.device_input(m, ln["batch"]),
-                              y=torch.empty(ctx.model_io(mids[m], ln["batch"])[1] // 4, device="cuda"), slo=slo[mi]))
-    hx = [common.host_input(ln["model"], ln["batch"]) for ln in lanes] if e2e_leg else []
-    hy = [torch.empty(ln["y"].numel(), dtype=torch.float32).pin_memory() for ln in lanes] if e2e_leg else []
-    cs = torch.cuda.Stream()
-    torch.cuda.current_stream().synchronize()
-    if not lanes:
-        return {"value": 0.0, "rate_multiplier": x, "rates": rates, "plan": dump, "lanes": []}
-    for g, (gid, nsm) in zip(used, ctx.create_gpulets(gpu, [g["size"] for g in used])):
-        made[gid] = (g["size"], nsm)
-        for ln in lanes:
-            if ln["slot"] == g["slot"]:
-                ln["gid"] = gid
-
-    def round_once(collect):
-        tickets = {ctx.submit_batch(ln["gid"], ln["mid"], ln["x"], ln["y"], ln["batch"], ln["slo"] / 1000.0): i
-                   for i, ln in enumerate(lanes)}
-        recs = []
-        while len(recs) < len(lanes):
-            recs += ctx.poll()
-        if collect is not None:
-            collect.append([(tickets[r.ticket], r.t_dequeue_ns, r.t_start_ns, r.t_end_ns) for r in recs])
-
+    if best is None:
+        return {"value": 0.0, "x_sched": xs, "x": 0.0, "probes": probes, "rates": [0] * len(common.MODELS)}
+    rates, dump, ok = srv.plan(scen, mode, world, best)
+    my = srv.setup(dump, rank)
+    res = {"x_sched": xs, "x": best, "probes": probes, "rates": rates, "plan": dump,
+           "lanes": [{k: ln[k] for k in ("model", "batch", "duty_us", "size", "sm", "weight", "gpulet")}
+                     for ln in srv.lanes]}
     try:
-        for _ in range(warmup):
-            round_once(None)
-        rounds = []
+        for s in range(a.warmup):
+            srv.window(my, a.window, 2000 + s)
         if dist:
             dist.barrier()
-        torch.cuda.current_stream().synchronize()
-        clk = ClockSampler(gpu) if clocks else None
+        clk = ClockSampler(srv.gpu) if clocks else None
         if clk:
             clk.__enter__()
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            round_once(rounds)
-        wall = time.perf_counter() - t0
+        wins = [srv.window(my, a.window, 3000 + s) for s in range(a.steps if timed else 1)]
         if clk:
             clk.__exit__()
-        t_first = min(min(r[1] for r in rd) for rd in rounds)
-        t_last = max(max(r[3] for r in rd) for rd in rounds)
-        dev_s = (t_last - t_first) * 1e-9
-        sat = tot = 0
-        busy = {gid: 0 for gid in made}
-        flops_g = {gid: 0.0 for gid in made}
-        lane_time = [0] * len(lanes)
-        for rd in rounds:
-            start = min(r[1] for r in rd)
-            for i, _tdq, ts, te in rd:
-                ln = lanes[i]
-                tot += ln["batch"]
-                if ln["D"] + (te - start) / 1000.0 <= ln["slo"]:
-                    sat += ln["batch"]
-                busy[ln["gid"]] += te - ts
-                flops_g[ln["gid"]] += ctx.model_cost(ln["mid"], ln["batch"])[0]
-                lane_time[i] += te - ts
-        e2e = None
-        if e2e_leg:
-            h2d = sum(t.numel() * t.element_size() for t in hx)
-            d2h = sum(t.numel() * 4 for t in hy)
-            e_sat = e_tot = 0
-            t0 = time.perf_counter()
-            for _ in range(steps):
-                ts = time.perf_counter()
-                with torch.cuda.stream(cs):
-                    for ln, h in zip(lanes, hx):
-                        ln["x"].copy_(h.view(ln["x"].dtype).view(ln["x"].shape), non_blocking=True)
-                cs.synchronize()
-                tickets = {ctx.submit_batch(ln["gid"], ln["mid"], ln["x"], ln["y"], ln["batch"]): i
-                           for i, ln in enumerate(lanes)}
-                done = 0
-                while done < len(lanes):
-                    for r in ctx.poll():
-                        i = tickets[r.ticket]
-                        with torch.cuda.stream(cs):
-                            hy[i].copy_(lanes[i]["y"], non_blocking=True)
-                        done += 1
-                cs.synchronize()
-                el_us = (time.perf_counter() - ts) * 1e6
-                for ln in lanes:
-                    e_tot += ln["batch"]
-                    e_sat += ln["batch"] if ln["D"] + el_us <= ln["slo"] else 0
-            e_wall = time.perf_counter() - t0
-            e2e = {"value": round(e_sat / e_wall, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": int(d2h), "all_req_per_s": round(e_tot / e_wall, 2)}
+            res["clocks"] = clk.summary()
+        sat, arr, viol = allsum(dist, [sum(w["sat"] for w in wins), sum(w["arrivals"] for w in wins),
+                                       sum(w["viol"] for w in wins)])
+        dev_s, wall_s = allmax(dist, [sum(w["dev_s"] for w in wins), sum(w["wall_s"] for w in wins)])
+        res.update(value=sat / dev_s if dev_s else 0.0, sat=sat, arrivals=arr, viol_frac=viol / max(arr, 1),
+                   dev_s=dev_s, wall_s=wall_s, windows=len(wins),
+                   per_model={k: v for w in wins[-1:] for k, v in w["per"].items()})
+        if a.e2e and timed:
+            ew = [srv.window(my, a.window, 4000 + s, e2e=True) for s in range(a.steps)]
+            esat, earr, eh, ed = allsum(dist, [sum(w["sat"] for w in ew), sum(w["arrivals"] for w in ew),
+                                               sum(w["h2d"] for w in ew), sum(w["d2h"] for w in ew)])
+            ewall, = allmax(dist, [sum(w["wall_s"] for w in ew)])
+            res["e2e"] = {"value": round(esat / ewall, 2) if ewall else 0.0, "unit": UNIT,
+                          "h2d_bytes_per_step": int(eh / len(ew)), "d2h_bytes_per_step": int(ed / len(ew)),
+                          "slo_satisfied_frac": round(esat / max(earr, 1), 4),
+                          "timing": "host wall clock of the windows, H2D/D2H of every batch inside"}
     finally:
-        for gid in list(made):
-            ctx.destroy_gpulet(gid)
-    dom = max(range(len(lanes)), key=lambda i: lane_time[i])
-    return {"value": sat / dev_s, "sat": sat, "tot": tot, "dev_s": dev_s, "wall": wall, "rate_multiplier": x,
-            "rates": rates, "plan": dump, "e2e": e2e, "clocks": clk.summary() if clk else None,
-            "gpulets": [{"size": made[g][0], "sm": made[g][1]} for g in made],
-            "lanes": [{"model": ln["model"], "batch": ln["batch"], "D_us": ln["D"]} for ln in lanes],
-            "gpulet_tensor_frac": {str(g): round(flops_g[g] / max(busy[g] * 1e-9, 1e-12) / 1e12 /
-                                                 (_peaks()[1] * made[g][1] / 148), 4) for g in made},
-            "dominant": lanes[dom]}
+        srv.teardown()
+    return res
+
+
+def roofline(ctx, srv, lanes):
+    """Dominant lane (most planned device time: rate / batch x L) -> its model
+    program at its batch, one executor launch on the whole GPU."""
+    from tools import common
+    hbm, peak_burst, _sus, src = _peaks()
+    if not lanes:
+        return None
+    def load(ln):
+        mi = common.MODELS.index(ln["model"])
+        return ln["weight"] / ln["batch"] * srv.lat[mi][ln["batch"] - 1][5]
+    ln = max(lanes, key=load)
+    m, b = ln["model"], ln["batch"]
+    mid = srv.mids[m]
+    durs = [sum(ctx.run_once(mid, b, srv.x[m, 0], srv.y[m, 0], 0, True)) for _ in range(4)][1:]
+    info = ctx.program_info(mid, b)
+    fl, by = sum(s[2] for s in info), sum(s[3] for s in info)
+    t = statistics.median(durs) * 1e-9
+    tensor = fl / max(by, 1) > peak_burst * 1e12 / (hbm * 1e9)
+    ach = fl / t / 1e12 if tensor else by / t / 1e9
+    peak = peak_burst if tensor else hbm
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", f"ncu_{m}_b{b}.json")
+    if os.path.exists(ncu_path):
+        with open(ncu_path) as f:
+            traffic = json.load(f).get("dram_bytes")
+    return {"bound": "tensor" if tensor else "hbm", "achieved": round(ach, 2), "peak": peak,
+            "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
+            "kernel": f"gl_executor, one launch of the {m} b={b} program on 148 SMs", "launch_us": round(t * 1e6, 1),
+            "algorithmic_flop": fl, "algorithmic_bytes": by,
+            "peak_source": f"{src} (MEASURED_PEAKS.json, burst: kernel timed alone)"}
 
 
 def our_arm(a, world, rank, local, dist):
     import torch
     from paper_2109_01611_b200 import gpulet
     from tools import common
-    from tools.dist_agg import aggregate
 
     torch.cuda.set_device(local)
-    hbm, peak_burst, _peak_sus, peak_src = _peaks()
     ctx = gpulet.Context(local + 1)
-    gpu = local
-    mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
     if not os.path.exists(common.PROFILE_CSV):
         raise SystemExit(f"missing {common.PROFILE_CSV}: run tools/profile_sweep.py on the GPU first")
     lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
     lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
     slo = common.slos_from(lat_env)
     prof = (lat_env, l2, mem, slo, common.load_coeffs())
-    head = run_scenario(ctx, gpu, mids, prof, a.scenario, a.mode, a.steps, a.warmup, not a.no_e2e, dist, clocks=True)
+    srv = Server(ctx, local, prof, a.e2e)
+    head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, timed=True, clocks=True)
     extra = {}
     if not a.headline_only:
-        for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), ("mix6", "mix6", a.mode),
-                                ("mix6_baseline_sbp", "mix6", "sbp")):
-            r = run_scenario(ctx, gpu, mids, prof, scen, mode, a.steps, a.warmup, False)
+        for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), ("gpulet_no_int", a.scenario, "gpulet"),
+                                ("mix6", "mix6", a.mode), ("mix6_baseline_sbp", "mix6", "sbp")):
+            r = run_mode(srv, dist, rank, world, scen, mode, a, timed=False)
             extra[key] = {"value": round(r["value"], 2), "scenario": scen, "mode": mode,
-                          "rate_multiplier": round(r["rate_multiplier"], 4), "rates_req_s": r["rates"],
-                          "lanes": r["lanes"]}
-    # roofline: the dominant lane's program, one executor launch on the whole GPU
-    ln = head["dominant"]
-    durs = [sum(ctx.run_once(ln["mid"], ln["batch"], ln["x"], ln["y"], 0, True)) for _ in range(3)]
-    info = ctx.program_info(ln["mid"], ln["batch"])
-    fl, by = sum(s[2] for s in info), sum(s[3] for s in info)
-    t = statistics.median(durs) * 1e-9
-    tensor = fl / max(by, 1) > peak_burst * 1e12 / (hbm * 1e9)
-    ach = fl / t / 1e12 if tensor else by / t / 1e9
-    peak = peak_burst if tensor else hbm
-    roof = {"bound": "tensor" if tensor else "hbm", "achieved": round(ach, 2), "peak": peak,
-            "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(ach / peak, 4), "traffic": None,
-            "kernel": f"gl_executor, one launch: {ln['model']} b={ln['batch']} on 148 SMs",
-            "launch_us": round(t * 1e6, 1), "algorithmic_flop": fl, "algorithmic_bytes": by,
-            "peak_source": f"{peak_src} (MEASURED_PEAKS.json, burst)"}
-    sat, tot, dev, wall = aggregate(dist, head["sat"], head["tot"], head["dev_s"], head["wall"])
+                          "rate_multiplier": round(r["x"], 4), "x_sched": round(r["x_sched"], 4),
+                          "rates_req_s": r["rates"], "viol_frac": round(r.get("viol_frac", 1.0), 4),
+                          "lanes": r.get("lanes", []), "note": r.get("note")}
+    roof = roofline(ctx, srv, head.get("lanes", [])) if rank == 0 else None
     if rank != 0:
         ctx.close()
         return None
+    rates = head["rates"]
+    app = rates[2] if a.scenario == "game" else None
     line = {
-        "metric": METRIC, "value": round(sat / dev, 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": round(1000 * dev / a.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"cfg4 {a.scenario} (paper game: 6 LeNet-5 + 1 ResNet-50 per app request, P:787) "
-                               f"on 1-GPU gpu-let plans, mode {a.mode}" if a.scenario == "game" else
-                               f"cfg4 {a.scenario}, mode {a.mode}",
-                   "rate_multiplier": round(head["rate_multiplier"], 4), "rates_req_s": head["rates"],
-                   "slo_us": slo, "gpulets": head["gpulets"], "lanes": head["lanes"],
-                   "requests_per_step": tot / (a.steps * world), "slo_satisfied_frac": round(sat / max(tot, 1), 4),
-                   "l2_flush": "none: inputs resident; the six models' weights (~0.58 GB) exceed L2 across steps",
-                   "parallelism": f"dp{world} (independent replicas of the 1-GPU plan)"},
-        "gpu_launches": len(head["gpulets"]) + 3,
-        "wall_req_per_s": round(tot / wall, 2),
-        "gpulet_tensor_frac": head["gpulet_tensor_frac"],
-        "roofline": roof, "clocks": head["clocks"], "e2e": head["e2e"],
+        "metric": METRIC, "value": round(head["value"], 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(1000 * head.get("dev_s", 0.0) / max(head.get("windows", 1), 1), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": (f"cfg4 {a.scenario}: paper game (6 LeNet-5 + 1 ResNet-50 per app request, P:787), "
+                                if a.scenario == "game" else f"cfg4 {a.scenario}, ")
+                   + f"max Poisson rate with <=1% SLO violations, mode {a.mode}, gpu-lets on {world} GPU(s)",
+                   "rate_multiplier": round(head["x"], 4), "x_sched_max": round(head["x_sched"], 4),
+                   "rates_req_s": rates, "app_req_s": app, "slo_us": slo, "lanes": head.get("lanes", []),
+                   "window_s": a.window, "arrivals": head.get("arrivals"),
+                   "slo_satisfied_frac": round(1 - head.get("viol_frac", 1.0), 4), "probes": head["probes"],
+                   "per_model": head.get("per_model"),
+                   "l2_flush": "none: inputs resident; six models' weights (~0.58 GB) exceed L2 between batches",
+                   "parallelism": f"dp{world} (gpu-lets placed on {world} GPU(s) by the scheduler)"},
+        "gpu_launches": len({ln["gpulet"] for ln in head.get("lanes", [])}),
+        "gpu_launches_note": "persistent executors serving the timed windows (launched at gpu-let creation)",
+        "roofline": roof, "clocks": head.get("clocks"), "e2e": head.get("e2e"),
     }
     line.update(extra)
     if not a.no_cpu_baseline and world == 1:
@@ -372,12 +477,15 @@ def our_arm(a, world, rank, local, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="gpulet+int", choices=["gpulet", "gpulet+int", "sbp"])
     ap.add_argument("--scenario", default="game")
-    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
+    ap.add_argument("--probe-window", type=float, default=0.5)
+    ap.add_argument("--probes", type=int, default=6)
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--verbose", action="store_true")

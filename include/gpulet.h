@@ -115,8 +115,12 @@ gl_status gl_poll(gl_ctx* ctx, gl_completion* out, int32_t max, int32_t* n_out);
 gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completion* out);
 
 /* ---- latency profiler (§4.3 L(b,p)) ------------------------ */
-/* Run `warmup` + `reps` back-to-back batches of model_id at `batch` on gpulet_id and
- * return the median device latency (t_end - t_start) in microseconds. */
+/* Run `warmup` + `reps` batches of model_id at `batch` on gpulet_id, one in flight
+ * at a time, and return the median service latency as the frontend observes it:
+ * gl_submit_batch -> completion visible to gl_poll (host clock, microseconds;
+ * includes the ring hand-off and completion detection, which the SLO-driven
+ * scheduler must budget for).  Other completions seen meanwhile are kept for
+ * gl_poll. */
 gl_status gl_profile(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t batch, int32_t warmup, int32_t reps,
                      const void* in_dev, void* out_dev, double* median_us);
 
@@ -144,13 +148,26 @@ typedef struct {
   int32_t pad_;
   const void* in_dev;   /* device input holding `batch` requests (first k used for a k-batch) */
   void* out_dev;        /* device output */
+  const void* in_host;  /* NULL, or pinned host inputs (end-to-end mode): the k requests of a batch are
+                           copied H2D into in_dev before it is submitted (request r of the trace uses
+                           in_host + (r % host_slots) * in_req_bytes) */
+  void* out_host;       /* end-to-end mode: outputs copied D2H here on completion (same slot rule) */
+  int64_t in_req_bytes, out_req_bytes;  /* bytes of one request's input / output */
+  int32_t host_slots;   /* requests held in in_host / out_host */
+  int32_t pad2_;
 } gl_lane;
 /* Replay an arrival trace in real time (host clock): arr_us[n_req] sorted arrival
  * times (us from the call), arr_model[n_req] model slot of each request.  Returns
- * per-request latency in lat_us (us; -1 dropped).  Blocks until every request is
- * completed or dropped.  Errors: GL_E_ARG, GL_E_TIMEOUT, errors of submit/poll. */
+ * per-request latency in lat_us (us; -1 dropped) and, when dev_ns is not NULL,
+ * dev_ns[0..1] = first dequeue and last completion (%globaltimer ns) of the
+ * batches it ran.  In end-to-end mode (lanes with in_host) a lane keeps at most
+ * one batch in flight and the latency includes the H2D / D2H copies; *h2d_bytes /
+ * *d2h_bytes (may be NULL) return the bytes copied.  Blocks until every request
+ * is completed or dropped.  Errors: GL_E_ARG, GL_E_TIMEOUT, GL_E_CUDA, errors of
+ * submit/poll. */
 gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
-                   const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us);
+                   const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
+                   uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* ---- scheduler (Alg. 1) --------------------------------- */
 typedef struct {

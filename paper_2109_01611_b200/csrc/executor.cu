@@ -58,6 +58,8 @@ struct Smem {
   uint64_t* tl;      // optional per-tile timeline of step 0 for this CTA (tuning tool)
   int tl_cap;
   int flags;         // ExecParams::dbg_flags
+  GemmArgs* opc;     // shared-memory copy of the current GEMM step's op args (first kOpCache ops)
+  int* opn;          //   and their unit counts
 };
 
 __device__ __forceinline__ void tl_mark(const Smem& S, int i, int k) {
@@ -230,7 +232,7 @@ __device__ __forceinline__ void rowcache_init(RowCache& rc, const Gather& g, int
       const int ho = rem / g.Wo, wo = rem - ho * g.Wo;
       rc.pix[i] = n * g.H * g.W;
       rc.h0[i] = ho * g.stride - g.pad;
-      rc.w0[i] = wo * g.stride - g.pad;
+      rc.w0[i] = wo * g.stride - g.padw;
     } else {
       rc.pix[i] = -1;
       rc.h0[i] = rc.w0[i] = 0;
@@ -279,6 +281,26 @@ __device__ __forceinline__ int locate(const OpDesc* ops, int nops, int t, int& l
   return i;
 }
 
+// The ops of a GEMM step with their args served from the shared-memory cache
+// (read once per step instead of from global memory on every tile).
+struct StepOps {
+  const OpDesc* ops;
+  const GemmArgs* sg;   // shared copies of ops[0 .. min(n, kOpCache))
+  const int* su;
+  int n;
+  __device__ __forceinline__ const GemmArgs& g(int i) const { return i < kOpCache ? sg[i] : ops[i].g; }
+  __device__ __forceinline__ int units(int i) const { return i < kOpCache ? su[i] : ops[i].n_units; }
+  __device__ __forceinline__ int locate(int t, int& lt) const {
+    int i = 0;
+    while (i < n - 1 && t >= units(i)) {
+      t -= units(i);
+      ++i;
+    }
+    lt = t;
+    return i;
+  }
+};
+
 // ------------------------------------------------------------------ GEMM step (K1-K4)
 // Roles.  Steps whose operands all come by TMA: warp 9 (one thread) produces,
 // warp 8 (one thread) issues tcgen05.mma, warps 0-7 run the epilogue (warp w
@@ -291,26 +313,41 @@ __device__ __forceinline__ int locate(const OpDesc* ops, int nops, int t, int& l
 // c fastest, so a box never straddles a tap (cb divides C).  Taps past the
 // filter (K padding; the weights there are zero) re-read tap (0, 0) so the smem
 // operand stays finite.
-__device__ __forceinline__ void im2col_kblock(const GemmArgs& g, const void* tmap, uint64_t* bar, uint32_t sa, int kb,
+struct Im2colGeo {   // register copy of the im2col geometry (no global reloads in the k loop)
+  int cb, C, KW, ntaps;
+};
+
+__device__ __forceinline__ void im2col_kblock(const Im2colGeo& q, const void* tmap, uint64_t* bar, uint32_t sa, int kb,
                                               int icw, int ich, int icn) {
-  const int cb = g.a_cb ? g.a_cb : 64;
-  const int ntaps = g.ga.KH * g.ga.KW;
-  for (int j = 0; j < 64 / cb; ++j) {
-    const int k0 = kb * 64 + j * cb;
-    int tap = k0 / g.ga.C, c0 = k0 - tap * g.ga.C;
-    if (tap >= ntaps) tap = 0, c0 = 0;
-    const int kh = tap / g.ga.KW, kw = tap - kh * g.ga.KW;
-    tma_load_im2col_4d(sa + j * 128 * cb * 2, tmap, bar, c0, icw, ich, icn, (uint16_t)kw, (uint16_t)kh);
+  for (int j = 0; j < 64 / q.cb; ++j) {
+    const int k0 = kb * 64 + j * q.cb;
+    int tap = k0 / q.C, c0 = k0 - tap * q.C;
+    if (tap >= q.ntaps) tap = 0, c0 = 0;
+    const int kh = tap / q.KW, kw = tap - kh * q.KW;
+    tma_load_im2col_4d(sa + j * 128 * q.cb * 2, tmap, bar, c0, icw, ich, icn, (uint16_t)kw, (uint16_t)kh);
   }
 }
 
-// UMMA smem descriptor of the A operand for the K=16 step k (0..3) of a stage.
-__device__ __forceinline__ uint64_t a_desc(const GemmArgs& g, uint32_t a0, int k) {
-  if (g.a_tma != SRC_IM2COL || g.a_cb == 0 || g.a_cb == 64) return umma_sdesc_sw128(a0 + k * 32);
-  switch (g.a_cb) {
-    case 32: return umma_sdesc(a0 + (k >> 1) * 8192 + (k & 1) * 32, 4, 512, 16);       // SW64, 64-B rows
-    case 16: return umma_sdesc(a0 + k * 4096, 6, 256, 16);                            // SW32, 32-B rows
-    default: return umma_sdesc(a0 + k * 4096, 0, 128, 2048);                         // no swizzle, 16-B rows
+__device__ __forceinline__ Im2colGeo im2col_geo(const GemmArgs& g) {
+  Im2colGeo q;
+  q.cb = g.a_cb ? g.a_cb : 64;
+  q.C = g.ga.C;
+  q.KW = g.ga.KW;
+  q.ntaps = g.ga.KH * g.ga.KW;
+  return q;
+}
+
+// UMMA smem descriptor of the A operand for the K=16 step k (0..3) of a stage;
+// amode = 64 (128-B swizzle), 32, 16 or 8 (im2col channel box).
+__device__ __forceinline__ int a_mode(const GemmArgs& g) {
+  return (g.a_tma != SRC_IM2COL || g.a_cb == 0 || g.a_cb == 64) ? 64 : g.a_cb;
+}
+__device__ __forceinline__ uint64_t a_desc(int amode, uint32_t a0, int k) {
+  switch (amode) {
+    case 64: return umma_sdesc_sw128(a0 + k * 32);
+    case 32: return umma_sdesc(a0 + (k >> 1) * 8192 + (k & 1) * 32, 4, 512, 16);   // SW64, 64-B rows
+    case 16: return umma_sdesc(a0 + k * 4096, 6, 256, 16);                        // SW32, 32-B rows
+    default: return umma_sdesc(a0 + k * 4096, 0, 128, 2048);                     // no swizzle, 16-B rows
   }
 }
 
@@ -392,13 +429,26 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
   }
 }
 
-__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& S, Pipe& P) {
+__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& Sio, Pipe& Pio) {
+  // register copies: the k loops must not reload ring state through memory
+  // after every asm statement (they all clobber "memory")
+  const Smem S = Sio;
+  Pipe P = Pio;
+  {
+    constexpr int W = (int)sizeof(GemmArgs) / 4;
+    const int nc = min(nops, kOpCache);
+    for (int i = threadIdx.x; i < nc * W; i += blockDim.x)
+      ((uint32_t*)S.opc)[i] = ((const uint32_t*)&ops[i / W].g)[i % W];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) S.opn[i] = ops[i].n_units;
+    __syncthreads();
+  }
+  const StepOps so{ops, S.opc, S.opn, nops};
   int total = 0, maxbn = 16;
   bool gstep = false;
   for (int i = 0; i < nops; ++i) {
-    total += ops[i].n_units;
-    maxbn = max(maxbn, ops[i].g.BN);
-    gstep |= ops[i].g.a_tma == SRC_GATHER || ops[i].g.b_tma == SRC_GATHER;
+    total += so.units(i);
+    maxbn = max(maxbn, so.g(i).BN);
+    gstep |= so.g(i).a_tma == SRC_GATHER || so.g(i).b_tma == SRC_GATHER;
   }
   const uint32_t sbytes = stage_bytes_for(maxbn);
   P.nst = min((uint32_t)kMaxStages, (uint32_t)kRingBytes / sbytes);
@@ -412,9 +462,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   int my_tiles = 0, my_kb = 0;
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     int lt;
-    const OpDesc* op = ops + locate(ops, nops, tile, lt);
+    const int oi = so.locate(tile, lt);
     int mb, nb, kb0, kb1;
-    decode_tile(op->g, lt, mb, nb, kb0, kb1);
+    decode_tile(so.g(oi), lt, mb, nb, kb0, kb1);
     ++my_tiles;
     my_kb += kb1 - kb0;
   }
@@ -425,8 +475,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     if (t == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
-      const OpDesc* op = ops + locate(ops, nops, tile, lt);
-      const GemmArgs& g = op->g;
+      const int oi = so.locate(tile, lt);
+      const OpDesc* op = ops + oi;
+      const GemmArgs& g = so.g(oi);
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
       const bool gather = g.a_tma == SRC_GATHER || g.b_tma == SRC_GATHER;
@@ -449,7 +500,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         icn = m0 / HoWo;
         const int rem = m0 - icn * HoWo, ho = rem / g.ga.Wo, wo = rem - ho * g.ga.Wo;
         ich = ho * g.ga.stride - g.ga.pad;
-        icw = wo * g.ga.stride - g.ga.pad;
+        icw = wo * g.ga.stride - g.ga.padw;
       }
       const uint32_t tx = (g.a_tma ? 128 * 128 : 0) + (g.b_tma ? g.BN * 128 : 0);
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -460,7 +511,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
           if (g.a_tma == SRC_TMA) {
             tma_load_2d(sa, &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
           } else if (g.a_tma == SRC_IM2COL) {
-            im2col_kblock(g, &op->tmap_a, &S.full[P.stage], sa, kb, icw, ich, icn);
+            im2col_kblock(im2col_geo(g), &op->tmap_a, &S.full[P.stage], sa, kb, icw, ich, icn);
           }
           if (g.b_tma) tma_load_2d(sbb, &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
         }
@@ -489,82 +540,101 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     P.npend = 0;
     if (t == 0) dbg_mark(S, 1);
   } else if (!gstep && warp == 9) {
-    // ---------------- TMA producer (one thread)
-    if (lane == 0) {
-      dbg_mark(S, 0);
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        int lt;
-        const OpDesc* op = ops + locate(ops, nops, tile, lt);
-        const GemmArgs& g = op->g;
-        int mb, nb, kb0, kb1;
-        decode_tile(g, lt, mb, nb, kb0, kb1);
-        int icw = 0, ich = 0, icn = 0;
-        if (g.a_tma == SRC_IM2COL) {
-          const int m0 = mb * 128, HoWo = g.ga.Ho * g.ga.Wo;
-          icn = m0 / HoWo;
-          const int rem = m0 - icn * HoWo, ho = rem / g.ga.Wo, wo = rem - ho * g.ga.Wo;
-          ich = ho * g.ga.stride - g.ga.pad;
-          icw = wo * g.ga.stride - g.ga.pad;
-        }
-        const uint32_t tx = 128 * 128 + g.BN * 128;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&S.empty[P.stage], par(P) ^ 1);   // empty[stage]
-          if (S.flags & 8) {
-            mbar_arrive_cnt(&S.full[P.stage], 129);
-            advance(P);
-            continue;
-          }
-          const uint32_t sa = ring + P.stage * sbytes, sbb = sa + kStageBytesA;
-          mbar_arrive_expect_tx(&S.full[P.stage], tx);
-          if (g.a_tma == SRC_TMA) {
-            tma_load_2d(sa, &op->tmap_a, &S.full[P.stage], kb * 64, mb * 128);
+    // ---------------- TMA producer (whole warp walks the loop; one elected lane issues)
+    if (lane == 0) dbg_mark(S, 0);
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int lt;
+      const int oi = so.locate(tile, lt);
+      const OpDesc* op = ops + oi;
+      const GemmArgs& g = so.g(oi);
+      int mb, nb, kb0, kb1;
+      decode_tile(g, lt, mb, nb, kb0, kb1);
+      int icw = 0, ich = 0, icn = 0;
+      if (g.a_tma == SRC_IM2COL) {
+        const int m0 = mb * 128, HoWo = g.ga.Ho * g.ga.Wo;
+        icn = m0 / HoWo;
+        const int rem = m0 - icn * HoWo, ho = rem / g.ga.Wo, wo = rem - ho * g.ga.Wo;
+        ich = ho * g.ga.stride - g.ga.pad;
+        icw = wo * g.ga.stride - g.ga.padw;
+      }
+      const uint32_t tx = 128 * 128 + g.BN * 128;
+      const bool a2d = g.a_tma == SRC_TMA;
+      const Im2colGeo q = im2col_geo(g);
+      const int arow = mb * 128, brow = nb * g.BN;
+      const void* tA = &op->tmap_a;
+      const void* tB = &op->tmap_b;
+      const bool skip = (S.flags & 8) != 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&S.empty[P.stage], par(P) ^ 1);
+        uint64_t* fb = &S.full[P.stage];
+        if (elect_one()) {
+          if (skip) {
+            mbar_arrive_cnt(fb, 129);
           } else {
-            im2col_kblock(g, &op->tmap_a, &S.full[P.stage], sa, kb, icw, ich, icn);
+            const uint32_t sa = ring + P.stage * sbytes;
+            mbar_arrive_expect_tx(fb, tx);
+            if (a2d)
+              tma_load_2d(sa, tA, fb, kb * 64, arow);
+            else
+              im2col_kblock(q, tA, fb, sa, kb, icw, ich, icn);
+            tma_load_2d(sa + kStageBytesA, tB, fb, kb * 64, brow);
+            mbar_arrive_cnt(fb, 128);
           }
-          tma_load_2d(sbb, &op->tmap_b, &S.full[P.stage], kb * 64, nb * g.BN);
-          mbar_arrive_cnt(&S.full[P.stage], 128);
-          advance(P);
         }
+        __syncwarp();
+        advance(P);
       }
-      dbg_mark(S, 1);
     }
-    __syncwarp();
+    if (lane == 0) dbg_mark(S, 1);
   } else if (warp == 8) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t tbase = *S.tmem_base;
-      int ntile = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        int lt;
-        const OpDesc* op = ops + locate(ops, nops, tile, lt);
-        const GemmArgs& g = op->g;
-        int mb, nb, kb0, kb1;
-        decode_tile(g, lt, mb, nb, kb0, kb1);
-        const uint32_t acc = P.acc & 1, use = P.acc >> 1;
-        mbar_wait(&S.tempty[acc], (use & 1) ^ 1);
-        tc_fence_after();
-        tl_mark(S, ntile, 0);
-        const uint32_t d = tbase + acc * 256;
-        const uint32_t idesc = umma_idesc_bf16(128, g.BN);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&S.full[P.stage], par(P));
-          tc_fence_after();
-          if (tile == (int)blockIdx.x && kb == kb0) dbg_mark(S, 2);
-          const uint32_t a0 = ring + P.stage * sbytes, b0 = a0 + kStageBytesA;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (!(S.flags & 4))
-              umma_bf16(d, a_desc(g, a0, k), umma_sdesc_sw128(b0 + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&S.empty[P.stage]);   // empty[stage]
-          advance(P);
+    // ---------------- MMA issuer (whole warp walks the loop; one elected lane issues)
+    const uint32_t tbase = *S.tmem_base;
+    const uint64_t bhi = umma_sdesc_sw128(0);
+    int ntile = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int lt;
+      const int oi = so.locate(tile, lt);
+      const OpDesc* op = ops + oi;
+      const GemmArgs& g = so.g(oi);
+      int mb, nb, kb0, kb1;
+      decode_tile(g, lt, mb, nb, kb0, kb1);
+      const uint32_t acc = P.acc & 1, use = P.acc >> 1;
+      mbar_wait(&S.tempty[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) tl_mark(S, ntile, 0);
+      const uint32_t d = tbase + acc * 256;
+      const uint32_t idesc = umma_idesc_bf16(128, g.BN);
+      // A descriptor = ahi | ((stage A address + ko[k]) >> 4) for the K=16 step k
+      const int amode = a_mode(g);
+      const uint64_t ahi = a_desc(amode, 0, 0);
+      const uint32_t ko1 = amode == 64 ? 32 : amode == 32 ? 32 : 4096;
+      const uint32_t ko2 = amode == 64 ? 64 : 8192;
+      const uint32_t ko3 = amode == 64 ? 96 : amode == 32 ? 8224 : 12288;
+      const bool do_mma = !(S.flags & 4);
+      if (tile == (int)blockIdx.x && lane == 0) dbg_mark(S, 2);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&S.full[P.stage], par(P));
+        if (!(S.flags & 16)) tc_fence_after();
+        const uint32_t a0 = ring + P.stage * sbytes, b0 = a0 + kStageBytesA;
+        if (elect_one()) {
+          if (do_mma) {
+            umma_bf16(d, ahi | ((a0 & 0x3FFFF) >> 4), bhi | ((b0 & 0x3FFFF) >> 4), idesc, kb > kb0 ? 1u : 0u);
+            umma_bf16(d, ahi | (((a0 + ko1) & 0x3FFFF) >> 4), bhi | (((b0 + 32) & 0x3FFFF) >> 4), idesc, 1u);
+            umma_bf16(d, ahi | (((a0 + ko2) & 0x3FFFF) >> 4), bhi | (((b0 + 64) & 0x3FFFF) >> 4), idesc, 1u);
+            umma_bf16(d, ahi | (((a0 + ko3) & 0x3FFFF) >> 4), bhi | (((b0 + 96) & 0x3FFFF) >> 4), idesc, 1u);
+          }
+          umma_commit(&S.empty[P.stage]);
         }
-        umma_commit(&S.tfull[acc]);
-        tl_mark(S, ntile++, 1);
-        ++P.acc;
+        __syncwarp();
+        advance(P);
       }
-      dbg_mark(S, 3);
+      if (elect_one()) umma_commit(&S.tfull[acc]);
+      __syncwarp();
+      if (lane == 0) tl_mark(S, ntile, 1);
+      ++ntile;
+      ++P.acc;
     }
-    __syncwarp();
+    if (lane == 0) dbg_mark(S, 3);
   } else if (warp < 8) {
     // ---------------- epilogue: warps 4-7 (all columns) or 0-7 (column halves)
     const int q = warp & 3, half = warp < 4 ? 1 : 0;
@@ -574,11 +644,19 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     int ntile = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
-      const OpDesc* op = ops + locate(ops, nops, tile, lt);
-      const GemmArgs& g = op->g;
+      const int oi = so.locate(tile, lt);
+      const OpDesc* op = ops + oi;
+      const GemmArgs& g = so.g(oi);
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
       const uint32_t acc = P.acc & 1, use = P.acc >> 1;
+      {
+        // bias lines of this tile -> L1 while the accumulator is still being computed
+        const char* bias = (const char*)res(g.ep.bias, X);
+        const int bn = g.ep.bias_on_m ? mb * 128 : nb * g.BN;
+        const int nbytes = (g.ep.bias_on_m ? 128 : g.BN) * 2;
+        if (bias && lane * 128 < nbytes) prefetch_l1(bias + bn * 2 + lane * 128);
+      }
       mbar_wait(&S.tfull[acc], use & 1);
       tc_fence_after();
       const bool lead = q == 0 && half == 0 && lane == 0;
@@ -609,6 +687,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   P.bits = bits0 ^ flips;
   P.stage = 0;
   P.acc = acc0 + my_tiles;
+  Pio = P;
 }
 
 // ------------------------------------------------------------------ split-K final
@@ -965,16 +1044,29 @@ __device__ __noinline__ void layernorm(const OpDesc* op, const Ctx& X) {
   const __nv_bfloat16 *g = (const __nv_bfloat16*)res(a.g, X), *b = (const __nv_bfloat16*)res(a.b, X);
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < a.rows; r += gridDim.x * wpb) {
-    float v[24];
+  const int nw = gridDim.x * wpb;
+  // two rows per warp iteration, both rows' loads issued before either reduction
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < a.rows; r += 2 * nw) {
+    const int r2 = r + nw;
+    uint4 u[2][3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const uint4 xv = *(const uint4*)(x + (int64_t)r * 768 + j * 256 + lane * 8);
-      const __nv_bfloat16* xx = (const __nv_bfloat16*)&xv;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) v[j * 8 + c] = __bfloat162float(xx[c]);
+      u[0][j] = __ldcs((const uint4*)(x + (int64_t)r * 768 + j * 256 + lane * 8));
+      u[1][j] = r2 < a.rows ? __ldcs((const uint4*)(x + (int64_t)r2 * 768 + j * 256 + lane * 8))
+                            : make_uint4(0u, 0u, 0u, 0u);
     }
-    ln_row_store(v, g, b, a.eps, y + (int64_t)r * 768, lane);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && r2 >= a.rows) break;
+      float v[24];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const __nv_bfloat16* xx = (const __nv_bfloat16*)&u[h][j];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[j * 8 + c] = __bfloat162float(xx[c]);
+      }
+      ln_row_store(v, g, b, a.eps, y + (int64_t)(h ? r2 : r) * 768, lane);
+    }
   }
 }
 
@@ -1203,6 +1295,38 @@ __device__ __noinline__ void softmax_rows(const OpDesc* op, const Ctx& X) {
   }
 }
 
+// ------------------------------------------------------------------ input re-layout for small-C first convs
+// k = 0: 2x2 space-to-depth, y[n, P, Q, (dy*2 + dx)*C + c] = x[n, 2P+dy, 2Q+dx, c];
+// k = 1: kw taps into channels, y[n, h, w, kw*C + c] = x[n, h, w + kw - pad, c]
+// (zero outside the image and for the channels past KW*C).  C = 8 (one 16-B
+// vector per pixel); one 16-B output vector per thread item.
+__device__ __noinline__ void pack_input(const OpDesc* op, const Ctx& X) {
+  const MiscArgs& a = op->m;
+  const uint4* x = (const uint4*)res(a.x, X);
+  uint4* y = (uint4*)res(a.y, X);
+  const int cv = a.C / 8;                 // input vectors per pixel
+  const int ov = a.cols / 8;              // output vectors per pixel
+  const int total = a.N * a.Ho * a.Wo * ov;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int j = i % ov;
+    int p = i / ov;
+    const int w = p % a.Wo;
+    p /= a.Wo;
+    const int h = p % a.Ho, n = p / a.Ho;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (a.k == 0) {
+      const int sub = j / cv, c = j % cv;   // sub = dy*2 + dx
+      const int hi = 2 * h + (sub >> 1), wi = 2 * w + (sub & 1);
+      v = __ldcs(x + ((n * a.H + hi) * a.W + wi) * cv + c);
+    } else {
+      const int kw = j / cv, c = j % cv;
+      const int wi = w + kw - a.pad;
+      if (kw < a.stride && wi >= 0 && wi < a.W) v = __ldg(x + ((n * a.H + h) * a.W + wi) * cv + c);
+    }
+    y[i] = v;
+  }
+}
+
 // ------------------------------------------------------------------ 16-B vector copy
 __device__ __noinline__ void copy_vec(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
@@ -1233,6 +1357,7 @@ __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P)
     case OP_SOFTMAX: softmax_rows(op, X); break;
     case OP_SPLITK_FINAL: splitk_final(op, X); break;
     case OP_COPY: copy_vec(op, X); break;
+    case OP_PACK: pack_input(op, X); break;
     default: __trap();
   }
 }
@@ -1288,6 +1413,8 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.tl = p.tl ? p.tl + (size_t)blockIdx.x * p.tl_cap : nullptr;
   S.tl_cap = p.tl_cap;
   S.flags = p.dbg_flags;
+  S.opc = (GemmArgs*)(base + kRingBytes + 1024 + kEpiStageBytes);
+  S.opn = (int*)(S.opc + kOpCache);
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {

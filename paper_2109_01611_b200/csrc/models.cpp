@@ -77,6 +77,80 @@ static WRef conv_weight(DevWeights& dw, const ParamMap& P, const std::string& na
   return r;
 }
 
+// Stride-2 conv on a 2x2 space-to-depth input: weight
+// [Cout, K, K, ci] -> [Cout, K', K', dy, dx, cin_pad] with kh = 2a + dy + p - 2A
+// (A = ceil(p / 2)), zero where (kh, kw) falls outside the K x K window.
+static WRef conv_weight_s2d(DevWeights& dw, const ParamMap& P, const std::string& name, int cin_pad, int pad, int& Kp,
+                            int& A, Err& e) {
+  auto it = P.find(name + ".w");
+  if (it == P.end()) {
+    e.fail("missing parameter " + name + ".w");
+    return {};
+  }
+  const Param& p = it->second;
+  const int co = p.shape[0], K = p.shape[1], ci = p.shape[3];
+  A = (pad + 1) / 2;
+  Kp = (K + 2 * A - pad + 1) / 2;
+  const int C4 = 4 * cin_pad;
+  WRef r;
+  r.rows = co;
+  r.K_real = Kp * Kp * C4;
+  r.K_pad = rup(r.K_real, 64);
+  const std::string key = name + "#s2d" + std::to_string(cin_pad);
+  auto f = dw.ptr.find(key);
+  if (f != dw.ptr.end()) {
+    r.ptr = f->second;
+    return r;
+  }
+  std::vector<uint16_t> buf((size_t)co * r.K_pad, 0);
+  for (int o = 0; o < co; ++o)
+    for (int a = 0; a < Kp; ++a)
+      for (int b = 0; b < Kp; ++b)
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            const int kh = 2 * a + dy + pad - 2 * A, kw = 2 * b + dx + pad - 2 * A;
+            if (kh < 0 || kh >= K || kw < 0 || kw >= K) continue;
+            for (int c = 0; c < ci; ++c)
+              buf[(size_t)o * r.K_pad + ((a * Kp + b) * 4 + dy * 2 + dx) * cin_pad + c] =
+                  p.data[(((size_t)o * K + kh) * K + kw) * ci + c];
+          }
+  r.ptr = upload(dw, buf.data(), buf.size() * 2);
+  dw.ptr[key] = r.ptr;
+  return r;
+}
+
+// Stride-1 conv on a kw-packed input (channel kw * cin_pad + c holds input
+// column w + kw - pad): weight [Cout, K, K, ci] -> [Cout, K, 1, cpk].
+static WRef conv_weight_kwpack(DevWeights& dw, const ParamMap& P, const std::string& name, int cin_pad, int cpk,
+                               Err& e) {
+  auto it = P.find(name + ".w");
+  if (it == P.end()) {
+    e.fail("missing parameter " + name + ".w");
+    return {};
+  }
+  const Param& p = it->second;
+  const int co = p.shape[0], K = p.shape[1], ci = p.shape[3];
+  WRef r;
+  r.rows = co;
+  r.K_real = K * cpk;
+  r.K_pad = rup(r.K_real, 64);
+  const std::string key = name + "#kwp" + std::to_string(cpk);
+  auto f = dw.ptr.find(key);
+  if (f != dw.ptr.end()) {
+    r.ptr = f->second;
+    return r;
+  }
+  std::vector<uint16_t> buf((size_t)co * r.K_pad, 0);
+  for (int o = 0; o < co; ++o)
+    for (int kh = 0; kh < K; ++kh)
+      for (int kw = 0; kw < K; ++kw)
+        for (int c = 0; c < ci; ++c)
+          buf[(size_t)o * r.K_pad + kh * cpk + kw * cin_pad + c] = p.data[(((size_t)o * K + kh) * K + kw) * ci + c];
+  r.ptr = upload(dw, buf.data(), buf.size() * 2);
+  dw.ptr[key] = r.ptr;
+  return r;
+}
+
 // FC weight [out, in] -> [out, K_pad].
 static WRef fc_weight(DevWeights& dw, const ParamMap& P, const std::string& name, Err& e) {
   auto it = P.find(name + ".w");
@@ -391,7 +465,7 @@ class Builder {
     std::memset(&g, 0, sizeof(g));
     g.x = x.ref;
     g.H = x.H, g.W = x.W, g.C = x.C, g.lda = x.ld;
-    g.KH = KH, g.KW = KH, g.stride = stride, g.pad = pad;
+    g.KH = KH, g.KW = KH, g.stride = stride, g.pad = pad, g.padw = pad;
     g.Ho = Ho, g.Wo = Wo;
     return g;
   }
@@ -400,7 +474,7 @@ class Builder {
     std::memset(&g, 0, sizeof(g));
     g.x = x;
     g.H = 1, g.W = 1, g.C = K, g.lda = lda;
-    g.KH = 1, g.KW = 1, g.stride = 1, g.pad = 0;
+    g.KH = 1, g.KW = 1, g.stride = 1, g.pad = 0, g.padw = 0;
     g.Ho = 1, g.Wo = 1;
     return g;
   }
@@ -409,8 +483,15 @@ class Builder {
   Act conv(const Act& x, const std::string& name, int k, int stride, int pad, int act, const Act* resid = nullptr,
            const Act* out = nullptr, int col_off = 0) {
     if (x.ref.kind == BUF_IN && x.C % 8 == 0 && !g_tune[TUNE_GATHER]) {
-      // the request input is not at a fixed address: stage it in the workspace
-      // (one copy step) so the conv reads it by TMA instead of a cp.async gather
+      // The request input is not at a fixed address: stage it in the workspace
+      // (one step) so the conv reads it by TMA.  Small-C first layers are
+      // re-laid out on the way so each im2col pixel carries >= 32 channels:
+      // stride 2 -> 2x2 space-to-depth; stride 1 -> kw taps packed into channels.
+      const int Ho = (x.H + 2 * pad - k) / stride + 1, Wo = (x.W + 2 * pad - k) / stride + 1;
+      if (x.C <= 16 && k >= 3 && stride == 2 && x.H % 2 == 0 && x.W % 2 == 0 && !resid && !out)
+        return conv_s2d(x, name, k, pad, act, Ho, Wo);
+      if (x.C <= 16 && k >= 3 && stride == 1 && k * x.C <= 64 && !resid && !out)
+        return conv_kwpack(x, name, k, pad, act, Ho, Wo);
       const Act xs = stage_input(x);
       const Act y = conv(xs, name, k, stride, pad, act, resid, out, col_off);
       release_off(xs.ref.off);
@@ -429,6 +510,47 @@ class Builder {
     ep.act = act;
     if (resid) ep.res = resid->ref;
     gemm_gather_a(conv_gather(x, k, stride, pad, Ho, Wo), x.N * Ho * Wo, w, bias, ep);
+    return y;
+  }
+
+  Act pack_input(const Act& x, int mode, int H, int W, int C, int kw, int pad) {
+    Act y = tensor(x.N, H, W, C);
+    OpDesc& op = add(OP_PACK);
+    MiscArgs& a = op.m;
+    a.x = x.ref, a.y = y.ref;
+    a.N = x.N, a.H = x.H, a.W = x.W, a.C = x.C;
+    a.Ho = H, a.Wo = W, a.cols = C, a.k = mode, a.stride = kw, a.pad = pad;
+    op.n_units = 1;
+    step();
+    return y;
+  }
+
+  Act conv_s2d(const Act& x, const std::string& name, int k, int pad, int act, int Ho, int Wo) {
+    const Act xs = pack_input(x, 0, x.H / 2, x.W / 2, 4 * x.C, 0, 0);
+    int Kp = 0, A = 0;
+    WRef w = conv_weight_s2d(dw, P, name, x.C, pad, Kp, A, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    Act y = tensor(x.N, Ho, Wo, w.rows);
+    Epilogue ep = plain_ep(y.ref, y.ld, 0);
+    ep.act = act;
+    gemm_gather_a(conv_gather(xs, Kp, 1, A, Ho, Wo), x.N * Ho * Wo, w, bias, ep);
+    release_off(xs.ref.off);
+    return y;
+  }
+
+  Act conv_kwpack(const Act& x, const std::string& name, int k, int pad, int act, int Ho, int Wo) {
+    const int cpk = k * x.C <= 16 ? 16 : k * x.C <= 32 ? 32 : 64;
+    const Act xs = pack_input(x, 1, x.H, x.W, cpk, k, pad);
+    WRef w = conv_weight_kwpack(dw, P, name, x.C, cpk, e);
+    void* bias = raw_param(dw, P, name + ".b", e);
+    Act y = tensor(x.N, Ho, Wo, w.rows);
+    Epilogue ep = plain_ep(y.ref, y.ld, 0);
+    ep.act = act;
+    Gather g = conv_gather(xs, k, 1, pad, Ho, Wo);
+    g.KW = 1;   // K x 1 window over the packed columns (the kw taps are channels)
+    g.padw = 0;
+    gemm_gather_a(g, x.N * Ho * Wo, w, bias, ep);
+    release_off(xs.ref.off);
     return y;
   }
 
@@ -1130,8 +1252,8 @@ bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::str
       const int nimg = x.rows / (x.Ho * x.Wo);
       cuuint64_t dims[4] = {(cuuint64_t)x.C, (cuuint64_t)x.W, (cuuint64_t)x.H, (cuuint64_t)nimg};
       cuuint64_t strides[3] = {(cuuint64_t)x.C * 2, (cuuint64_t)x.W * x.C * 2, (cuuint64_t)x.H * x.W * x.C * 2};
-      int lower[2] = {-x.pad, -x.pad};
-      int upper[2] = {-x.pad + (x.Wo - 1) * x.stride - (x.W - 1), -x.pad + (x.Ho - 1) * x.stride - (x.H - 1)};
+      int lower[2] = {-x.padw, -x.pad};
+      int upper[2] = {-x.padw + (x.Wo - 1) * x.stride - (x.W - 1), -x.pad + (x.Ho - 1) * x.stride - (x.H - 1)};
       cuuint32_t es[4] = {1, (cuuint32_t)x.stride, (cuuint32_t)x.stride, 1};
       const int cb = g.a_cb ? g.a_cb : 64;
       const CUtensorMapSwizzle sw = cb == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -1197,6 +1319,9 @@ void op_cost(const OpDesc& op, double& flops, double& bytes) {
       break;
     case OP_COPY:
       bytes = 32.0 * op.m.rows;
+      break;
+    case OP_PACK:
+      bytes = 2.0 * op.m.N * ((double)op.m.H * op.m.W * op.m.C + (double)op.m.Ho * op.m.Wo * op.m.cols);
       break;
     default: break;
   }

@@ -22,7 +22,9 @@ enum OpType : int32_t {
   OP_ATTENTION = 8,    // per (sequence, head) softmax(QK^T/8) V (K9)
   OP_SOFTMAX = 9,      // in-place fp32 row softmax (K11)
   OP_SPLITK_FINAL = 10, // split-K reduction epilogue
-  OP_COPY = 11         // 16-B vector copy (request input -> workspace, so TMA can read it)
+  OP_COPY = 11,        // 16-B vector copy (request input -> workspace, so TMA can read it)
+  OP_PACK = 12         // request input -> workspace re-layout for small-C convs (k = 0: space-to-depth 2x2,
+                       //   k = 1: the KW horizontal taps packed into channels)
 };
 
 enum BufKind : int32_t { BUF_NONE = 0, BUF_WS = 1, BUF_IN = 2, BUF_OUT = 3, BUF_ABS = 4 };
@@ -46,7 +48,7 @@ struct Gather {
   int32_t KH, KW, stride, pad;
   int32_t Ho, Wo;             // rows = n_img * Ho * Wo
   int32_t rows;               // total rows of this operand (M or N)
-  int32_t pad_;
+  int32_t padw;               // padding along W (pad is along H)
 };
 
 struct Epilogue {
@@ -159,7 +161,8 @@ struct ExecParams {
   uint64_t* trace;              // optional: %globaltimer at program start and after every step
   int32_t trace_cap;
   int32_t dbg_flags;            // tuning experiments only (0 in production): 1 epilogue skips bias/act/stores,
-                                //   2 epilogue skips global stores, 4 MMA issues no UMMA, 8 producer issues no loads
+                                //   2 epilogue skips global stores, 4 MMA issues no UMMA, 8 producer issues no loads,
+                                //   16 MMA skips tcgen05.fence::after_thread_sync after full-barrier waits
   int32_t tl_cap;               // optional per-CTA tile timeline of step 0 (tuning tool): tl[cta * tl_cap + 4 * i + k]
   uint64_t* tl;                 //   k = 0 MMA start (accumulator acquired), 1 MMA last commit, 2 epilogue start, 3 epilogue end
 };
@@ -172,6 +175,8 @@ constexpr int kRingBytes = kStages * (kStageBytesA + kStageBytesB);  // GEMM sme
 constexpr int kMaxStages = 8;   // GEMM ring depth: kRingBytes / (A + B stage bytes), at most 8
 constexpr int kEpiRowBytes = 80;                   // 32 bf16 + 16 B pad per staged row
 constexpr int kEpiStageBytes = 8 * 32 * kEpiRowBytes;  // 8 epilogue warps x (32 rows x 32 columns)
-constexpr int kSmemBytes = kRingBytes + 1024 + kEpiStageBytes;  // + barriers
+constexpr int kOpCache = 8;     // GEMM args of the first 8 ops of a step are cached in shared memory
+constexpr int kOpCacheBytes = kOpCache * (int)sizeof(GemmArgs) + 64;
+constexpr int kSmemBytes = kRingBytes + 1024 + kEpiStageBytes + kOpCacheBytes;  // + barriers
 
 }  // namespace gl

@@ -867,51 +867,32 @@ gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completio
 
 gl_status gl_profile(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32_t warmup, int32_t reps,
                      const void* in_dev, void* out_dev, double* median_us) {
+  // Service latency as the frontend sees it: one batch in
+  // flight; submit -> its completion record visible to gl_poll (host clock).
   if (!ctx || !median_us || reps < 1 || warmup < 0) return fail(GL_E_ARG, "gl_profile: bad arguments");
   std::vector<double> lat;
-  const int total = warmup + reps;
-  uint64_t last = 0;
-  for (int i = 0; i < total; ++i) {
+  for (int i = 0; i < warmup + reps; ++i) {
     uint64_t t;
-    gl_status s;
-    while ((s = gl_submit_batch(ctx, gid, mid, in_dev, out_dev, batch, 0.f, &t)) == GL_E_QUEUE_FULL) {
-      gl_completion c[64];
-      int n = collect(ctx, c, 64);
-      for (int k = 0; k < n; ++k) ctx->stash.push_back(c[k]);
-    }
+    const gl_status s = gl_submit_batch(ctx, gid, mid, in_dev, out_dev, batch, 0.f, &t);
     if (s) return s;
-    last = t;
-    (void)last;
-  }
-  // collect everything we submitted
-  int got = 0;
-  auto t0 = std::chrono::steady_clock::now();
-  std::vector<gl_completion> mine;
-  while (got < total) {
-    gl_completion c[64];
-    int n = collect(ctx, c, 64);
-    for (int k = 0; k < n; ++k) {
-      if (c[k].gpulet == gid && c[k].model == mid) {
-        mine.push_back(c[k]);
-        ++got;
-      } else {
-        ctx->stash.push_back(c[k]);
+    const uint64_t t_sub = now_ns();
+    const auto t0 = std::chrono::steady_clock::now();
+    bool done = false;
+    while (!done) {
+      gl_completion c[64];
+      const int n = collect(ctx, c, 64);
+      for (int k = 0; k < n; ++k) {
+        if (c[k].ticket == t) {
+          done = true;
+          if (i >= warmup) lat.push_back((now_ns() - t_sub) / 1000.0);
+        } else {
+          ctx->stash.push_back(c[k]);
+        }
       }
+      if (!done && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        return fail(GL_E_TIMEOUT, "gl_profile: timeout");
     }
-    for (auto it = ctx->stash.begin(); it != ctx->stash.end() && got < total;) {
-      if (it->gpulet == gid && it->model == mid) {
-        mine.push_back(*it);
-        ++got;
-        it = ctx->stash.erase(it);
-      } else {
-        ++it;
-      }
-    }
-    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) return fail(GL_E_TIMEOUT, "gl_profile: timeout");
-    if (!n) std::this_thread::yield();
   }
-  std::sort(mine.begin(), mine.end(), [](const gl_completion& a, const gl_completion& b) { return a.ticket < b.ticket; });
-  for (size_t i = warmup; i < mine.size(); ++i) lat.push_back((mine[i].t_end_ns - mine[i].t_start_ns) / 1000.0);
   std::sort(lat.begin(), lat.end());
   *median_us = lat[lat.size() / 2];
   return GL_OK;

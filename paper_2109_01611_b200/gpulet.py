@@ -49,7 +49,9 @@ class Lane(ctypes.Structure):
     _fields_ = [("gpulet", ctypes.c_int32), ("model_id", ctypes.c_int32), ("model_slot", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("duty_us", ctypes.c_int32), ("weight", ctypes.c_int32),
                 ("drop_us", ctypes.c_int32), ("pad_", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
-                ("out_dev", ctypes.c_void_p)]
+                ("out_dev", ctypes.c_void_p), ("in_host", ctypes.c_void_p), ("out_host", ctypes.c_void_p),
+                ("in_req_bytes", ctypes.c_int64), ("out_req_bytes", ctypes.c_int64), ("host_slots", ctypes.c_int32),
+                ("pad2_", ctypes.c_int32)]
 
 
 _lib = None
@@ -81,7 +83,8 @@ def lib():
             "gl_program_info": [P, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(D),
                                 ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
             "gl_serve": [P, ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
-                         ctypes.POINTER(I32), ctypes.POINTER(I64)],
+                         ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(U64), ctypes.POINTER(I64),
+                         ctypes.POINTER(I64)],
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
@@ -227,23 +230,34 @@ class Context:
             rl.append([(v - ts[s]) if v else None for v in st])
         return durs, rl
 
-    def serve(self, lanes, n_models, arr_us, arr_model, slo_us):
+    def serve(self, lanes, n_models, arr_us, arr_model, slo_us, stats=False):
         """gl_serve: lanes = list of dicts (gpulet, model_id, model_slot, batch, duty_us,
-        weight, drop_us, x, y); returns per-request latency (us, -1 dropped)."""
+        weight, drop_us, x, y[, x_host, y_host, in_req_bytes, out_req_bytes, host_slots]);
+        returns per-request latency (us, -1 dropped), and with stats also
+        {"dev_ns": (first dequeue, last end), "h2d_bytes", "d2h_bytes"}."""
         import numpy as np
         L = (Lane * len(lanes))()
         for i, d in enumerate(lanes):
             L[i].gpulet, L[i].model_id, L[i].model_slot = d["gpulet"], d["model_id"], d["model_slot"]
             L[i].batch, L[i].duty_us, L[i].weight, L[i].drop_us = d["batch"], d["duty_us"], d["weight"], d["drop_us"]
             L[i].in_dev, L[i].out_dev = _ptr(d["x"]), _ptr(d["y"])
+            if d.get("x_host") is not None:
+                L[i].in_host, L[i].out_host = _ptr(d["x_host"]), _ptr(d["y_host"])
+                L[i].in_req_bytes, L[i].out_req_bytes = d["in_req_bytes"], d["out_req_bytes"]
+                L[i].host_slots = d["host_slots"]
         a = np.ascontiguousarray(arr_us, dtype=np.int64)
         m = np.ascontiguousarray(arr_model, dtype=np.int32)
         s = np.ascontiguousarray(slo_us, dtype=np.int32)
         out = np.zeros(len(a), dtype=np.int64)
+        dev = (ctypes.c_uint64 * 2)()
+        hb, db = ctypes.c_int64(), ctypes.c_int64()
         _check(lib().gl_serve(self.h, L, len(lanes), n_models, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                               m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
                               s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), dev, ctypes.byref(hb),
+                              ctypes.byref(db)))
+        if stats:
+            return out, {"dev_ns": (dev[0], dev[1]), "h2d_bytes": hb.value, "d2h_bytes": db.value}
         return out
 
     def program_info(self, mid, batch, cap=1024):

@@ -69,14 +69,16 @@ CONV_CASES = [(2, 14, 14, 64, 128, 3, 1, 1), (1, 30, 30, 8, 64, 7, 2, 3), (2, 9,
               (1, 56, 56, 64, 64, 3, 1, 1), (2, 28, 28, 128, 128, 3, 2, 1), (2, 10, 10, 256, 512, 3, 2, 1),
               (3, 7, 7, 512, 256, 1, 1, 0), (2, 5, 5, 128, 64, 5, 1, 2), (2, 14, 14, 96, 128, 3, 1, 1),
               (1, 14, 14, 24, 64, 5, 1, 2), (2, 7, 7, 160, 320, 3, 1, 1), (2, 28, 28, 48, 128, 5, 1, 2),
-              (4, 32, 32, 8, 64, 3, 1, 1)]
+              (4, 32, 32, 8, 64, 3, 1, 1), (2, 32, 32, 8, 64, 7, 2, 3), (2, 30, 30, 8, 32, 3, 2, 1)]
 
 
-@pytest.mark.parametrize("in_ws", [0, 1])
+@pytest.mark.parametrize("in_ws", [0, 1, 2])
 @pytest.mark.parametrize("N,H,W,C,Co,k,s,p", CONV_CASES)
 def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p, in_ws):
     """in_ws=0: cp.async implicit-im2col gather (forced by tuning key 4);
-    in_ws=1: TMA (2-D for 1x1/s1, im2col boxes of 64/32/16/8 channels otherwise)."""
+    in_ws=1: TMA (2-D for 1x1/s1, im2col boxes of 64/32/16/8 channels otherwise);
+    in_ws=2: input at the request address, staged into the workspace by the
+    program (copy, 2x2 space-to-depth or kw-packing for small-C convs)."""
     import torch
     from paper_2109_01611_b200 import gpulet
     r = np.random.default_rng(H * C + Co)
@@ -85,9 +87,9 @@ def test_conv_vs_oracle(ctx, N, H, W, C, Co, k, s, p, in_ws):
     b = _bf16(r, (Co,), 0.05)
     Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
     y = torch.empty((N, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
-    gpulet.Context.set_tuning(4, 1 - in_ws)
+    gpulet.Context.set_tuning(4, 1 if in_ws == 0 else 0)
     try:
-        ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1, in_ws=in_ws)
+        ctx.test_conv(0, to_dev_bf16(x), w, b, y, N, H, W, C, Co, k, s, p, act=1, in_ws=1 if in_ws == 1 else 0)
     finally:
         gpulet.Context.set_tuning(4, 0)
     torch.cuda.synchronize()
