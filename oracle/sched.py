@@ -96,6 +96,19 @@ class Scheduler:
                 best = b
         return best
 
+    def b_int(self, m, p, A):
+        """Interference-aware batch (reading R13, P:532-537 / P:594: "the maximum
+        batch size b is decided and checked whether it can meet the SLO when there
+        is the additional interference-induced overhead"): the largest b <= b_sat
+        with 2 Leff(b, F(b)) <= SLO_m, or None.  Equals b_sat without interference."""
+        b0 = self.b_sat(m, p)
+        if b0 is None:
+            return None
+        for b in range(b0, 0, -1):
+            if 2 * self.leff(m, b, p, self.factor(m, b, p, A)) <= self.slo[m]:
+                return b
+        return None
+
     def cap(self, m, p, F=1000):
         b = self.b_sat(m, p)
         if b is None:
@@ -155,9 +168,9 @@ class Scheduler:
         p = g.size if size is None else size
         if len(lanes) == 1:
             ln = lanes[0]
-            b = self.b_sat(ln.m, p)
             if check_only_batches:        # stats lookup only: never fails
-                return [(ln, b or 1)]
+                return [(ln, self.b_sat(ln.m, p) or 1)]
+            b = self.b_int(ln.m, p, A)
             if b is None:
                 return None
             F = self.factor(ln.m, b, p, A)
@@ -168,7 +181,7 @@ class Scheduler:
         # k >= 2 lanes: Nexus-style merge
         Ds = []
         for ln in lanes:
-            b = self.b_sat(ln.m, p)
+            b = self.b_sat(ln.m, p) if check_only_batches else self.b_int(ln.m, p, A)
             if b is None:
                 if check_only_batches:
                     return [(l2, 1) for l2 in lanes]
@@ -275,12 +288,12 @@ class Scheduler:
             if g.size == 100 and p_ideal < 100 and not self.fixed:
                 t, s = self._split(g, p_ideal)                  # Split
                 si = (g, t, s)
-            b = self.b_sat(m, t.size)                           # b = argmax_k 2L <= SLO
+            A = self.aggregate(self.sibling(t))
+            b = self.b_int(m, t.size, A)                        # max b: 2 (L + intf) <= SLO
             ok = b is not None
             if ok:
-                F = self.factor(m, b, t.size, self.aggregate(self.sibling(t)))
+                F = self.factor(m, b, t.size, A)
                 e = self.leff(m, b, t.size, F)
-                ok = 2 * e <= self.slo[m]                       # L + intf <= SLO
             if ok:
                 r = min(R, b * 1_000_000 // e)
                 t.lanes = [Lane(m, r)]

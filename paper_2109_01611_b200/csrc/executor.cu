@@ -161,34 +161,32 @@ __device__ __forceinline__ void add_bf16x8(float* v, const uint4& u) {
 // `nfull` full 32-column chunks starting at output column n00 (bf16 row-major
 // output): TMEM -> registers, + bias (+ residual) -> ACT -> bf16.  Rows are
 // staged in shared memory so that residual loads and output stores move 16 B
-// per lane with four lanes per 64-B row segment.
+// per lane with four lanes per 64-B row segment.  The caller loaded the bias
+// (lane l of chunk j holds column n00 + 32 j + l in bl[j]) and issued chunk 0's
+// residual copy before the accumulator was ready; chunk j + 1's residual is
+// requested while chunk j's TMEM load is in flight.
 template <int ACT, bool RES>
 __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, const Ctx& X, uint32_t taddr,
-                                         int row0, int n00, int nfull, uint8_t* stg, int lane, bool nostore) {
-  const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+                                         int row0, int n00, int nfull, uint8_t* stg, int lane, bool nostore,
+                                         const float* bl, bool has_bias) {
   const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
   __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
   const int sr = lane >> 2, seg = lane & 3;
   const int64_t ldc = e.ldc;
   const int64_t coff = e.col_off;
+  const int M = g.M;
+#pragma unroll 1
   for (int j = 0; j < nfull; ++j) {
     const int n0 = n00 + j * 32;
-    if (RES) {
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int r = it * 8 + sr;
-        const bool ok = row0 + r < g.M;
-        const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n0 + seg * 8 : rsd;
-        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
-      }
-      cp_async_commit();
-    }
     float v[32];
     tmem_ld32(taddr + j * 32, v);
-    if (bias) {
-      const uint4* bp = (const uint4*)(bias + n0);
+    if (has_bias) {
+      float bj = 0.f;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, __ldg(bp + k));
+      for (int q = 0; q < 8; ++q)
+        if (q == j) bj = bl[q];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] += __shfl_sync(0xffffffffu, bj, c);
     }
     if (RES) {
       cp_async_wait<0>();
@@ -207,10 +205,20 @@ __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, c
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const int r = it * 8 + sr;
-      if (row0 + r < g.M && !nostore)
+      if (row0 + r < M && !nostore)
         *(uint4*)(outp + (row0 + r) * ldc + coff + n0 + seg * 8) = *(const uint4*)(stg + r * kEpiRowBytes + seg * 16);
     }
     __syncwarp();
+    if (RES && j + 1 < nfull) {
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int r = it * 8 + sr;
+        const bool ok = row0 + r < M;
+        const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n0 + 32 + seg * 8 : rsd;
+        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
+      }
+      cp_async_commit();
+    }
   }
 }
 
@@ -356,12 +364,40 @@ __device__ __forceinline__ uint32_t stage_bytes_for(int bn) {
 }
 
 // Epilogue of one warp over the tile columns [c0, c1) (relative to the tile).
+// Waits for the accumulator itself (tfull / parity) after issuing the loads
+// that do not depend on it (bias, first residual chunk).
 __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, const Smem& S, uint32_t taddr, int mb,
-                                              int nb, int kb0, int q, int c0, int c1, uint8_t* stg, int lane) {
+                                              int nb, int kb0, int q, int c0, int c1, uint8_t* stg, int lane,
+                                              uint64_t* tfull, uint32_t parity) {
   const Epilogue& e = g.ep;
   const int m = mb * 128 + q * 32 + lane;
   const int nend = min(g.N, (nb + 1) * g.BN);
   c1 = min(c1, nend - nb * g.BN);
+  const bool fast = !(S.flags & 1) && e.splitk <= 1 && !e.transpose && !e.out_fp32 && e.rows_per_img >= g.M &&
+                    (e.ldc % 8) == 0 && (e.col_off % 8) == 0 && c1 > c0;
+  const int nfull = fast ? min(8, (c1 - c0) / 32) : 0;
+  float bl[8];
+  const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
+  const bool rs = e.res.kind != BUF_NONE;
+  const int row0 = mb * 128 + q * 32, n00 = nb * g.BN + c0;
+  if (nfull > 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bl[j] = (bias && j < nfull) ? __bfloat162float(bias[n00 + 32 * j + lane]) : 0.f;
+    if (rs) {
+      const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
+      const int sr = lane >> 2, seg = lane & 3;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int r = it * 8 + sr;
+        const bool ok = row0 + r < g.M;
+        const __nv_bfloat16* src = ok ? rsd + (int64_t)(row0 + r) * e.ldc + e.col_off + n00 + seg * 8 : rsd;
+        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
+      }
+      cp_async_commit();
+    }
+  }
+  mbar_wait(tfull, parity);
+  tc_fence_after();
   if (c1 <= c0) return;
   int j0 = c0;   // first column (within the tile) not yet stored
   if (S.flags & 1) {
@@ -400,22 +436,20 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
     }
     return;
   }
-  if (!e.transpose && !e.out_fp32 && e.rows_per_img >= g.M && (e.ldc % 8) == 0 && (e.col_off % 8) == 0) {
+  if (nfull > 0) {
     // bf16 row-major output: warp-collective staged epilogue on the full 32-column chunks
-    const int nfull = (c1 - c0) / 32;
-    const bool rs = e.res.kind != BUF_NONE;
-    const int row0 = mb * 128 + q * 32, n00 = nb * g.BN + c0;
     const uint32_t ta = taddr + c0;
     const bool ns = (S.flags & 2) != 0;
+    const bool hb = bias != nullptr;
     switch (e.act * 2 + (rs ? 1 : 0)) {
-      case 0: epi_rows<ACT_NONE, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 1: epi_rows<ACT_NONE, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 2: epi_rows<ACT_RELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 3: epi_rows<ACT_RELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 4: epi_rows<ACT_GELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 5: epi_rows<ACT_GELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      case 6: epi_rows<ACT_TANH, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
-      default: epi_rows<ACT_TANH, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns); break;
+      case 0: epi_rows<ACT_NONE, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 1: epi_rows<ACT_NONE, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 2: epi_rows<ACT_RELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 3: epi_rows<ACT_RELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 4: epi_rows<ACT_GELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 5: epi_rows<ACT_GELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 6: epi_rows<ACT_TANH, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      default: epi_rows<ACT_TANH, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
     }
     j0 = c0 + nfull * 32;
   }
@@ -650,18 +684,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
       const uint32_t acc = P.acc & 1, use = P.acc >> 1;
-      {
-        // bias lines of this tile -> L1 while the accumulator is still being computed
-        const char* bias = (const char*)res(g.ep.bias, X);
-        const int bn = g.ep.bias_on_m ? mb * 128 : nb * g.BN;
-        const int nbytes = (g.ep.bias_on_m ? 128 : g.BN) * 2;
-        if (bias && lane * 128 < nbytes) prefetch_l1(bias + bn * 2 + lane * 128);
-      }
-      mbar_wait(&S.tfull[acc], use & 1);
-      tc_fence_after();
       const bool lead = q == 0 && half == 0 && lane == 0;
-      if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
-      if (lead) tl_mark(S, ntile, 2);
       const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * 256;
       int c0 = 0, c1 = g.BN;
       if (!gstep) {
@@ -669,7 +692,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         c0 = half ? split : 0;
         c1 = half ? g.BN : split;
       }
-      epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane);
+      if (lead) tl_mark(S, ntile, 2);
+      if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
+      epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane, &S.tfull[acc], use & 1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cnt(&S.tempty[acc], arrive_n);
@@ -753,9 +778,8 @@ __device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u <<
 __device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
 template <int STRIDE, int STRIP>
-__device__ __forceinline__ void dw_item(const MiscArgs& a, const __nv_bfloat16* __restrict__ x, const uint4 (&wv)[9],
-                                        const uint4& bv, __nv_bfloat16* __restrict__ y, int n, int ho, int wo0,
-                                        int cg) {
+__device__ __forceinline__ void dw_item(const MiscArgs& a, const __nv_bfloat16* __restrict__ x, const float* __restrict__ wsm,
+                                        __nv_bfloat16* __restrict__ y, int n, int ho, int wo0, int cg) {
   constexpr int NCOL = (STRIP - 1) * STRIDE + 3;
   uint4 xin[3][NCOL];
   const int wi0 = wo0 * STRIDE - a.pad;
@@ -772,26 +796,28 @@ __device__ __forceinline__ void dw_item(const MiscArgs& a, const __nv_bfloat16* 
     }
   }
   float acc[STRIP][8];
-  const uint32_t* bw = (const uint32_t*)&bv;
+  {
+    const float4 b0 = *(const float4*)(wsm + 9 * a.C + cg * 8), b1 = *(const float4*)(wsm + 9 * a.C + cg * 8 + 4);
 #pragma unroll
-  for (int o = 0; o < STRIP; ++o)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      acc[o][2 * c] = bf_lo(bw[c]);
-      acc[o][2 * c + 1] = bf_hi(bw[c]);
+    for (int o = 0; o < STRIP; ++o) {
+      acc[o][0] = b0.x, acc[o][1] = b0.y, acc[o][2] = b0.z, acc[o][3] = b0.w;
+      acc[o][4] = b1.x, acc[o][5] = b1.y, acc[o][6] = b1.z, acc[o][7] = b1.w;
     }
+  }
 #pragma unroll
   for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
     for (int kw = 0; kw < 3; ++kw) {
-      const uint32_t* ww = (const uint32_t*)&wv[kh * 3 + kw];
+      const float4 w0 = *(const float4*)(wsm + (kh * 3 + kw) * a.C + cg * 8);
+      const float4 w1 = *(const float4*)(wsm + (kh * 3 + kw) * a.C + cg * 8 + 4);
+      const float wf[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
       for (int o = 0; o < STRIP; ++o) {
         const uint32_t* xx = (const uint32_t*)&xin[kh][o * STRIDE + kw];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          acc[o][2 * c] = fmaf(bf_lo(xx[c]), bf_lo(ww[c]), acc[o][2 * c]);
-          acc[o][2 * c + 1] = fmaf(bf_hi(xx[c]), bf_hi(ww[c]), acc[o][2 * c + 1]);
+          acc[o][2 * c] = fmaf(bf_lo(xx[c]), wf[2 * c], acc[o][2 * c]);
+          acc[o][2 * c + 1] = fmaf(bf_hi(xx[c]), wf[2 * c + 1], acc[o][2 * c + 1]);
         }
       }
     }
@@ -806,39 +832,38 @@ __device__ __forceinline__ void dw_item(const MiscArgs& a, const __nv_bfloat16* 
 }
 
 template <int STRIDE, int STRIP>
-__device__ __forceinline__ void dw_loop(const MiscArgs& a, const __nv_bfloat16* x, const __nv_bfloat16* w,
-                                        const __nv_bfloat16* b, __nv_bfloat16* y) {
+__device__ __forceinline__ void dw_loop(const MiscArgs& a, const __nv_bfloat16* x, const float* wsm,
+                                        __nv_bfloat16* y) {
   const int CG = a.C / 8, WS = (a.Wo + STRIP - 1) / STRIP;
   const int total = a.N * a.Ho * WS * CG;
   const int stride_t = gridDim.x * blockDim.x;
-  int cg_cached = -1;
-  uint4 wv[9], bv = make_uint4(0u, 0u, 0u, 0u);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride_t) {
     const int cg = i % CG;
     int p = i / CG;
     const int ws = p % WS;
     p /= WS;
     const int ho = p % a.Ho, n = p / a.Ho;
-    if (cg != cg_cached) {
-      cg_cached = cg;
-#pragma unroll
-      for (int t = 0; t < 9; ++t) wv[t] = __ldg((const uint4*)(w + t * a.C + cg * 8));
-      bv = __ldg((const uint4*)(b + cg * 8));
-    }
-    dw_item<STRIDE, STRIP>(a, x, wv, bv, y, n, ho, ws * STRIP, cg);
+    dw_item<STRIDE, STRIP>(a, x, wsm, y, n, ho, ws * STRIP, cg);
   }
 }
 
-__device__ __noinline__ void dwconv(const OpDesc* op, const Ctx& X) {
+// Weights ([9][C] tap-major) and bias are expanded to fp32 in shared memory
+// once per CTA (the GEMM ring is idle during this step).
+__device__ __noinline__ void dwconv(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
   const MiscArgs& a = op->m;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
-  const __nv_bfloat16* w = (const __nv_bfloat16*)res(a.w, X);   // [9][C] tap-major
+  const __nv_bfloat16* w = (const __nv_bfloat16*)res(a.w, X);
   const __nv_bfloat16* b = (const __nv_bfloat16*)res(a.b, X);
   __nv_bfloat16* y = (__nv_bfloat16*)res(a.y, X);
+  float* wsm = (float*)scratch;   // [9][C] weights then [C] bias
+  for (int i = threadIdx.x; i < 10 * a.C; i += blockDim.x)
+    wsm[i] = __bfloat162float(i < 9 * a.C ? w[i] : b[i - 9 * a.C]);
+  __syncthreads();
   if (a.stride == 1)
-    dw_loop<1, 4>(a, x, w, b, y);
+    dw_loop<1, 2>(a, x, wsm, y);
   else
-    dw_loop<2, 2>(a, x, w, b, y);
+    dw_loop<2, 2>(a, x, wsm, y);
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ max pool (K6)
@@ -1347,7 +1372,7 @@ __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P)
     return;
   }
   switch (op->type) {
-    case OP_DWCONV: dwconv(op, X); break;
+    case OP_DWCONV: dwconv(op, X, S.scratch); break;
     case OP_MAXPOOL: maxpool(op, X); break;
     case OP_AVGPOOL: avgpool(op, X); break;
     case OP_LENET: lenet(op, X, S.scratch); break;
@@ -1389,7 +1414,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
 
 }  // namespace
 
-extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams p) {
+extern "C" __global__ void __maxnreg__(200) gl_executor(ExecParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem S;

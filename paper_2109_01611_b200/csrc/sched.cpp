@@ -140,6 +140,15 @@ class Sched {
     return f < 1000.0 ? 1000 : (int)f;
   }
 
+  // Interference-aware batch (reading R13, P:532-537 / P:594): the largest
+  // b <= b_sat with 2 Leff(b, F(b)) <= SLO, 0 if none; = b_sat without interference.
+  int bint(int m, int p, const Agg& A) const {
+    const int b0 = bsat(m, p);
+    for (int b = b0; b >= 1; --b)
+      if (2 * leff(m, b, p, factor(m, b, p, A)) <= in.slo_us[m]) return b;
+    return 0;
+  }
+
   // Interference-free batches of a lane set (for the partner aggregate).
   void batches(const std::vector<Lane>& lanes, int p, std::vector<int>& out) const {
     out.clear();
@@ -187,7 +196,7 @@ class Sched {
     recs.clear();
     if (lanes.size() == 1) {
       const Lane& ln = lanes[0];
-      const int b = bsat(ln.m, p);
+      const int b = bint(ln.m, p, A);
       if (!b) return false;
       const int F = factor(ln.m, b, p, A);
       const int64_t e = leff(ln.m, b, p, F);
@@ -198,7 +207,7 @@ class Sched {
     }
     D = -1;
     for (const Lane& ln : lanes) {
-      const int b = bsat(ln.m, p);
+      const int b = bint(ln.m, p, A);
       if (!b) return false;
       const int64_t d = leff(ln.m, b, p, factor(ln.m, b, p, A));
       D = D < 0 ? d : std::min(D, d);
@@ -279,13 +288,13 @@ class Sched {
         s = add(pool[g].gpu, 1, 100 - pideal, 0);
         split = true;
       }
-      const int b = bsat(m, pool[t].size);
+      const Agg A = aggregate(sibling(t));
+      const int b = bint(m, pool[t].size, A);  // max b: 2 (L + intf) <= SLO
       bool ok = b > 0;
       int64_t e = 0;
       if (ok) {
-        const int F = factor(m, b, pool[t].size, aggregate(sibling(t)));
+        const int F = factor(m, b, pool[t].size, A);
         e = leff(m, b, pool[t].size, F);
-        ok = 2 * e <= in.slo_us[m];  // L + intf <= SLO
       }
       if (ok) {
         r = std::min<int64_t>(R, (int64_t)b * 1000000 / e);

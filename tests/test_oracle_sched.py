@@ -325,3 +325,20 @@ def test_soundness_replay(mode):
             assert s["violations"] == 0, (mode, m, s["late"], s["dropped"], plan.dump)
         checked += 1
     assert checked >= 5
+
+
+def test_interference_aware_batch_is_maximal():
+    """Reading R13: with a partner the batch is the largest
+    b <= b_sat whose interference-inflated latency still fits the duty-cycle
+    rule 2 Leff <= SLO; a zero-slack b_sat (SLO = 2 L(32)) must shrink."""
+    P = prof_from([W2])
+    slo = [2 * P.L(0, 32, 100)]
+    S = sched.Scheduler(P, slo, (0.0, 0.0, 0.0, 0.0, 1.2), "gpulet+int")
+    A = (0.5, 0.5)
+    for p in (40, 60, 100):
+        b0 = S.b_sat(0, p)
+        b = S.b_int(0, p, A)
+        assert b is not None and b < b0
+        assert 2 * S.leff(0, b, p, S.factor(0, b, p, A)) <= slo[0]
+        assert 2 * S.leff(0, b + 1, p, S.factor(0, b + 1, p, A)) > slo[0]
+        assert S.b_int(0, p, None) == b0          # no partner: solo b_sat

@@ -61,10 +61,12 @@ def _inst(rnd, M):
     return P, [2 * P.L(m, 32, 100) for m in range(M)]
 
 
+@pytest.mark.parametrize("c", [(0.12, 0.08, 0.21, 0.17, 0.97), (0.068, 0.097, -1.42, 0.71, 1.05)])
 @pytest.mark.parametrize("mode", ["gpulet", "gpulet+int", "sbp", "ideal"])
-def test_random_instances_identical(mode):
+def test_random_instances_identical(mode, c):
+    """Second coefficient set: the shape of the B200 fit (c5 > 1, negative c3),
+    where the interference-aware batch drops below b_sat."""
     rnd = random.Random(hash(mode) % 1000)
-    c = (0.12, 0.08, 0.21, 0.17, 0.97)
     n = 0
     for _ in range(300 if mode != "ideal" else 40):
         M, N = rnd.randint(1, 6), rnd.randint(1, 4 if mode != "ideal" else 2)
