@@ -93,20 +93,27 @@ __device__ __forceinline__ void advance(Pipe& p) {
 __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    // release-add (orders this CTA's prior writes, made visible CTA-wide by the
+    // __syncthreads above), then acquire-poll: tight for the first ~1 us, then
+    // with a short back-off (idle executors wait here for work)
     const unsigned long long target = (unsigned long long)(epoch + 1) * gridDim.x;
-    atomicAdd(&st->barrier, 1ull);
-    uint64_t t0 = may_idle ? 0 : globaltimer();
-    uint32_t ns = 32;
+    red_release_gpu_add_u64((unsigned long long*)&st->barrier, 1ull);
+    uint32_t spins = 0, ns = 32;
+    uint64_t t0 = 0;
     while (ld_acquire_gpu_u64((volatile uint64_t*)&st->barrier) < target) {
+      if (++spins < 256) continue;
       __nanosleep(ns);
       if (ns < 256) ns <<= 1;
-      if (!may_idle && globaltimer() - t0 > 20ull * 1000000000ull) __trap();
+      if (!may_idle) {
+        if (t0 == 0) t0 = globaltimer();
+        else if (globaltimer() - t0 > 20ull * 1000000000ull) __trap();
+      }
     }
-    __threadfence();
   }
   ++epoch;
   __syncthreads();
+  // the next step's TMA (async proxy) reads what other CTAs stored (generic proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ epilogue helpers
@@ -946,61 +953,75 @@ __device__ __noinline__ void avgpool(const OpDesc* op, const Ctx& X) {
 __device__ __forceinline__ float bfr(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
 __device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+  // One CTA per image (grid-stride); the packed bf16 parameters (123 KB) are
+  // staged in shared memory once per CTA, activations stay in shared memory
+  // in fp32 (rounded to bf16 where the oracle rounds: after each ReLU, C1.4).
   const MiscArgs& a = op->m;
+  if ((int)blockIdx.x >= a.N) return;
   const __nv_bfloat16* x = (const __nv_bfloat16*)res(a.x, X);
-  const __nv_bfloat16* W = (const __nv_bfloat16*)res(a.w, X);  // packed params in manifest order
+  const __nv_bfloat16* Wg = (const __nv_bfloat16*)res(a.w, X);  // packed params in manifest order
   float* y = (float*)res(a.y, X);
+  constexpr int kParams = 61706, kParamVec = (kParams + 7) / 8;
+  __nv_bfloat16* W = (__nv_bfloat16*)scratch;
+  for (int i = threadIdx.x; i < kParamVec; i += blockDim.x) ((uint4*)W)[i] = __ldg((const uint4*)Wg + i);
   const __nv_bfloat16 *w1 = W, *b1 = w1 + 150, *w2 = b1 + 6, *b2 = w2 + 2400, *f1 = b2 + 16, *fb1 = f1 + 48000,
                       *f2 = fb1 + 120, *fb2 = f2 + 10080, *f3 = fb2 + 84, *fb3 = f3 + 840;
-  float* img = (float*)scratch;   // 28*28
-  float* p1 = img + 784;          // 14*14*6
-  float* p2 = p1 + 1176;          // 5*5*16
+  float* img = (float*)(scratch + kParamVec * 16);   // 28*28
+  float* c1 = img + 784;          // 28*28*6 pre-pool (relu, bf16-rounded)
+  float* p1 = c1 + 4704;          // 14*14*6
+  float* c2 = p1 + 1176;          // 10*10*16 pre-pool
+  float* p2 = c2 + 1600;          // 5*5*16 (NHWC flatten)
   float* h1 = p2 + 400;           // 120
   float* h2 = h1 + 120;           // 84
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int n = blockIdx.x; n < a.N; n += gridDim.x) {
     for (int i = threadIdx.x; i < 784; i += blockDim.x) img[i] = __bfloat162float(x[(int64_t)n * 784 + i]);
     __syncthreads();
-    for (int i = threadIdx.x; i < 1176; i += blockDim.x) {   // conv1 5x5 pad 2 + relu + bf16 + maxpool2
+    for (int i = threadIdx.x; i < 4704; i += blockDim.x) {   // conv1 5x5 pad 2 + relu + bf16
+      const int co = i % 6, ox = (i / 6) % 28, oy = i / 168;
+      float s = __bfloat162float(b1[co]);
+#pragma unroll
+      for (int kh = 0; kh < 5; ++kh) {
+        const int iy = oy + kh - 2;
+        if (iy < 0 || iy >= 28) continue;
+#pragma unroll
+        for (int kw = 0; kw < 5; ++kw) {
+          const int ix = ox + kw - 2;
+          if (ix < 0 || ix >= 28) continue;
+          s = fmaf(img[iy * 28 + ix], __bfloat162float(w1[co * 25 + kh * 5 + kw]), s);
+        }
+      }
+      c1[i] = bfr(fmaxf(s, 0.f));   // index (oy*28 + ox)*6 + co
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 1176; i += blockDim.x) {   // maxpool 2x2
       const int co = i % 6, px = (i / 6) % 14, py = i / 84;
-      float m = -INFINITY;
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-          const int oy = 2 * py + dy, ox = 2 * px + dx;
-          float s = __bfloat162float(b1[co]);
-          for (int kh = 0; kh < 5; ++kh) {
-            const int iy = oy + kh - 2;
-            if (iy < 0 || iy >= 28) continue;
-            for (int kw = 0; kw < 5; ++kw) {
-              const int ix = ox + kw - 2;
-              if (ix < 0 || ix >= 28) continue;
-              s = fmaf(img[iy * 28 + ix], __bfloat162float(w1[co * 25 + kh * 5 + kw]), s);
-            }
-          }
-          m = fmaxf(m, bfr(fmaxf(s, 0.f)));
-        }
-      p1[i] = m;   // index (py*14 + px)*6 + co
+      const float* q = c1 + ((2 * py) * 28 + 2 * px) * 6 + co;
+      p1[i] = fmaxf(fmaxf(q[0], q[6]), fmaxf(q[168], q[174]));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 400; i += blockDim.x) {    // conv2 5x5 (6->16) + relu + bf16 + maxpool2
+    for (int i = threadIdx.x; i < 1600; i += blockDim.x) {   // conv2 5x5 (6->16) + relu + bf16
+      const int co = i % 16, ox = (i / 16) % 10, oy = i / 160;
+      float s = __bfloat162float(b2[co]);
+      const __nv_bfloat16* wr = w2 + co * 150;
+#pragma unroll
+      for (int kh = 0; kh < 5; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < 5; ++kw) {
+          const float* pp = p1 + ((oy + kh) * 14 + ox + kw) * 6;
+#pragma unroll
+          for (int ci = 0; ci < 6; ++ci) s = fmaf(pp[ci], __bfloat162float(wr[(kh * 5 + kw) * 6 + ci]), s);
+        }
+      c2[i] = bfr(fmaxf(s, 0.f));   // index (oy*10 + ox)*16 + co
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 400; i += blockDim.x) {    // maxpool 2x2 -> NHWC flatten (h, w, c)
       const int co = i % 16, px = (i / 16) % 5, py = i / 80;
-      float m = -INFINITY;
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-          const int oy = 2 * py + dy, ox = 2 * px + dx;
-          float s = __bfloat162float(b2[co]);
-          for (int kh = 0; kh < 5; ++kh)
-            for (int kw = 0; kw < 5; ++kw)
-              for (int ci = 0; ci < 6; ++ci)
-                s = fmaf(p1[((oy + kh) * 14 + ox + kw) * 6 + ci],
-                         __bfloat162float(w2[((co * 5 + kh) * 5 + kw) * 6 + ci]), s);
-          m = fmaxf(m, bfr(fmaxf(s, 0.f)));
-        }
-      p2[i] = m;   // NHWC flatten (h, w, c)
+      const float* q = c2 + ((2 * py) * 10 + 2 * px) * 16 + co;
+      p2[i] = fmaxf(fmaxf(q[0], q[16]), fmaxf(q[160], q[176]));
     }
     __syncthreads();
-    // fully connected layers: one warp per output neuron, lanes stride over k
-    // (coalesced weight rows), shuffle reduction
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // fully connected layers: one warp per output neuron, lanes stride over k, shuffle reduction
     for (int j = warp; j < 120; j += nw) {
       float s = 0.f;
       for (int k = lane; k < 400; k += 32) s = fmaf(p2[k], __bfloat162float(f1[j * 400 + k]), s);
@@ -1414,7 +1435,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
 
 }  // namespace
 
-extern "C" __global__ void __maxnreg__(200) gl_executor(ExecParams p) {
+extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem S;

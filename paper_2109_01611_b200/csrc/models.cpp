@@ -667,6 +667,7 @@ static void build_lenet(Builder& B, size_t& in_b, size_t& out_b) {
       }
       buf.insert(buf.end(), it->second.data.begin(), it->second.data.end());
     }
+    buf.resize((buf.size() + 7) / 8 * 8, 0);   // whole 16-B vectors (staged into smem by the kernel)
     w = upload(B.dw, buf.data(), buf.size() * 2);
     B.dw.ptr[key] = w;
   }
