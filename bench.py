@@ -14,7 +14,9 @@ the measured B200 profile (profiles/profile_b200.csv); scenario rates are the
 paper's, scaled to B200, times a multiplier x.
 
 Method ("maximum achievable throughput"): x starts at the largest
-multiplier the native scheduler (Alg. 1, mode gpulet+int) accepts for N GPUs;
+multiplier the native scheduler (Alg. 1; headline mode gpulet, the paper's
+gpu-let scheduler without the interference check — DESIGN.md R22 — with
+gpulet+int reported beside it) accepts for N GPUs;
 the plan's gpu-lets are created (green contexts + persistent executors) and
 Poisson traffic is replayed in real time through the native frontend
 (gl_serve: smooth-WRR routing, duty-cycle batching, drops); x is bisected
@@ -436,7 +438,8 @@ def our_arm(a, world, rank, local, dist):
     head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, timed=True, clocks=True)
     extra = {}
     if not a.headline_only:
-        for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), ("gpulet_no_int", a.scenario, "gpulet"),
+        other = "gpulet+int" if a.mode == "gpulet" else "gpulet"
+        for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), (other.replace("+", "_"), a.scenario, other),
                                 ("mix6", "mix6", a.mode), ("mix6_baseline_sbp", "mix6", "sbp")):
             r = run_mode(srv, dist, rank, world, scen, mode, a, timed=False)
             extra[key] = {"value": round(r["value"], 2), "scenario": scen, "mode": mode,
@@ -480,7 +483,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="gpulet+int", choices=["gpulet", "gpulet+int", "sbp"])
+    ap.add_argument("--mode", default="gpulet", choices=["gpulet", "gpulet+int", "sbp"])
     ap.add_argument("--scenario", default="game")
     ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
     ap.add_argument("--probe-window", type=float, default=0.5)

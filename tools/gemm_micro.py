@@ -18,6 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 SHAPES = {
     "res_conv1": ("conv", (32, 224, 224, 8, 64, 7, 2, 3)),
     "res_l1_1x1_64": ("conv", (32, 56, 56, 64, 64, 1, 1, 0)),
+    "res_l1_1x1_256to64": ("conv", (32, 56, 56, 256, 64, 1, 1, 0)),
     "res_l1_3x3_64": ("conv", (32, 56, 56, 64, 64, 3, 1, 1)),
     "res_l1_1x1_256": ("conv", (32, 56, 56, 64, 256, 1, 1, 0)),
     "res_l2_3x3_128": ("conv", (32, 28, 28, 128, 128, 3, 1, 1)),
