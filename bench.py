@@ -165,7 +165,7 @@ def reference_arm(a, world, rank):
             times.append(time.perf_counter() - t0)
     tot = sum(times)
     val = a.steps / tot
-    cores = os.cpu_count()
+    cores = _blas_threads()
     return {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1000 * tot / a.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -173,6 +173,15 @@ def reference_arm(a, world, rank):
             "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": "1 request per step, models cycled in canonical order"},
             "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads", 1) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count()
 
 
 def cpu_baseline_sample():
@@ -185,7 +194,7 @@ def cpu_baseline_sample():
         t0 = time.perf_counter()
         omodels.forward(m, w, x)
         t += time.perf_counter() - t0
-    return {"value": round(len(synthgen.MODELS) / t, 4), "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+    return {"value": round(len(synthgen.MODELS) / t, 4), "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
             "sample": "one batch-1 request of each of the six models (fp64 numpy forward)"}
 
 
@@ -225,13 +234,21 @@ class Server:
         self.lat, self.l2, self.mem, self.slo, self.coeffs = prof
         self.mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
         self.x, self.y, self.xh, self.yh, self.req_bytes = {}, {}, {}, {}, {}
+        self.x2, self.y2 = {}, {}
+        self.cost = {}
         for m in common.MODELS:
             inb, outb = ctx.model_io(self.mids[m], 32)
             self.req_bytes[m] = (inb // 32, outb // 32)
+            f1, wb = ctx.model_cost(self.mids[m], 1)
+            self.cost[m] = (f1, wb)   # FLOPs per request (batch-linear), weight bytes per batch
             for slot in (0, 1):
                 self.x[m, slot] = common.device_input(m, 32)
                 self.y[m, slot] = torch.empty(outb // 4, device="cuda")
             if e2e:
+                # a second device buffer pair per lane: one batch copies while the other runs
+                for slot in (0, 1):
+                    self.x2[m, slot] = common.device_input(m, 32)
+                    self.y2[m, slot] = torch.empty(outb // 4, device="cuda")
                 h = common.host_input(m, 32)
                 reps = [h] * (self.HOST_SLOTS // 32)
                 self.xh[m] = torch.cat(reps).pin_memory()
@@ -279,6 +296,7 @@ class Server:
                 self.lanes.append(dict(gpulet=gid, model_id=self.mids[m], model_slot=mi, batch=ln["batch"],
                                        duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.x[m, g["slot"]],
                                        y=self.y[m, g["slot"]], x_host=self.xh.get(m), y_host=self.yh.get(m),
+                                       x2=self.x2.get((m, g["slot"])), y2=self.y2.get((m, g["slot"])),
                                        in_req_bytes=ib, out_req_bytes=ob, host_slots=self.HOST_SLOTS,
                                        size=g["size"], sm=nsm, model=m))
                 my_rates[mi] += ln["rate"]
@@ -295,8 +313,8 @@ class Server:
         from tools import common
         t, m = poisson_trace(rates, secs, seed)
         if len(t) == 0 or not self.lanes:
-            return dict(arrivals=0, sat=0, viol=0, dev_s=0.0, wall_s=0.0, h2d=0, d2h=0, per={})
-        lanes = self.lanes if e2e else [{k: v for k, v in ln.items() if k not in ("x_host", "y_host")}
+            return dict(arrivals=0, sat=0, viol=0, dev_s=0.0, wall_s=0.0, h2d=0, d2h=0, per={}, lanes=[])
+        lanes = self.lanes if e2e else [{k: v for k, v in ln.items() if k not in ("x_host", "y_host", "x2", "y2")}
                                          for ln in self.lanes]
         w0 = time.perf_counter()
         lat, st = self.ctx.serve(lanes, len(common.MODELS), t, m, self.slo, stats=True)
@@ -313,7 +331,8 @@ class Server:
                              "slo_us": int(self.slo[mi])}
         d0, d1 = st["dev_ns"]
         return dict(arrivals=int(len(lat)), sat=int((~viol).sum()), viol=int(viol.sum()),
-                    dev_s=max(d1 - d0, 0) * 1e-9, wall_s=wall, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], per=per)
+                    dev_s=max(d1 - d0, 0) * 1e-9, wall_s=wall, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], per=per,
+                    lanes=st["lanes"])
 
 
 def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
@@ -369,6 +388,7 @@ def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
         if clk:
             clk.__exit__()
             res["clocks"] = clk.summary()
+        res["lane_util"] = lane_util(srv, wins)
         sat, arr, viol = allsum(dist, [sum(w["sat"] for w in wins), sum(w["arrivals"] for w in wins),
                                        sum(w["viol"] for w in wins)])
         dev_s, wall_s = allmax(dist, [sum(w["dev_s"] for w in wins), sum(w["wall_s"] for w in wins)])
@@ -389,6 +409,63 @@ def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
     return res
 
 
+def lane_util(srv, wins):
+    """Per lane (gpu-let share of a model) over the timed windows: batches,
+    requests, device busy time (the executor's %globaltimer stamps of each batch)
+    and the achieved tensor / HBM rates against the gpu-let's SM-share roofline:
+    FLOPs = requests x FLOP/request; algorithmic bytes = per batch, weights once
+    + each request's input and output (SURVEY §8(d) D0 floors)."""
+    hbm, _burst, sus, src = _peaks()
+    out = []
+    for i, ln in enumerate(srv.lanes):
+        b = sum(w["lanes"][i]["batches"] for w in wins if w["lanes"])
+        r = sum(w["lanes"][i]["requests"] for w in wins if w["lanes"])
+        ns = sum(w["lanes"][i]["busy_ns"] for w in wins if w["lanes"])
+        m = ln["model"]
+        f1, wb = srv.cost[m]
+        ib, ob = srv.req_bytes[m]
+        t = ns * 1e-9
+        fl, by = f1 * r, wb * b + (ib + ob) * r
+        peak_t = ln["sm"] / 148.0 * sus
+        ach_t = fl / t / 1e12 if t else 0.0
+        ach_b = by / t / 1e9 if t else 0.0
+        out.append({"model": m, "gpulet_pct": ln["size"], "sm": ln["sm"], "planned_batch": ln["batch"],
+                    "batches": b, "requests": r, "busy_s": round(t, 4),
+                    "mean_batch": round(r / b, 2) if b else 0.0, "mean_batch_us": round(t / b * 1e6, 1) if b else 0.0,
+                    "tflops": round(ach_t, 2), "tensor_frac": round(ach_t / peak_t, 4) if peak_t else 0.0,
+                    "tensor_peak_tflops": round(peak_t, 1), "gbs": round(ach_b, 1),
+                    "hbm_frac": round(ach_b / hbm, 4), "hbm_peak_gbs": hbm,
+                    "peak_source": f"{src}: SM-share of the sustained bf16 peak (kernel inside a long run); HBM copy"})
+    return out
+
+
+def roofline_serving(util):
+    """The dominant kernel: the lane with the most device busy time in the timed
+    windows.  Tensor-bound when its FLOP per algorithmic byte exceeds the ridge."""
+    if not util:
+        return None
+    u = max(util, key=lambda d: d["busy_s"])
+    if not u["busy_s"]:
+        return None
+    hbm, _burst, sus, src = _peaks()
+    tensor = u["tflops"] * 1e12 / max(u["gbs"] * 1e9, 1.0) > sus * 1e12 / (hbm * 1e9)
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", f"ncu_{u['model']}_b{u['planned_batch']}.json")
+    if os.path.exists(ncu_path):
+        with open(ncu_path) as f:
+            traffic = json.load(f).get("dram_bytes")
+    return {"bound": "tensor" if tensor else "hbm", "achieved": u["tflops"] if tensor else u["gbs"],
+            "peak": u["tensor_peak_tflops"] if tensor else u["hbm_peak_gbs"],
+            "unit": "TFLOP/s" if tensor else "GB/s",
+            "frac": u["tensor_frac"] if tensor else u["hbm_frac"], "traffic": traffic,
+            "traffic_note": (f"ncu dram__bytes_read+write of one whole-GPU launch of {u['model']} b={u['planned_batch']}"
+                             if traffic else "no ncu capture at this batch"),
+            "kernel": f"gl_executor serving {u['model']} on a {u['gpulet_pct']}% gpu-let ({u['sm']} SMs)",
+            "timing": "device %globaltimer per batch inside the timed windows (persistent kernel: no per-batch launch)",
+            "batches": u["batches"], "mean_batch": u["mean_batch"], "mean_batch_us": u["mean_batch_us"],
+            "peak_source": u["peak_source"]}
+
+
 def roofline(ctx, srv, lanes):
     """Dominant lane (most planned device time: rate / batch x L) -> its model
     program at its batch, one executor launch on the whole GPU."""
@@ -403,8 +480,9 @@ def roofline(ctx, srv, lanes):
     m, b = ln["model"], ln["batch"]
     mid = srv.mids[m]
     durs = [sum(ctx.run_once(mid, b, srv.x[m, 0], srv.y[m, 0], 0, True)) for _ in range(4)][1:]
-    info = ctx.program_info(mid, b)
-    fl, by = sum(s[2] for s in info), sum(s[3] for s in info)
+    fl, wb = ctx.model_cost(mid, b)
+    ib, ob = srv.req_bytes[m]
+    by = wb + b * (ib + ob)          # weights once + the batch's input and output
     t = statistics.median(durs) * 1e-9
     tensor = fl / max(by, 1) > peak_burst * 1e12 / (hbm * 1e9)
     ach = fl / t / 1e12 if tensor else by / t / 1e9
@@ -418,6 +496,7 @@ def roofline(ctx, srv, lanes):
             "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
             "kernel": f"gl_executor, one launch of the {m} b={b} program on 148 SMs", "launch_us": round(t * 1e6, 1),
             "algorithmic_flop": fl, "algorithmic_bytes": by,
+            "timing": "device %globaltimer of the launch (first step start -> last barrier)",
             "peak_source": f"{src} (MEASURED_PEAKS.json, burst: kernel timed alone)"}
 
 
@@ -440,13 +519,16 @@ def our_arm(a, world, rank, local, dist):
     if not a.headline_only:
         other = "gpulet+int" if a.mode == "gpulet" else "gpulet"
         for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), (other.replace("+", "_"), a.scenario, other),
+                                ("traffic", "traffic", a.mode), ("traffic_baseline_sbp", "traffic", "sbp"),
+                                ("long_only", "long-only", a.mode), ("long_only_baseline_sbp", "long-only", "sbp"),
                                 ("mix6", "mix6", a.mode), ("mix6_baseline_sbp", "mix6", "sbp")):
             r = run_mode(srv, dist, rank, world, scen, mode, a, timed=False)
             extra[key] = {"value": round(r["value"], 2), "scenario": scen, "mode": mode,
                           "rate_multiplier": round(r["x"], 4), "x_sched": round(r["x_sched"], 4),
                           "rates_req_s": r["rates"], "viol_frac": round(r.get("viol_frac", 1.0), 4),
                           "lanes": r.get("lanes", []), "note": r.get("note")}
-    roof = roofline(ctx, srv, head.get("lanes", [])) if rank == 0 else None
+    roof = roofline_serving(head.get("lane_util")) if rank == 0 else None
+    roof1 = roofline(ctx, srv, head.get("lanes", [])) if rank == 0 else None
     if rank != 0:
         ctx.close()
         return None
@@ -468,7 +550,8 @@ def our_arm(a, world, rank, local, dist):
                    "parallelism": f"dp{world} (gpu-lets placed on {world} GPU(s) by the scheduler)"},
         "gpu_launches": len({ln["gpulet"] for ln in head.get("lanes", [])}),
         "gpu_launches_note": "persistent executors serving the timed windows (launched at gpu-let creation)",
-        "roofline": roof, "clocks": head.get("clocks"), "e2e": head.get("e2e"),
+        "roofline": roof, "roofline_oneshot_148sm": roof1, "gpulets": head.get("lane_util"),
+        "clocks": head.get("clocks"), "e2e": head.get("e2e"),
     }
     line.update(extra)
     if not a.no_cpu_baseline and world == 1:

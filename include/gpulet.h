@@ -153,21 +153,39 @@ typedef struct {
                            in_host + (r % host_slots) * in_req_bytes) */
   void* out_host;       /* end-to-end mode: outputs copied D2H here on completion (same slot rule) */
   int64_t in_req_bytes, out_req_bytes;  /* bytes of one request's input / output */
-  int32_t host_slots;   /* requests held in in_host / out_host */
+  int32_t host_slots;   /* requests held in in_host / out_host (per model, ring order) */
   int32_t pad2_;
+  const void* in_dev2;  /* end-to-end mode, optional second device input/output pair: with it a lane keeps */
+  void* out_dev2;       /*   two batches in flight (one copying while the other runs); NULL = one */
 } gl_lane;
 /* Replay an arrival trace in real time (host clock): arr_us[n_req] sorted arrival
  * times (us from the call), arr_model[n_req] model slot of each request.  Returns
  * per-request latency in lat_us (us; -1 dropped) and, when dev_ns is not NULL,
  * dev_ns[0..1] = first dequeue and last completion (%globaltimer ns) of the
- * batches it ran.  In end-to-end mode (lanes with in_host) a lane keeps at most
- * one batch in flight and the latency includes the H2D / D2H copies; *h2d_bytes /
- * *d2h_bytes (may be NULL) return the bytes copied.  Blocks until every request
- * is completed or dropped.  Errors: GL_E_ARG, GL_E_TIMEOUT, GL_E_CUDA, errors of
- * submit/poll. */
+ * batches it ran.  End-to-end mode (lanes with in_host): the i-th request of a
+ * model (arrival order) lives in host slot i % host_slots of in_host / out_host
+ * (a pinned per-model ring, as a network receive path would fill it); a batch's
+ * inputs are copied H2D (asynchronously, on a per-lane stream, contiguous slots
+ * coalesced into one copy) and it is submitted when the copy has landed; on
+ * completion its outputs are copied D2H the same way and the requests complete
+ * when that copy has landed, so the latency includes both copies.  A lane keeps
+ * one batch in flight, two with in_dev2/out_dev2.  *h2d_bytes / *d2h_bytes (may
+ * be NULL) return the bytes copied; lane_stats (may be NULL; n_lanes entries) the
+ * per-lane execution record.  The frontend thread never blocks on a copy.
+ * Blocks until every request is completed or dropped.  Errors: GL_E_ARG,
+ * GL_E_TIMEOUT, GL_E_CUDA, errors of submit/poll. */
+/* Per-lane execution record of one gl_serve call: batches and requests run, and
+ * the summed device time of its batches (t_end - t_start, %globaltimer ns: the
+ * executor's own clock, since a persistent kernel has no per-batch launch). */
+typedef struct {
+  int64_t batches;
+  int64_t requests;
+  uint64_t busy_ns;
+  uint64_t pad_;
+} gl_lane_stats;
 gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
                    const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
-                   uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes);
+                   uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes, gl_lane_stats* lane_stats);
 
 /* ---- scheduler (Alg. 1) --------------------------------- */
 typedef struct {

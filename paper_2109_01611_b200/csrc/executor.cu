@@ -60,6 +60,7 @@ struct Smem {
   int flags;         // ExecParams::dbg_flags
   GemmArgs* opc;     // shared-memory copy of the current GEMM step's op args (first kOpCache ops)
   int* opn;          //   and their unit counts
+  float* ebias;      // epilogue: per-warp fp32 bias of the current tile's columns (8 x 256)
 };
 
 __device__ __forceinline__ void tl_mark(const Smem& S, int i, int k) {
@@ -164,68 +165,116 @@ __device__ __forceinline__ void add_bf16x8(float* v, const uint4& u) {
   }
 }
 
+// Request the residual chunk [32 rows x 32 columns] at column `col` into the
+// staging rows (cp.async, L2 only): lane (sr, seg) copies 16 B of rows
+// it * 8 + sr (it = 0..3) at segment seg of the 64-B row chunk.
+__device__ __forceinline__ void res_request(uint8_t* stg, const __nv_bfloat16* rsd, int row0, int M, int64_t ldc,
+                                            int64_t col, int lane) {
+  const int sr = lane >> 2, seg = lane & 3;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + sr;
+    const bool ok = row0 + r < M;
+    const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + col + seg * 8 : rsd;
+    cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
+  }
+  cp_async_commit();
+}
+
+// One 16-column half h of chunk j (see epi_rows): v holds its accumulators
+// (TMEM already waited), sb the chunk's fp32 bias (smem), the lane's staging
+// row the chunk's residual (RES).  Returns the bf16 results in o.
+template <int ACT, bool RES>
+__device__ __forceinline__ void epi_half(const uint32_t (&v)[16], const float* sb, bool has_bias, const uint4& r0,
+                                         const uint4& r1, int h, uint4 (&o)[2]) {
+  float x[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) x[c] = __uint_as_float(v[c]);
+  if (has_bias) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 b = ((const float4*)(sb + h * 16))[k];   // broadcast
+      x[4 * k] += b.x, x[4 * k + 1] += b.y, x[4 * k + 2] += b.z, x[4 * k + 3] += b.w;
+    }
+  }
+  if (RES) {
+    add_bf16x8(x, r0);
+    add_bf16x8(x + 8, r1);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    __nv_bfloat162 hh[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      hh[q] = __floats2bfloat162_rn(act_t<ACT>(x[8 * k + 2 * q]), act_t<ACT>(x[8 * k + 2 * q + 1]));
+    o[k] = *(const uint4*)hh;
+  }
+}
+
 // Warp-collective epilogue of the 32 rows [row0, row0 + 32) of one tile, for
 // `nfull` full 32-column chunks starting at output column n00 (bf16 row-major
-// output): TMEM -> registers, + bias (+ residual) -> ACT -> bf16.  Rows are
-// staged in shared memory so that residual loads and output stores move 16 B
-// per lane with four lanes per 64-B row segment.  The caller loaded the bias
-// (lane l of chunk j holds column n00 + 32 j + l in bl[j]) and issued chunk 0's
-// residual copy before the accumulator was ready; chunk j + 1's residual is
-// requested while chunk j's TMEM load is in flight.
+// output): TMEM -> registers, + bias (+ residual) -> ACT -> bf16.  TMEM is read
+// in 16-column halves with the next half's load in flight while the current
+// one is processed.  Rows are staged in shared memory so that residual loads
+// and output stores move 16 B per lane with four lanes per 64-B row segment.
+// The caller put the tile's fp32 bias for these columns in sb and, for RES,
+// requested chunk 0's residual into the staging rows before the accumulator
+// was ready; chunk j + 1's residual is requested after chunk j's stores.
 template <int ACT, bool RES>
 __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, const Ctx& X, uint32_t taddr,
                                          int row0, int n00, int nfull, uint8_t* stg, int lane, bool nostore,
-                                         const float* bl, bool has_bias) {
+                                         const float* sb, bool has_bias, int flags) {
   const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
   __nv_bfloat16* outp = (__nv_bfloat16*)res(e.out, X);
-  const int sr = lane >> 2, seg = lane & 3;
   const int64_t ldc = e.ldc;
   const int64_t coff = e.col_off;
   const int M = g.M;
+  const int sr = lane >> 2, seg = lane & 3;
+  uint8_t* srow = stg + lane * kEpiRowBytes;
+  uint32_t va[16], vb[16];
+  tmem_ld16_issue(taddr, va);
+  tmem_wait_ld16(va);
+  const bool direct = (flags & 32) != 0;   // tuning: own-row stores (measured slower than staged)
 #pragma unroll 1
   for (int j = 0; j < nfull; ++j) {
     const int n0 = n00 + j * 32;
-    float v[32];
-    tmem_ld32(taddr + j * 32, v);
-    if (has_bias) {
-      float bj = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == j) bj = bl[q];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) v[c] += __shfl_sync(0xffffffffu, bj, c);
-    }
+    tmem_ld16_issue(taddr + j * 32 + 16, vb);
+    uint4 rr[4];
     if (RES) {
+      // this chunk's residual (staged rows) -> registers; the staging rows are
+      // then free, so the next chunk's residual is requested right away
       cp_async_wait<0>();
       __syncwarp();
-      const uint4* rp = (const uint4*)(stg + lane * kEpiRowBytes);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) add_bf16x8(v + 8 * k, rp[k]);
+      for (int k = 0; k < 4; ++k) rr[k] = ((const uint4*)srow)[k];
+      __syncwarp();
+      if (direct && j + 1 < nfull) res_request(stg, rsd, row0, M, ldc, coff + n0 + 32, lane);
     }
-    __align__(16) __nv_bfloat16 o[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) o[c] = __float2bfloat16_rn(act_t<ACT>(v[c]));
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ((uint4*)(stg + lane * kEpiRowBytes))[k] = ((const uint4*)o)[k];
-    __syncwarp();
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int r = it * 8 + sr;
-      if (row0 + r < M && !nostore)
-        *(uint4*)(outp + (row0 + r) * ldc + coff + n0 + seg * 8) = *(const uint4*)(stg + r * kEpiRowBytes + seg * 16);
-    }
-    __syncwarp();
-    if (RES && j + 1 < nfull) {
+    uint4 oa[2], ob[2];
+    epi_half<ACT, RES>(va, sb + j * 32, has_bias, rr[0], rr[1], 0, oa);
+    tmem_wait_ld16(vb);
+    if (j + 1 < nfull) tmem_ld16_issue(taddr + (j + 1) * 32, va);
+    epi_half<ACT, RES>(vb, sb + j * 32, has_bias, rr[2], rr[3], 1, ob);
+    if (direct) {
+      // this lane's row: 64 contiguous bytes
+      if (row0 + lane < M && !nostore) {
+        uint4* dst = (uint4*)(outp + (row0 + lane) * ldc + coff + n0);
+        dst[0] = oa[0], dst[1] = oa[1], dst[2] = ob[0], dst[3] = ob[1];
+      }
+    } else {
+      __syncwarp();
+      ((uint4*)srow)[0] = oa[0], ((uint4*)srow)[1] = oa[1], ((uint4*)srow)[2] = ob[0], ((uint4*)srow)[3] = ob[1];
+      __syncwarp();
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
-        const int r = it * 8 + sr;
-        const bool ok = row0 + r < M;
-        const __nv_bfloat16* src = ok ? rsd + (row0 + r) * ldc + coff + n0 + 32 + seg * 8 : rsd;
-        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
+        const int rw = it * 8 + sr;
+        if (row0 + rw < M && !nostore)
+          *(uint4*)(outp + (row0 + rw) * ldc + coff + n0 + seg * 8) = *(const uint4*)(stg + rw * kEpiRowBytes + seg * 16);
       }
-      cp_async_commit();
+      __syncwarp();
+      if (RES && j + 1 < nfull) res_request(stg, rsd, row0, M, ldc, coff + n0 + 32, lane);
     }
+    if (j + 1 < nfull) tmem_wait_ld16(va);
   }
 }
 
@@ -316,6 +365,47 @@ struct StepOps {
   }
 };
 
+// Prefetch what the next step reads first, one step ahead.  prefetch_desc:
+// its descriptors into L2 (no loads: issued by all threads at step start).
+// prefetch_ops: its tensor maps (this SM's descriptor cache) and, with
+// GL_WEIGHT_PF, the weights of its GEMM ops (L2; the range is split over the
+// gpu-let's CTAs) -- this reads the descriptors, so one warp issues it where it
+// would otherwise idle (the MMA warp after its last tile, a single lane of a
+// CUDA-core step).
+constexpr int kPfOps = 8;
+#ifdef GL_WEIGHT_PF
+constexpr uint64_t kPfMaxBytes = 8ull << 20;
+#endif
+__device__ __forceinline__ void prefetch_desc(const OpDesc* nxt, int n) {
+  constexpr int kLines = (int)((sizeof(OpDesc) + 127) / 128);
+  const int t = threadIdx.x;
+  if (t < n * kLines) {
+    const char* p = (const char*)(nxt + t / kLines) + (t % kLines) * 128;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
+}
+__device__ __forceinline__ void prefetch_ops(const OpDesc* nxt, int n, int lane) {
+  if (lane >= n) return;
+  const OpDesc* op = nxt + lane;
+  const int ty = op->type;
+  if ((ty == OP_GEMM && op->g.a_tma != SRC_GATHER) || (ty == OP_ATTENTION && op->g.act_tmap))
+    tma_prefetch_desc(&op->tmap_a);
+  if (ty == OP_GEMM && op->g.b_tma != SRC_GATHER) tma_prefetch_desc(&op->tmap_b);
+#ifdef GL_WEIGHT_PF
+  // off: measured to raise the co-located LeNet lane's SLO violations (L2/DRAM
+  // interference of the bulk prefetch) more than it saves (tools/serve_ab.py)
+  const uint64_t a = op->pf_addr, bytes = op->pf_bytes;
+  if (a && bytes && bytes <= kPfMaxBytes) {
+    const uint64_t chunk = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    if (lo < bytes) {
+      const uint32_t sz = (uint32_t)min(chunk, bytes - lo);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + lo), "r"(sz) : "memory");
+    }
+  }
+#endif
+}
+
 // ------------------------------------------------------------------ GEMM step (K1-K4)
 // Roles.  Steps whose operands all come by TMA: warp 9 (one thread) produces,
 // warp 8 (one thread) issues tcgen05.mma, warps 0-7 run the epilogue (warp w
@@ -375,7 +465,8 @@ __device__ __forceinline__ uint32_t stage_bytes_for(int bn) {
 // that do not depend on it (bias, first residual chunk).
 __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, const Smem& S, uint32_t taddr, int mb,
                                               int nb, int kb0, int q, int c0, int c1, uint8_t* stg, int lane,
-                                              uint64_t* tfull, uint32_t parity) {
+                                              uint64_t* tfull, uint32_t parity, float* sb, uint32_t key,
+                                              uint32_t& bkey) {
   const Epilogue& e = g.ep;
   const int m = mb * 128 + q * 32 + lane;
   const int nend = min(g.N, (nb + 1) * g.BN);
@@ -383,25 +474,18 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
   const bool fast = !(S.flags & 1) && e.splitk <= 1 && !e.transpose && !e.out_fp32 && e.rows_per_img >= g.M &&
                     (e.ldc % 8) == 0 && (e.col_off % 8) == 0 && c1 > c0;
   const int nfull = fast ? min(8, (c1 - c0) / 32) : 0;
-  float bl[8];
   const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
   const bool rs = e.res.kind != BUF_NONE;
   const int row0 = mb * 128 + q * 32, n00 = nb * g.BN + c0;
   if (nfull > 0) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) bl[j] = (bias && j < nfull) ? __bfloat162float(bias[n00 + 32 * j + lane]) : 0.f;
-    if (rs) {
-      const __nv_bfloat16* rsd = (const __nv_bfloat16*)res(e.res, X);
-      const int sr = lane >> 2, seg = lane & 3;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int r = it * 8 + sr;
-        const bool ok = row0 + r < g.M;
-        const __nv_bfloat16* src = ok ? rsd + (int64_t)(row0 + r) * e.ldc + e.col_off + n00 + seg * 8 : rsd;
-        cp_async16(smem_u32(stg + r * kEpiRowBytes + seg * 16), src, ok ? 16u : 0u);
-      }
-      cp_async_commit();
+    // the tile's bias columns, fp32 in smem; reloaded only when (op, n block) changes
+    // (a CTA's tiles of one op mostly share nb: m blocks vary fastest)
+    if (bias && bkey != key) {
+      for (int i = lane; i < nfull * 32; i += 32) sb[i] = __bfloat162float(bias[n00 + i]);
+      __syncwarp();
+      bkey = key;
     }
+    if (rs) res_request(stg, (const __nv_bfloat16*)res(e.res, X), row0, g.M, e.ldc, (int64_t)e.col_off + n00, lane);
   }
   mbar_wait(tfull, parity);
   tc_fence_after();
@@ -449,14 +533,14 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
     const bool ns = (S.flags & 2) != 0;
     const bool hb = bias != nullptr;
     switch (e.act * 2 + (rs ? 1 : 0)) {
-      case 0: epi_rows<ACT_NONE, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 1: epi_rows<ACT_NONE, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 2: epi_rows<ACT_RELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 3: epi_rows<ACT_RELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 4: epi_rows<ACT_GELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 5: epi_rows<ACT_GELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      case 6: epi_rows<ACT_TANH, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
-      default: epi_rows<ACT_TANH, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, bl, hb); break;
+      case 0: epi_rows<ACT_NONE, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 1: epi_rows<ACT_NONE, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 2: epi_rows<ACT_RELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 3: epi_rows<ACT_RELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 4: epi_rows<ACT_GELU, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 5: epi_rows<ACT_GELU, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      case 6: epi_rows<ACT_TANH, false>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
+      default: epi_rows<ACT_TANH, true>(e, g, X, ta, row0, n00, nfull, stg, lane, ns, sb, hb, S.flags); break;
     }
     j0 = c0 + nfull * 32;
   }
@@ -470,7 +554,7 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
   }
 }
 
-__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& Sio, Pipe& Pio) {
+__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& Sio, Pipe& Pio, int n_next) {
   // register copies: the k loops must not reload ring state through memory
   // after every asm statement (they all clobber "memory")
   const Smem S = Sio;
@@ -500,15 +584,6 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   // every thread ends the step with the ring and accumulator state the
   // participating threads reached: this CTA's tile and k-block counts.
   const uint32_t bits0 = P.bits, acc0 = P.acc;
-  int my_tiles = 0, my_kb = 0;
-  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    int lt;
-    const int oi = so.locate(tile, lt);
-    int mb, nb, kb0, kb1;
-    decode_tile(so.g(oi), lt, mb, nb, kb0, kb1);
-    ++my_tiles;
-    my_kb += kb1 - kb0;
-  }
 
   if (gstep && warp < 4) {
     // ---------------- gather producers (128 threads; thread 0 also issues the TMA half)
@@ -631,7 +706,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     // ---------------- MMA issuer (whole warp walks the loop; one elected lane issues)
     const uint32_t tbase = *S.tmem_base;
     const uint64_t bhi = umma_sdesc_sw128(0);
-    int ntile = 0;
+    int ntile = 0, nkb_total = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const int oi = so.locate(tile, lt);
@@ -671,16 +746,24 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       }
       if (elect_one()) umma_commit(&S.tfull[acc]);
       __syncwarp();
+      nkb_total += kb1 - kb0;
       if (lane == 0) tl_mark(S, ntile, 1);
       ++ntile;
       ++P.acc;
     }
-    if (lane == 0) dbg_mark(S, 3);
+    if (lane == 0) {
+      dbg_mark(S, 3);
+      S.opn[kOpCache] = ntile;
+      S.opn[kOpCache + 1] = nkb_total;
+    }
+    prefetch_ops(ops + nops, n_next, lane);
   } else if (warp < 8) {
     // ---------------- epilogue: warps 4-7 (all columns) or 0-7 (column halves)
     const int q = warp & 3, half = warp < 4 ? 1 : 0;
     const uint32_t tbase = *S.tmem_base;
     uint8_t* stg = S.estage + warp * 32 * kEpiRowBytes;
+    float* sbias = S.ebias + warp * 256;
+    uint32_t bkey = 0xffffffffu;   // (op, n block) whose bias sbias holds
     const uint32_t arrive_n = gstep ? 2u : 1u;
     int ntile = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -701,7 +784,8 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       }
       if (lead) tl_mark(S, ntile, 2);
       if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
-      epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane, &S.tfull[acc], use & 1);
+      epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane, &S.tfull[acc], use & 1, sbias,
+                    ((uint32_t)oi << 16) | (uint32_t)nb, bkey);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cnt(&S.tempty[acc], arrive_n);
@@ -711,6 +795,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     }
     if (q == 0 && half == 0 && lane == 0) dbg_mark(S, 5);
   }
+  // this CTA's tile and k-block counts, counted by the MMA warp as it walked them
+  __syncthreads();
+  const int my_tiles = S.opn[kOpCache], my_kb = S.opn[kOpCache + 1];
   uint32_t flips = 0;
   for (uint32_t st = 0; st < P.nst; ++st) {
     const uint32_t uses = my_kb / P.nst + (st < my_kb % P.nst ? 1u : 0u);
@@ -1346,6 +1433,25 @@ __device__ __noinline__ void softmax_rows(const OpDesc* op, const Ctx& X) {
 // k = 1: kw taps into channels, y[n, h, w, kw*C + c] = x[n, h, w + kw - pad, c]
 // (zero outside the image and for the channels past KW*C).  C = 8 (one 16-B
 // vector per pixel); one 16-B output vector per thread item.
+__device__ __forceinline__ uint4 pack_item(const MiscArgs& a, const uint4* __restrict__ x, int i, int cv, int ov) {
+  const int j = i % ov;
+  int p = i / ov;
+  const int w = p % a.Wo;
+  p /= a.Wo;
+  const int h = p % a.Ho, n = p / a.Ho;
+  if (a.k == 0) {
+    const int sub = j / cv, c = j % cv;   // sub = dy*2 + dx
+    const int hi = 2 * h + (sub >> 1), wi = 2 * w + (sub & 1);
+    return __ldcs(x + ((n * a.H + hi) * a.W + wi) * cv + c);
+  }
+  const int kw = j / cv, c = j % cv;
+  const int wi = w + kw - a.pad;
+  if (kw < a.stride && wi >= 0 && wi < a.W) return __ldg(x + ((n * a.H + h) * a.W + wi) * cv + c);
+  return make_uint4(0u, 0u, 0u, 0u);
+}
+
+// Four items per thread per iteration, all loads issued before the stores
+// (memory-level parallelism: the input comes from HBM).
 __device__ __noinline__ void pack_input(const OpDesc* op, const Ctx& X) {
   const MiscArgs& a = op->m;
   const uint4* x = (const uint4*)res(a.x, X);
@@ -1353,23 +1459,14 @@ __device__ __noinline__ void pack_input(const OpDesc* op, const Ctx& X) {
   const int cv = a.C / 8;                 // input vectors per pixel
   const int ov = a.cols / 8;              // output vectors per pixel
   const int total = a.N * a.Ho * a.Wo * ov;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int j = i % ov;
-    int p = i / ov;
-    const int w = p % a.Wo;
-    p /= a.Wo;
-    const int h = p % a.Ho, n = p / a.Ho;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (a.k == 0) {
-      const int sub = j / cv, c = j % cv;   // sub = dy*2 + dx
-      const int hi = 2 * h + (sub >> 1), wi = 2 * w + (sub & 1);
-      v = __ldcs(x + ((n * a.H + hi) * a.W + wi) * cv + c);
-    } else {
-      const int kw = j / cv, c = j % cv;
-      const int wi = w + kw - a.pad;
-      if (kw < a.stride && wi >= 0 && wi < a.W) v = __ldg(x + ((n * a.H + h) * a.W + wi) * cv + c);
-    }
-    y[i] = v;
+  const int st = gridDim.x * blockDim.x;
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * st) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = i0 + u * st < total ? pack_item(a, x, i0 + u * st, cv, ov) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * st < total) y[i0 + u * st] = v[u];
   }
 }
 
@@ -1418,9 +1515,12 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     int j = i;
     while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
     S.step = step;
+    const int n_next = min(kPfOps, w.n_ops - j - 1);
+    prefetch_desc(w.prog + j + 1, n_next);
     if (w.prog[i].type == OP_GEMM) {
-      gemm_step(w.prog + i, j - i + 1, X, S, P);
+      gemm_step(w.prog + i, j - i + 1, X, S, P, n_next);
     } else {
+      if (threadIdx.x >= kThreads - 32) prefetch_ops(w.prog + j + 1, n_next, threadIdx.x - (kThreads - 32));
       for (int k = i; k <= j; ++k) run_misc(w.prog + k, X, S, P);
     }
     fence_proxy_async_smem();
@@ -1461,6 +1561,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.flags = p.dbg_flags;
   S.opc = (GemmArgs*)(base + kRingBytes + 1024 + kEpiStageBytes);
   S.opn = (int*)(S.opc + kOpCache);
+  S.ebias = (float*)(base + kRingBytes + 1024 + kEpiStageBytes + kOpCacheBytes);
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {

@@ -6,11 +6,17 @@
 // requests that can no longer meet their SLO (drops count as violations,
 // P:860).  A request's latency is host completion time - arrival time.
 //
-// End-to-end mode (lanes with in_host): the batch's inputs are copied from
-// pinned host memory into the lane's device buffer before the batch is
-// submitted, and its outputs back to the host when it completes, inside the
-// measured latency; a lane then keeps one batch in flight (its device buffers
-// are reused by the next batch).
+// End-to-end mode (lanes with in_host): a model's i-th request lives in host
+// slot i % host_slots of the lane's pinned ring.  A dispatched batch goes
+// through three stages, none of which blocks the frontend thread:
+//   H2D  its inputs are copied into a device buffer of the lane on the lane's
+//        stream (contiguous slots coalesced into one cudaMemcpyAsync), an event
+//        marks the end of the copy;
+//   RUN  submitted to the gpu-let once that event has completed;
+//   D2H  on completion its outputs are copied back the same way; the requests
+//        complete when that copy's event has completed.
+// A lane has one or two device buffers (in_dev2), i.e. one or two batches in
+// flight: with two, the copy of the next batch overlaps the current one's run.
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -22,49 +28,105 @@
 #include "../../include/gpulet.h"
 
 namespace {
+enum Stage { FREE = 0, H2D, RUN, D2H };
+
+struct Batch {
+  Stage stage = FREE;
+  std::vector<int64_t> reqs;   // request indices
+  std::vector<int64_t> slots;  // their host slots (end-to-end mode)
+  cudaEvent_t ev = nullptr;
+  uint64_t ticket = 0;
+};
+
+struct Inflight {
+  int lane;
+  int buf;                     // end-to-end buffer index, -1 in plain mode
+  std::vector<int64_t> reqs;   // plain mode: the batch's request indices
+};
+
 struct LaneState {
   gl_lane cfg;
   std::deque<int64_t> q;  // request indices
   int64_t window_us = 0;
   int64_t cur = 0;        // smooth WRR credit
-  bool busy = false;      // end-to-end mode: a batch of this lane is in flight
-};
-struct Inflight {
-  int lane;
-  std::vector<int64_t> reqs;
+  int nbuf = 1;           // device buffers (batches in flight)
+  Batch buf[2];
+  cudaStream_t stream = nullptr;
+  const void* in_dev(int b) const { return b ? cfg.in_dev2 : cfg.in_dev; }
+  void* out_dev(int b) const { return b ? cfg.out_dev2 : cfg.out_dev; }
+  int free_buf() const {
+    for (int b = 0; b < nbuf; ++b)
+      if (buf[b].stage == FREE) return b;
+    return -1;
+  }
+  bool idle() const {
+    for (int b = 0; b < nbuf; ++b)
+      if (buf[b].stage != FREE) return false;
+    return true;
+  }
 };
 
-// Copy k request slots between a host slot array and a contiguous device buffer.
-bool copy_slots(void* dev, const void* host, const std::vector<int64_t>& reqs, int64_t bytes, int32_t slots,
-                bool h2d, int64_t* moved) {
-  for (size_t i = 0; i < reqs.size(); ++i) {
-    const int64_t slot = slots > 0 ? reqs[i] % slots : 0;
-    char* d = (char*)dev + i * bytes;
-    char* h = (char*)host + slot * bytes;
-    const cudaError_t e = h2d ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, cudaStreamPerThread)
-                              : cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, cudaStreamPerThread);
+// Copy the request slots of a batch between the host ring and a contiguous
+// device buffer (request i of the batch at dev + i * bytes), one async copy per
+// run of consecutive slots.
+bool copy_slots(void* dev, const void* host, const std::vector<int64_t>& slots, int64_t bytes, bool h2d,
+                cudaStream_t st, int64_t* moved) {
+  size_t i = 0;
+  while (i < slots.size()) {
+    size_t j = i + 1;
+    while (j < slots.size() && slots[j] == slots[j - 1] + 1) ++j;
+    char* d = (char*)dev + (int64_t)i * bytes;
+    char* h = (char*)host + slots[i] * bytes;
+    const size_t n = (j - i) * (size_t)bytes;
+    const cudaError_t e = h2d ? cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st)
+                              : cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return false;
-    *moved += bytes;
+    *moved += (int64_t)n;
+    i = j;
   }
-  return cudaStreamSynchronize(cudaStreamPerThread) == cudaSuccess;
+  return true;
 }
+
+struct Cleanup {
+  std::vector<LaneState>& L;
+  ~Cleanup() {
+    for (auto& ln : L) {
+      if (ln.stream) cudaStreamSynchronize(ln.stream);
+      for (auto& b : ln.buf)
+        if (b.ev) cudaEventDestroy(b.ev);
+      if (ln.stream) cudaStreamDestroy(ln.stream);
+    }
+  }
+};
 }  // namespace
 
 extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
                               const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
-                              int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+                              int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                              gl_lane_stats* lane_stats) {
   if (!ctx || !lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || !slo_us || !lat_us)
     return GL_E_ARG;
   std::vector<LaneState> L(n_lanes);
+  Cleanup cleanup{L};
   std::vector<std::vector<int>> by_model(n_models);
   for (int i = 0; i < n_lanes; ++i) {
     L[i].cfg = lanes[i];
     if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models) return GL_E_ARG;
-    if (lanes[i].in_host && (!lanes[i].out_host || lanes[i].in_req_bytes <= 0 || lanes[i].out_req_bytes <= 0))
-      return GL_E_ARG;
+    if (lanes[i].in_host) {
+      if (!lanes[i].out_host || lanes[i].in_req_bytes <= 0 || lanes[i].out_req_bytes <= 0 || lanes[i].host_slots < 1)
+        return GL_E_ARG;
+      L[i].nbuf = (lanes[i].in_dev2 && lanes[i].out_dev2) ? 2 : 1;
+      if (cudaStreamCreateWithFlags(&L[i].stream, cudaStreamNonBlocking) != cudaSuccess) return GL_E_CUDA;
+      for (int b = 0; b < L[i].nbuf; ++b)
+        if (cudaEventCreateWithFlags(&L[i].buf[b].ev, cudaEventDisableTiming) != cudaSuccess) return GL_E_CUDA;
+    }
     by_model[lanes[i].model_slot].push_back(i);
   }
   for (int64_t r = 0; r < n_req; ++r) lat_us[r] = -2;
+  if (lane_stats)
+    for (int i = 0; i < n_lanes; ++i) lane_stats[i] = gl_lane_stats{0, 0, 0, 0};
+  std::vector<int64_t> seq_of(n_req, 0);   // model-local arrival index of each request (host slot rule)
+  std::vector<int64_t> model_seq(n_models, 0);
   int64_t h2d = 0, d2h = 0;
   uint64_t t_first = ~0ull, t_last = 0;
   std::unordered_map<uint64_t, Inflight> inflight;
@@ -73,15 +135,25 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
     return (int64_t)std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0)
         .count();
   };
+  auto complete = [&](Batch& b, int64_t t, int64_t& outstanding) {
+    for (int64_t r : b.reqs) {
+      lat_us[r] = t - arr_us[r];
+      --outstanding;
+    }
+    b.reqs.clear();
+    b.slots.clear();
+    b.stage = FREE;
+  };
   int64_t next = 0, outstanding = 0;
   gl_completion comp[128];
   const int64_t deadline = (n_req ? arr_us[n_req - 1] : 0) + 30'000'000;
   while (next < n_req || outstanding > 0) {
-    const int64_t now = now_us();
+    int64_t now = now_us();
     if (now > deadline) return GL_E_TIMEOUT;
     // 1. arrivals -> lanes (smooth weighted round-robin per model)
     while (next < n_req && arr_us[next] <= now) {
       const int m = arr_model[next];
+      seq_of[next] = model_seq[m]++;
       auto& cand = by_model[m];
       if (cand.empty()) {
         lat_us[next] = -1;
@@ -103,7 +175,9 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
     // 2. duty-cycle dispatch
     for (int li = 0; li < n_lanes; ++li) {
       LaneState& ln = L[li];
-      if (ln.q.empty() || ln.busy) continue;
+      if (ln.q.empty()) continue;
+      const int b = ln.cfg.in_host ? ln.free_buf() : 0;
+      if (b < 0) continue;
       const bool full = (int)ln.q.size() >= ln.cfg.batch;
       const bool timeout = now - ln.window_us >= ln.cfg.duty_us;
       if (!full && !timeout) continue;
@@ -120,20 +194,52 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       ln.window_us = now;
       if (ln.q.empty()) continue;
       const int k = std::min<int>((int)ln.q.size(), ln.cfg.batch);
-      std::vector<int64_t> reqs(ln.q.begin(), ln.q.begin() + k);
-      if (ln.cfg.in_host &&
-          !copy_slots((void*)ln.cfg.in_dev, ln.cfg.in_host, reqs, ln.cfg.in_req_bytes, ln.cfg.host_slots, true, &h2d))
-        return GL_E_CUDA;
+      if (ln.cfg.in_host) {
+        Batch& bt = ln.buf[b];
+        bt.reqs.assign(ln.q.begin(), ln.q.begin() + k);
+        bt.slots.resize(k);
+        for (int i = 0; i < k; ++i) bt.slots[i] = seq_of[bt.reqs[i]] % ln.cfg.host_slots;
+        ln.q.erase(ln.q.begin(), ln.q.begin() + k);
+        if (!copy_slots((void*)ln.in_dev(b), ln.cfg.in_host, bt.slots, ln.cfg.in_req_bytes, true, ln.stream, &h2d) ||
+            cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
+          return GL_E_CUDA;
+        bt.stage = H2D;
+        continue;
+      }
       uint64_t ticket = 0;
       const gl_status s = gl_submit_batch(ctx, ln.cfg.gpulet, ln.cfg.model_id, ln.cfg.in_dev, ln.cfg.out_dev, k,
                                           (float)slo_us[ln.cfg.model_slot] / 1000.f, &ticket);
       if (s == GL_E_QUEUE_FULL) continue;
       if (s != GL_OK) return s;
+      inflight.emplace(ticket, Inflight{li, -1, std::vector<int64_t>(ln.q.begin(), ln.q.begin() + k)});
       ln.q.erase(ln.q.begin(), ln.q.begin() + k);
-      ln.busy = ln.cfg.in_host != nullptr;
-      inflight.emplace(ticket, Inflight{li, std::move(reqs)});
     }
-    // 3. completions
+    // 3. end-to-end stage transitions (event polls; never block)
+    for (int li = 0; li < n_lanes; ++li) {
+      LaneState& ln = L[li];
+      if (!ln.cfg.in_host) continue;
+      for (int b = 0; b < ln.nbuf; ++b) {
+        Batch& bt = ln.buf[b];
+        if (bt.stage != H2D && bt.stage != D2H) continue;
+        const cudaError_t q = cudaEventQuery(bt.ev);
+        if (q == cudaErrorNotReady) continue;
+        if (q != cudaSuccess) return GL_E_CUDA;
+        if (bt.stage == D2H) {
+          complete(bt, now_us(), outstanding);
+          continue;
+        }
+        uint64_t ticket = 0;
+        const gl_status s = gl_submit_batch(ctx, ln.cfg.gpulet, ln.cfg.model_id, ln.in_dev(b), ln.out_dev(b),
+                                            (int32_t)bt.reqs.size(), (float)slo_us[ln.cfg.model_slot] / 1000.f,
+                                            &ticket);
+        if (s == GL_E_QUEUE_FULL) continue;
+        if (s != GL_OK) return s;
+        bt.ticket = ticket;
+        bt.stage = RUN;
+        inflight.emplace(ticket, Inflight{li, b, {}});
+      }
+    }
+    // 4. completions
     int32_t n = 0;
     const gl_status s = gl_poll(ctx, comp, 128, &n);
     if (s != GL_OK) return s;
@@ -142,19 +248,29 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       if (it == inflight.end()) continue;
       if (comp[i].t_dequeue_ns < t_first) t_first = comp[i].t_dequeue_ns;
       if (comp[i].t_end_ns > t_last) t_last = comp[i].t_end_ns;
-      LaneState& ln = L[it->second.lane];
-      if (ln.cfg.in_host) {
-        if (!copy_slots(ln.cfg.out_dev, ln.cfg.out_host, it->second.reqs, ln.cfg.out_req_bytes, ln.cfg.host_slots,
-                        false, &d2h))
-          return GL_E_CUDA;
-        ln.busy = false;
+      if (lane_stats) {
+        gl_lane_stats& ls = lane_stats[it->second.lane];
+        ls.batches += 1;
+        ls.requests += comp[i].batch;
+        ls.busy_ns += comp[i].t_end_ns > comp[i].t_start_ns ? comp[i].t_end_ns - comp[i].t_start_ns : 0;
       }
-      const int64_t t = now_us();
-      for (int64_t r : it->second.reqs) {
-        lat_us[r] = t - arr_us[r];
-        --outstanding;
+      LaneState& ln = L[it->second.lane];
+      const int b = it->second.buf;
+      if (b < 0) {
+        const int64_t t = now_us();
+        for (int64_t r : it->second.reqs) {
+          lat_us[r] = t - arr_us[r];
+          --outstanding;
+        }
+        inflight.erase(it);
+        continue;
       }
       inflight.erase(it);
+      Batch& bt = ln.buf[b];
+      if (!copy_slots(ln.out_dev(b), ln.cfg.out_host, bt.slots, ln.cfg.out_req_bytes, false, ln.stream, &d2h) ||
+          cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
+        return GL_E_CUDA;
+      bt.stage = D2H;
     }
   }
   if (dev_ns) {

@@ -354,6 +354,8 @@ class Builder {
     choose_split(op, allow_split);
     g.ep = ep;
     encode_tmap(&op.tmap_b, w.ptr, w.K_pad, w.rows, g.BN, e);
+    op.pf_addr = (uint64_t)(uintptr_t)w.ptr;
+    op.pf_bytes = (uint64_t)w.rows * w.K_pad * 2;
     finish_gemm(op);
     prog.flops += 2.0 * M * g.N * (double)w.K_real;
     prog.weight_bytes += (double)w.rows * w.K_real * 2;
@@ -386,6 +388,8 @@ class Builder {
     choose_split(op, true);
     g.ep = ep;
     encode_tmap(&op.tmap_a, w.ptr, w.K_pad, w.rows, 128, e);
+    op.pf_addr = (uint64_t)(uintptr_t)w.ptr;
+    op.pf_bytes = (uint64_t)w.rows * w.K_pad * 2;
     finish_gemm(op);
     prog.flops += 2.0 * nrows * g.M * (double)w.K_real;
     prog.weight_bytes += (double)w.rows * w.K_real * 2;

@@ -98,6 +98,8 @@ struct alignas(128) OpDesc {
   int32_t step_end;             // 1: gpu-let barrier after this op
   int32_t n_units;              // work units (tiles) of this op
   int32_t pad_;
+  uint64_t pf_addr;             // read-only operand (weights) prefetched into L2 one step ahead (0: none)
+  uint64_t pf_bytes;
   GemmArgs g;
   MiscArgs m;
 };
@@ -177,6 +179,7 @@ constexpr int kEpiRowBytes = 80;                   // 32 bf16 + 16 B pad per sta
 constexpr int kEpiStageBytes = 8 * 32 * kEpiRowBytes;  // 8 epilogue warps x (32 rows x 32 columns)
 constexpr int kOpCache = 8;     // GEMM args of the first 8 ops of a step are cached in shared memory
 constexpr int kOpCacheBytes = kOpCache * (int)sizeof(GemmArgs) + 64;
-constexpr int kSmemBytes = kRingBytes + 1024 + kEpiStageBytes + kOpCacheBytes;  // + barriers
+constexpr int kEpiBiasBytes = 8 * 256 * 4;        // 8 epilogue warps x up to 256 fp32 bias values of the tile
+constexpr int kSmemBytes = kRingBytes + 1024 + kEpiStageBytes + kOpCacheBytes + kEpiBiasBytes;  // + barriers
 
 }  // namespace gl

@@ -998,6 +998,7 @@ extern "C" gl_status gl_run_once(gl_ctx* ctx, int32_t mid, int32_t batch, const 
   p.one_shot = 1;
   p.trace = tr;
   p.trace_cap = tcap;
+  p.dbg_flags = g_tune[TUNE_MISC];   // tuning experiments only (0 unless gl_set_tuning)
   cudaStream_t s;
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   gl_status rc = launch_executor(ctx, G.dev, (CUstream)s, n_sm, p);

@@ -51,7 +51,7 @@ class Lane(ctypes.Structure):
                 ("drop_us", ctypes.c_int32), ("pad_", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
                 ("out_dev", ctypes.c_void_p), ("in_host", ctypes.c_void_p), ("out_host", ctypes.c_void_p),
                 ("in_req_bytes", ctypes.c_int64), ("out_req_bytes", ctypes.c_int64), ("host_slots", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32)]
+                ("pad2_", ctypes.c_int32), ("in_dev2", ctypes.c_void_p), ("out_dev2", ctypes.c_void_p)]
 
 
 _lib = None
@@ -61,9 +61,10 @@ def lib():
     """Load libgpulet.so (fails loudly when it was not built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise GpuletError(-12, f"{LIB_PATH} missing: run `python -m paper_2109_01611_b200.build`")
-        L = ctypes.CDLL(LIB_PATH)
+        path = os.environ.get("GL_LIB", LIB_PATH)   # GL_LIB: an alternative in-tree build (A/B tuning runs)
+        if not os.path.exists(path):
+            raise GpuletError(-12, f"{path} missing: run `python -m paper_2109_01611_b200.build`")
+        L = ctypes.CDLL(path)
         P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
         sig = {
             "gl_init": [ctypes.c_int, ctypes.POINTER(P)],
@@ -84,7 +85,7 @@ def lib():
                                 ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
             "gl_serve": [P, ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
                          ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(U64), ctypes.POINTER(I64),
-                         ctypes.POINTER(I64)],
+                         ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int64)],
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
@@ -232,7 +233,7 @@ class Context:
 
     def serve(self, lanes, n_models, arr_us, arr_model, slo_us, stats=False):
         """gl_serve: lanes = list of dicts (gpulet, model_id, model_slot, batch, duty_us,
-        weight, drop_us, x, y[, x_host, y_host, in_req_bytes, out_req_bytes, host_slots]);
+        weight, drop_us, x, y[, x_host, y_host, in_req_bytes, out_req_bytes, host_slots[, x2, y2]]);
         returns per-request latency (us, -1 dropped), and with stats also
         {"dev_ns": (first dequeue, last end), "h2d_bytes", "d2h_bytes"}."""
         import numpy as np
@@ -245,19 +246,25 @@ class Context:
                 L[i].in_host, L[i].out_host = _ptr(d["x_host"]), _ptr(d["y_host"])
                 L[i].in_req_bytes, L[i].out_req_bytes = d["in_req_bytes"], d["out_req_bytes"]
                 L[i].host_slots = d["host_slots"]
+                if d.get("x2") is not None:
+                    L[i].in_dev2, L[i].out_dev2 = _ptr(d["x2"]), _ptr(d["y2"])
         a = np.ascontiguousarray(arr_us, dtype=np.int64)
         m = np.ascontiguousarray(arr_model, dtype=np.int32)
         s = np.ascontiguousarray(slo_us, dtype=np.int32)
         out = np.zeros(len(a), dtype=np.int64)
         dev = (ctypes.c_uint64 * 2)()
         hb, db = ctypes.c_int64(), ctypes.c_int64()
+        ls = (ctypes.c_int64 * (4 * len(lanes)))()   # gl_lane_stats[n_lanes]
         _check(lib().gl_serve(self.h, L, len(lanes), n_models, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                               m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
                               s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), dev, ctypes.byref(hb),
-                              ctypes.byref(db)))
+                              ctypes.byref(db), ls))
         if stats:
-            return out, {"dev_ns": (dev[0], dev[1]), "h2d_bytes": hb.value, "d2h_bytes": db.value}
+            lanes_st = [{"batches": ls[4 * i], "requests": ls[4 * i + 1], "busy_ns": ls[4 * i + 2] & (2**64 - 1)}
+                        for i in range(len(lanes))]
+            return out, {"dev_ns": (dev[0], dev[1]), "h2d_bytes": hb.value, "d2h_bytes": db.value,
+                         "lanes": lanes_st}
         return out
 
     def program_info(self, mid, batch, cap=1024):

@@ -93,13 +93,21 @@ def scenario_rates(name, slo_us, x=1.0):
     """Rates of a scenario, scaled by SLO_paper/SLO_B200 (C4.3) and multiplier x."""
     base = {"equal": (50,) * 6, "mix6": (50,) * 6, "long-only": (0, 0, 100, 100, 100, 100),
             "short-skew": (100, 100, 100, 50, 50, 50)}
+    app_ref = None
     if name.startswith("game"):
         r = (6, 0, 1, 0, 0, 0)
         base_r = [v * 100 for v in r]
+        app_ref = "resnet50"           # app SLO = ResNet-50's (P:791-792)
     elif name.startswith("traffic"):
         base_r = [0, 100, 0, 100, 100, 0]
+        app_ref = "ssd_mobilenet_v1"   # app SLO = SSD's 136 ms (P:791-792)
     else:
         base_r = list(base[name])
+    if app_ref is not None:
+        # an application keeps its composition (P:787-790: 6 LeNet + 1 ResNet per
+        # game request): one B200 scale for all its models, the app-SLO model's
+        s = PAPER_SLO_MS[app_ref] * 1000.0 / slo_us[MODELS.index(app_ref)]
+        return [int(r * s * x) for r in base_r]
     out = []
     for m, r in enumerate(base_r):
         ref = MODELS[m] if MODELS[m] in PAPER_SLO_MS else "resnet50"

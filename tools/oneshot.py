@@ -22,10 +22,13 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--n_sm", type=int, default=0)
     ap.add_argument("--json", default="")
+    ap.add_argument("--flags", type=int, default=0, help="executor dbg_flags (tuning experiments)")
     a = ap.parse_args()
     import torch
     from paper_2109_01611_b200 import gpulet
     ctx = gpulet.Context(1)
+    if a.flags:
+        gpulet.Context.set_tuning(2, a.flags)
     mid = ctx.load_model(0, a.model, synthgen.weight_file(a.model))
     x = common.device_input(a.model, a.batch)
     y = torch.empty(ctx.model_io(mid, a.batch)[1] // 4, device="cuda")
