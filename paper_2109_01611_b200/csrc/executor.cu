@@ -81,6 +81,7 @@ struct Pipe {
   uint32_t att_phase = 0;         // attention barrier parity (every thread tracks it)
   int npend = 0;
   uint32_t pend[kLag];
+  int fix = 0;                    // a GEMM step ended: apply its tile / k-block counts after the barrier
 };
 
 __device__ __forceinline__ uint32_t par(const Pipe& p) { return (p.bits >> p.stage) & 1u; }
@@ -185,7 +186,7 @@ __device__ __forceinline__ void res_request(uint8_t* stg, const __nv_bfloat16* r
 // (TMEM already waited), sb the chunk's fp32 bias (smem), the lane's staging
 // row the chunk's residual (RES).  Returns the bf16 results in o.
 template <int ACT, bool RES>
-__device__ __forceinline__ void epi_half(const uint32_t (&v)[16], const float* sb, bool has_bias, const uint4& r0,
+__device__ __forceinline__ void epi_half(const uint32_t (&v)[16], uint32_t sb, bool has_bias, const uint4& r0,
                                          const uint4& r1, int h, uint4 (&o)[2]) {
   float x[16];
 #pragma unroll
@@ -193,7 +194,7 @@ __device__ __forceinline__ void epi_half(const uint32_t (&v)[16], const float* s
   if (has_bias) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float4 b = ((const float4*)(sb + h * 16))[k];   // broadcast
+      const float4 b = lds_f4(sb + h * 64 + k * 16);   // broadcast
       x[4 * k] += b.x, x[4 * k + 1] += b.y, x[4 * k + 2] += b.z, x[4 * k + 3] += b.w;
     }
   }
@@ -230,7 +231,7 @@ __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, c
   const int64_t coff = e.col_off;
   const int M = g.M;
   const int sr = lane >> 2, seg = lane & 3;
-  uint8_t* srow = stg + lane * kEpiRowBytes;
+  const uint32_t srow = smem_u32(stg) + lane * kEpiRowBytes, sstg = smem_u32(stg), sbs = smem_u32(sb);
   uint32_t va[16], vb[16];
   tmem_ld16_issue(taddr, va);
   tmem_wait_ld16(va);
@@ -246,15 +247,15 @@ __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, c
       cp_async_wait<0>();
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 4; ++k) rr[k] = ((const uint4*)srow)[k];
+      for (int k = 0; k < 4; ++k) rr[k] = lds128(srow + k * 16);
       __syncwarp();
       if (direct && j + 1 < nfull) res_request(stg, rsd, row0, M, ldc, coff + n0 + 32, lane);
     }
     uint4 oa[2], ob[2];
-    epi_half<ACT, RES>(va, sb + j * 32, has_bias, rr[0], rr[1], 0, oa);
+    epi_half<ACT, RES>(va, sbs + j * 128, has_bias, rr[0], rr[1], 0, oa);
     tmem_wait_ld16(vb);
     if (j + 1 < nfull) tmem_ld16_issue(taddr + (j + 1) * 32, va);
-    epi_half<ACT, RES>(vb, sb + j * 32, has_bias, rr[2], rr[3], 1, ob);
+    epi_half<ACT, RES>(vb, sbs + j * 128, has_bias, rr[2], rr[3], 1, ob);
     if (direct) {
       // this lane's row: 64 contiguous bytes
       if (row0 + lane < M && !nostore) {
@@ -263,13 +264,13 @@ __device__ __forceinline__ void epi_rows(const Epilogue& e, const GemmArgs& g, c
       }
     } else {
       __syncwarp();
-      ((uint4*)srow)[0] = oa[0], ((uint4*)srow)[1] = oa[1], ((uint4*)srow)[2] = ob[0], ((uint4*)srow)[3] = ob[1];
+      sts128(srow, oa[0]), sts128(srow + 16, oa[1]), sts128(srow + 32, ob[0]), sts128(srow + 48, ob[1]);
       __syncwarp();
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
         const int rw = it * 8 + sr;
         if (row0 + rw < M && !nostore)
-          *(uint4*)(outp + (row0 + rw) * ldc + coff + n0 + seg * 8) = *(const uint4*)(stg + rw * kEpiRowBytes + seg * 16);
+          *(uint4*)(outp + (row0 + rw) * ldc + coff + n0 + seg * 8) = lds128(sstg + rw * kEpiRowBytes + seg * 16);
       }
       __syncwarp();
       if (RES && j + 1 < nfull) res_request(stg, rsd, row0, M, ldc, coff + n0 + 32, lane);
@@ -500,9 +501,6 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
     return;
   }
   if (e.splitk > 1) {
-    // split-K: this split's fp32 partial tile -> ws[split][R][Cc] in OUTPUT
-    // order (R x Cc = M x N, or N x M for swap-AB), L2-only stores; an
-    // OP_SPLITK_FINAL step reduces the splits in order.
     const int split = kb0 / g.kb_per_split;
     for (int j = c0; j < c1; j += 32) {
       float v[32];
@@ -795,18 +793,27 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     }
     if (q == 0 && half == 0 && lane == 0) dbg_mark(S, 5);
   }
-  // this CTA's tile and k-block counts, counted by the MMA warp as it walked them
-  __syncthreads();
+  // The ring / accumulator state every thread must leave the step with depends
+  // on this CTA's tile and k-block counts, which the MMA warp counted as it
+  // walked them; gemm_finish() applies them after the gpu-let barrier, whose
+  // __syncthreads makes the counts visible (no extra CTA barrier here).
+  P.bits = bits0;
+  P.acc = acc0;
+  P.fix = 1;
+  Pio = P;
+}
+
+__device__ __forceinline__ void gemm_finish(Pipe& P, const Smem& S) {
   const int my_tiles = S.opn[kOpCache], my_kb = S.opn[kOpCache + 1];
   uint32_t flips = 0;
   for (uint32_t st = 0; st < P.nst; ++st) {
     const uint32_t uses = my_kb / P.nst + (st < my_kb % P.nst ? 1u : 0u);
     flips |= (uses & 1u) << st;
   }
-  P.bits = bits0 ^ flips;
+  P.bits ^= flips;
   P.stage = 0;
-  P.acc = acc0 + my_tiles;
-  Pio = P;
+  P.acc += my_tiles;
+  P.fix = 0;
 }
 
 // ------------------------------------------------------------------ split-K final
@@ -1526,6 +1533,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     fence_proxy_async_smem();
     if (threadIdx.x == 0) dbg_mark(S, 6);
     gridsync(st, epoch, false);
+    if (P.fix) gemm_finish(P, S);
     if (threadIdx.x == 0) dbg_mark(S, 7);
     ++step;
     if (tr && step < trace_cap) trace[step] = globaltimer();

@@ -1209,6 +1209,12 @@ namespace gl {
 // workspace (TMA descriptors hold absolute addresses).
 bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::string& err) {
   out = p.ops;
+  for (size_t i = 0; i < out.size();) {   // step extents, read by the executor when it stages a step's args
+    size_t j = i;
+    while (j + 1 < out.size() && !out[j].step_end) ++j;
+    for (size_t k = i; k <= j; ++k) out[k].step_nops = (k == i) ? (int32_t)(j - i + 1) : 0;
+    i = j + 1;
+  }
   Err e;
   for (OpDesc& op : out) {
     if (op.type == OP_ATTENTION && op.g.act_tmap) {

@@ -97,7 +97,7 @@ struct alignas(128) OpDesc {
   int32_t type;
   int32_t step_end;             // 1: gpu-let barrier after this op
   int32_t n_units;              // work units (tiles) of this op
-  int32_t pad_;
+  int32_t step_nops;            // first op of a step: the step's op count (set at bind time; diagnostics)
   uint64_t pf_addr;             // read-only operand (weights) prefetched into L2 one step ahead (0: none)
   uint64_t pf_bytes;
   GemmArgs g;

@@ -235,6 +235,25 @@ __device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
   for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(r[i]));   // uses of r stay after the wait
 }
 
+// ---------------------------------------------------------------- explicit shared-space vectors
+// (generic pointers to shared memory compile to LD.E / ST.E; these are LDS / STS)
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------- scoped memory ops
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const volatile uint64_t* p) {
   uint64_t v;
