@@ -269,6 +269,14 @@ class Server:
                                    self.coeffs)
         return rates, dump, ok
 
+    def plan_rates(self, rates, n_gpus=1, mode="gpulet"):
+        """Plan for explicit per-model rates (periodic rescheduling, tools/adapt.py)."""
+        from paper_2109_01611_b200 import gpulet
+        from tools import common
+        dump, ok = gpulet.schedule(common.MODELS, self.lat, self.l2, self.mem, self.slo, list(rates), n_gpus, mode,
+                                   self.coeffs)
+        return list(rates), dump, ok
+
     def max_sched_x(self, scen, mode, n_gpus):
         lo, hi = 0.0, 0.25
         while self.plan(scen, mode, n_gpus, hi)[2] and hi < 1e6:
