@@ -105,6 +105,8 @@ gl_status gl_gpulet_smids(gl_ctx* ctx, int32_t gpulet_id, int32_t* smids, int32_
  * (layouts as gl_model_io), owned by the caller and valid until the ticket is polled.
  * slo_ms is recorded for accounting only.  Out: *ticket.
  * Errors: GL_E_ARG, GL_E_CAPACITY, GL_E_MODEL, GL_E_STATE, GL_E_QUEUE_FULL. */
+/* in_dev / out_dev: device memory of the gpu-let's GPU, or pinned host memory (UVA-mapped; the
+ * executor reads / writes it over PCIe). */
 gl_status gl_submit_batch(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, const void* in_dev, void* out_dev,
                           int32_t batch, float slo_ms, uint64_t* ticket);
 /* Collect up to `max` completions across all gpu-lets (non-blocking); FIFO per
@@ -168,7 +170,9 @@ typedef struct {
  * inputs are copied H2D (asynchronously, on a per-lane stream, contiguous slots
  * coalesced into one copy) and it is submitted when the copy has landed; on
  * completion its outputs are copied D2H the same way and the requests complete
- * when that copy has landed, so the latency includes both copies.  A lane keeps
+ * when that copy has landed, so the latency includes both copies.  Requests of
+ * at most 64 KB in and out whose batch occupies contiguous slots skip the
+ * copies: the executor reads / writes the pinned ring directly (UVA).  A lane keeps
  * one batch in flight, two with in_dev2/out_dev2.  *h2d_bytes / *d2h_bytes (may
  * be NULL) return the bytes copied; lane_stats (may be NULL; n_lanes entries) the
  * per-lane execution record.  The frontend thread never blocks on a copy.

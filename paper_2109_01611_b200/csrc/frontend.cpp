@@ -17,6 +17,9 @@
 //        complete when that copy's event has completed.
 // A lane has one or two device buffers (in_dev2), i.e. one or two batches in
 // flight: with two, the copy of the next batch overlaps the current one's run.
+// Small requests (kZeroCopyMax) skip both copies: the executor reads the
+// contiguous host-ring slots of the batch and writes its outputs there itself
+// (pinned memory, UVA); the bytes still cross PCIe and are counted.
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -29,6 +32,11 @@
 
 namespace {
 enum Stage { FREE = 0, H2D, RUN, D2H };
+// Requests at most this large (in and out) skip the copy stages: a batch of
+// contiguous host-ring slots is handed to the executor as UVA-mapped pinned
+// memory (LeNet 1.6 KB, BERT 512 B: a copy's fixed latency is most of their
+// SLO); larger ones go through the async copy path.
+constexpr int64_t kZeroCopyMax = 64 * 1024;
 
 struct Batch {
   Stage stage = FREE;
@@ -36,6 +44,7 @@ struct Batch {
   std::vector<int64_t> slots;  // their host slots (end-to-end mode)
   cudaEvent_t ev = nullptr;
   uint64_t ticket = 0;
+  bool zero_copy = false;      // inputs / outputs read / written in the host ring by the executor
 };
 
 struct Inflight {
@@ -50,6 +59,7 @@ struct LaneState {
   int64_t window_us = 0;
   int64_t cur = 0;        // smooth WRR credit
   int nbuf = 1;           // device buffers (batches in flight)
+  bool zero_copy = false; // requests small enough for the executor to read / write the host ring directly
   Batch buf[2];
   cudaStream_t stream = nullptr;
   const void* in_dev(int b) const { return b ? cfg.in_dev2 : cfg.in_dev; }
@@ -116,6 +126,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       if (!lanes[i].out_host || lanes[i].in_req_bytes <= 0 || lanes[i].out_req_bytes <= 0 || lanes[i].host_slots < 1)
         return GL_E_ARG;
       L[i].nbuf = (lanes[i].in_dev2 && lanes[i].out_dev2) ? 2 : 1;
+      L[i].zero_copy = lanes[i].in_req_bytes <= kZeroCopyMax && lanes[i].out_req_bytes <= kZeroCopyMax;
       if (cudaStreamCreateWithFlags(&L[i].stream, cudaStreamNonBlocking) != cudaSuccess) return GL_E_CUDA;
       for (int b = 0; b < L[i].nbuf; ++b)
         if (cudaEventCreateWithFlags(&L[i].buf[b].ev, cudaEventDisableTiming) != cudaSuccess) return GL_E_CUDA;
@@ -199,6 +210,31 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
         bt.reqs.assign(ln.q.begin(), ln.q.begin() + k);
         bt.slots.resize(k);
         for (int i = 0; i < k; ++i) bt.slots[i] = seq_of[bt.reqs[i]] % ln.cfg.host_slots;
+        bool contiguous = true;
+        for (int i = 1; i < k; ++i) contiguous &= bt.slots[i] == bt.slots[0] + i;
+        if (ln.zero_copy && contiguous) {
+          // small requests: the executor reads the inputs from / writes the
+          // outputs to the pinned host ring itself (UVA-mapped), no copy stage
+          const char* in = (const char*)ln.cfg.in_host + bt.slots[0] * ln.cfg.in_req_bytes;
+          char* out = (char*)ln.cfg.out_host + bt.slots[0] * ln.cfg.out_req_bytes;
+          uint64_t ticket = 0;
+          const gl_status s = gl_submit_batch(ctx, ln.cfg.gpulet, ln.cfg.model_id, in, out, k,
+                                              (float)slo_us[ln.cfg.model_slot] / 1000.f, &ticket);
+          if (s == GL_E_QUEUE_FULL) {   // retry next iteration (the requests are still queued)
+            bt.reqs.clear();
+            bt.slots.clear();
+            continue;
+          }
+          if (s != GL_OK) return s;
+          h2d += (int64_t)k * ln.cfg.in_req_bytes;
+          bt.zero_copy = true;
+          bt.ticket = ticket;
+          bt.stage = RUN;
+          inflight.emplace(ticket, Inflight{li, b, {}});
+          ln.q.erase(ln.q.begin(), ln.q.begin() + k);
+          continue;
+        }
+        bt.zero_copy = false;
         ln.q.erase(ln.q.begin(), ln.q.begin() + k);
         if (!copy_slots((void*)ln.in_dev(b), ln.cfg.in_host, bt.slots, ln.cfg.in_req_bytes, true, ln.stream, &h2d) ||
             cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
@@ -267,6 +303,11 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       }
       inflight.erase(it);
       Batch& bt = ln.buf[b];
+      if (bt.zero_copy) {   // outputs already in the host ring
+        d2h += (int64_t)bt.reqs.size() * ln.cfg.out_req_bytes;
+        complete(bt, now_us(), outstanding);
+        continue;
+      }
       if (!copy_slots(ln.out_dev(b), ln.cfg.out_host, bt.slots, ln.cfg.out_req_bytes, false, ln.stream, &d2h) ||
           cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
         return GL_E_CUDA;
