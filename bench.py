@@ -231,6 +231,7 @@ class Server:
     gpu-lets of the current plan."""
 
     HOST_SLOTS = 64
+    HOST_SLOTS_SMALL = 1024
 
     def __init__(self, ctx, gpu, prof, e2e):
         import torch
@@ -240,6 +241,7 @@ class Server:
         self.mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
         self.x, self.y, self.xh, self.yh, self.req_bytes = {}, {}, {}, {}, {}
         self.x2, self.y2 = {}, {}
+        self.host_slots = {}
         self.cost = {}
         for m in common.MODELS:
             inb, outb = ctx.model_io(self.mids[m], 32)
@@ -254,12 +256,17 @@ class Server:
                 for slot in (0, 1):
                     self.x2[m, slot] = common.device_input(m, 32)
                     self.y2[m, slot] = torch.empty(outb // 4, device="cuda")
+                # per-model pinned request ring: deep for small requests (their
+                # batches stay contiguous -> zero-copy path), 64 slots otherwise
+                ns = self.HOST_SLOTS_SMALL if max(inb, outb) // 32 <= 64 * 1024 else self.HOST_SLOTS
+                self.host_slots[m] = ns
                 h = common.host_input(m, 32)
-                reps = [h] * (self.HOST_SLOTS // 32)
+                reps = [h] * (ns // 32)
                 self.xh[m] = torch.cat(reps).pin_memory()
-                self.yh[m] = torch.empty(self.HOST_SLOTS * (outb // 32) // 4, dtype=torch.float32).pin_memory()
+                self.yh[m] = torch.empty(ns * (outb // 32) // 4, dtype=torch.float32).pin_memory()
         torch.cuda.current_stream().synchronize()
         self.made, self.lanes = [], []
+        self.made_sizes, self.made_nsm, self.reorganised = None, [], False
 
     def plan(self, scen, mode, n_gpus, x):
         from paper_2109_01611_b200 import gpulet
@@ -288,18 +295,29 @@ class Server:
                 break
         return lo
 
-    def setup(self, dump, rank):
+    def setup(self, dump, rank, reuse=False):
         """Create this GPU's gpu-lets of the plan and build its lanes; returns
-        the per-model arrival rates this rank must serve."""
+        the per-model arrival rates this rank must serve.  reuse: when the plan
+        keeps this GPU's gpu-let sizes, keep the live gpu-lets and only re-plan
+        the lanes (batch, duty cycle, routing weights are frontend parameters);
+        self.reorganised says whether gpu-lets were rebuilt."""
         from tools import common
-        self.teardown()
         gls, _ = common.parse_plan(dump)
         used = [g for g in sorted(gls, key=lambda d: d["slot"]) if g["lanes"] and g["gpu"] == rank]
+        sizes = [g["size"] for g in used]
+        if reuse and self.made and sizes == getattr(self, "made_sizes", None):
+            made = list(zip(self.made, self.made_nsm))
+            self.lanes = []
+            self.reorganised = False
+        else:
+            self.teardown()
+            self.reorganised = True
+            made = self.ctx.create_gpulets(self.gpu, sizes) if used else []
+            self.made = [gid for gid, _n in made]
+            self.made_sizes, self.made_nsm = sizes, [n for _g, n in made]
         my_rates = [0] * len(common.MODELS)
         if not used:
             return my_rates
-        made = self.ctx.create_gpulets(self.gpu, [g["size"] for g in used])
-        self.made = [gid for gid, _n in made]
         for g, (gid, nsm) in zip(used, made):
             for ln in g["lanes"]:
                 m = ln["model"]
@@ -310,7 +328,7 @@ class Server:
                                        duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.x[m, g["slot"]],
                                        y=self.y[m, g["slot"]], x_host=self.xh.get(m), y_host=self.yh.get(m),
                                        x2=self.x2.get((m, g["slot"])), y2=self.y2.get((m, g["slot"])),
-                                       in_req_bytes=ib, out_req_bytes=ob, host_slots=self.HOST_SLOTS,
+                                       in_req_bytes=ib, out_req_bytes=ob, host_slots=self.host_slots.get(m, self.HOST_SLOTS),
                                        size=g["size"], sm=nsm, model=m))
                 my_rates[mi] += ln["rate"]
         return my_rates
@@ -319,6 +337,7 @@ class Server:
         for gid in self.made:
             self.ctx.destroy_gpulet(gid)
         self.made, self.lanes = [], []
+        self.made_sizes, self.made_nsm = None, []
 
     def window(self, rates, secs, seed, e2e=False):
         """One serving window of Poisson traffic at `rates` through gl_serve."""
@@ -404,13 +423,18 @@ def search(srv, dist, rank, world, scen, mode, a, x0, e2e):
         rates, dump, ok = srv.plan(scen, mode, world, x)
         w = None
         if ok and sum(rates) > 0:
+            # median violation rate of three runs ("iterate the experiment
+            # three times ... and pick the median SLO violation rate")
             my = srv.setup(dump, rank)
-            w = srv.window(my, a.probe_window, (5000 if e2e else 1000) + it, e2e=e2e)
+            runs = []
+            for rep in range(3):
+                w = srv.window(my, a.probe_window, (5000 if e2e else 1000) + 10 * it + rep, e2e=e2e)
+                arr_r, viol_r = allsum(dist, [w["arrivals"], w["viol"]])
+                runs.append((viol_r / arr_r if arr_r else 1.0, arr_r, viol_r))
             srv.teardown()
-            arr, viol = allsum(dist, [w["arrivals"], w["viol"]])
+            frac, arr, viol = sorted(runs)[1]
         else:
-            arr, viol = 0, 1
-        frac = viol / arr if arr else 1.0
+            arr, viol, frac = 0, 1, 1.0
         probes.append({"x": round(x, 4), "viol_frac": round(frac, 4),
                        "viol_by_model": {k: v["viol"] for k, v in (w["per"] if w else {}).items() if v["viol"]}})
         log(f"[{scen}/{mode}{'/e2e' if e2e else ''}] probe x={x:.4f} viol={frac:.4f}")
@@ -616,7 +640,7 @@ def main():
     ap.add_argument("--mode", default="gpulet", choices=["gpulet", "gpulet+int", "sbp"])
     ap.add_argument("--scenario", default="game")
     ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
-    ap.add_argument("--probe-window", type=float, default=0.5)
+    ap.add_argument("--probe-window", type=float, default=0.3, help="seconds per probe run (3 runs per probe)")
     ap.add_argument("--probes", type=int, default=6)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
