@@ -175,7 +175,8 @@ typedef struct {
  * copies: the executor reads / writes the pinned ring directly (UVA).  A lane keeps
  * one batch in flight, two with in_dev2/out_dev2.  *h2d_bytes / *d2h_bytes (may
  * be NULL) return the bytes copied; lane_stats (may be NULL; n_lanes entries) the
- * per-lane execution record.  The frontend thread never blocks on a copy.
+ * per-lane execution record.  The frontend thread never blocks on a copy
+ * (GL_SERVE_RT=1: it runs SCHED_FIFO priority 10 during the call when permitted).
  * Blocks until every request is completed or dropped.  Errors: GL_E_ARG,
  * GL_E_TIMEOUT, GL_E_CUDA, errors of submit/poll. */
 /* Per-lane execution record of one gl_serve call: batches and requests run, and

@@ -52,6 +52,7 @@ struct Smem {
   uint8_t* scratch;  // non-GEMM ops reuse the stage area
   uint64_t* att;     // attention barriers: [0] Q/K/V landed, [1] S = QK^T done, [2] O = PV done
   int* epi_flag;     // epilogue broadcast word (split-K last arriver)
+  volatile uint64_t* wtag;   // global address of the LeNet parameters resident in scratch (0: none)
   uint8_t* estage;   // epilogue staging: 4 warps x 32 rows x kEpiRowBytes (coalesced stores)
   uint64_t* dbg;     // optional per-step role stamps of CTA 0 (one-shot trace mode)
   int step;          // current step index (for dbg)
@@ -1046,7 +1047,7 @@ __device__ __noinline__ void avgpool(const OpDesc* op, const Ctx& X) {
 // ------------------------------------------------------------------ LeNet-5 fused (K7)
 __device__ __forceinline__ float bfr(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
-__device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch) {
+__device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scratch, volatile uint64_t* wtag) {
   // One CTA per image (grid-stride); the packed bf16 parameters (123 KB) are
   // staged in shared memory once per CTA, activations stay in shared memory
   // in fp32 (rounded to bf16 where the oracle rounds: after each ReLU, C1.4).
@@ -1057,7 +1058,15 @@ __device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scra
   float* y = (float*)res(a.y, X);
   constexpr int kParams = 61706, kParamVec = (kParams + 7) / 8;
   __nv_bfloat16* W = (__nv_bfloat16*)scratch;
-  for (int i = threadIdx.x; i < kParamVec; i += blockDim.x) ((uint4*)W)[i] = __ldg((const uint4*)Wg + i);
+  // The parameters stay resident in shared memory across batches while only
+  // LeNet runs on this gpu-let (wtag = the global address they were staged
+  // from; any other op clears it, run_program): a steady LeNet lane reads
+  // 123 KB per CTA once instead of once per batch.
+  if (*wtag != (uint64_t)(uintptr_t)Wg) {
+    for (int i = threadIdx.x; i < kParamVec; i += blockDim.x) ((uint4*)W)[i] = __ldg((const uint4*)Wg + i);
+    __syncthreads();
+    if (threadIdx.x == 0) *wtag = (uint64_t)(uintptr_t)Wg;
+  }
   const __nv_bfloat16 *w1 = W, *b1 = w1 + 150, *w2 = b1 + 6, *b2 = w2 + 2400, *f1 = b2 + 16, *fb1 = f1 + 48000,
                       *f2 = fb1 + 120, *fb2 = f2 + 10080, *f3 = fb2 + 84, *fb3 = f3 + 840;
   float* img = (float*)(scratch + kParamVec * 16);   // 28*28
@@ -1500,7 +1509,7 @@ __device__ void run_misc(const OpDesc* op, const Ctx& X, const Smem& S, Pipe& P)
     case OP_DWCONV: dwconv(op, X, S.scratch); break;
     case OP_MAXPOOL: maxpool(op, X); break;
     case OP_AVGPOOL: avgpool(op, X); break;
-    case OP_LENET: lenet(op, X, S.scratch); break;
+    case OP_LENET: lenet(op, X, S.scratch, S.wtag); break;
     case OP_EMBED_LN: embed_ln(op, X); break;
     case OP_LAYERNORM: layernorm(op, X); break;
     case OP_ATTENTION: attention(op, X, S.scratch); break;
@@ -1522,6 +1531,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     int j = i;
     while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
     S.step = step;
+    if (threadIdx.x == 0 && w.prog[i].type != OP_LENET) *S.wtag = 0;   // smem scratch / ring reused
     const int n_next = min(kPfOps, w.n_ops - j - 1);
     prefetch_desc(w.prog + j + 1, n_next);
     if (w.prog[i].type == OP_GEMM) {
@@ -1560,6 +1570,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.att = bars + 2 * kMaxStages + 4;
   S.tmem_base = (uint32_t*)(bars + 2 * kMaxStages + 7);
   S.epi_flag = (int*)(bars + 2 * kMaxStages + 8);
+  S.wtag = bars + 2 * kMaxStages + 10;
   S.estage = base + kRingBytes + 1024;
   S.scratch = base;
   S.dbg = nullptr;
@@ -1582,6 +1593,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
       mbar_init(&S.tempty[s], 8);   // one arrival per epilogue warp (count 2 each when only 4 run)
     }
     for (int s = 0; s < 3; ++s) mbar_init(&S.att[s], 1);
+    *S.wtag = 0;
     fence_mbar_init();
   }
   if (warp == 8) tmem_alloc(S.tmem_base, 512);

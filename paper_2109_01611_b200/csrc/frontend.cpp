@@ -22,8 +22,12 @@
 // (pinned memory, UVA); the bytes still cross PCIe and are counted.
 #include <cuda_runtime.h>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <deque>
 #include <unordered_map>
 #include <vector>
@@ -97,6 +101,27 @@ bool copy_slots(void* dev, const void* host, const std::vector<int64_t>& slots, 
   return true;
 }
 
+// Optional (GL_SERVE_RT=1): run the busy-polling frontend loop SCHED_FIFO for
+// the duration of the call when the process may (root / CAP_SYS_NICE).  Off by
+// default: measured no better than the default policy on the B200 boxes
+// (profiles/ab_r1r_*.log).
+struct RtGuard {
+  int policy = 0;
+  sched_param old{};
+  bool set = false;
+  RtGuard() {
+    const char* e = std::getenv("GL_SERVE_RT");
+    if (!e || e[0] != '1') return;
+    if (pthread_getschedparam(pthread_self(), &policy, &old) != 0) return;
+    sched_param p{};
+    p.sched_priority = 10;
+    set = pthread_setschedparam(pthread_self(), SCHED_FIFO, &p) == 0;
+  }
+  ~RtGuard() {
+    if (set) pthread_setschedparam(pthread_self(), policy, &old);
+  }
+};
+
 struct Cleanup {
   std::vector<LaneState>& L;
   ~Cleanup() {
@@ -118,6 +143,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
     return GL_E_ARG;
   std::vector<LaneState> L(n_lanes);
   Cleanup cleanup{L};
+  RtGuard rt;
   std::vector<std::vector<int>> by_model(n_models);
   for (int i = 0; i < n_lanes; ++i) {
     L[i].cfg = lanes[i];
