@@ -655,6 +655,9 @@ def main():
     if a.impl == "reference":
         line = reference_arm(a, world, rank)
     else:
+        if world > 1:
+            import torch
+            torch.cuda.set_device(local)   # this rank's GPU before the NCCL communicator exists
         dist = init_dist(world, "nccl")
         line = our_arm(a, world, rank, local, dist)
     if line is not None and rank == 0:
