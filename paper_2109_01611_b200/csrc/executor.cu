@@ -28,7 +28,21 @@ struct Ctx {
   const char* in;
   char* out;
   char* ws;
+  uint32_t* cnt;   // the program's completion counters (barrier-free GEMM step joins)
 };
+
+// Wait until counter *p reaches `need` (acquire, gpu scope).  A join whose
+// producer never completes is a bug: trap after 20 s instead of hanging.
+__device__ __noinline__ void wait_count(const uint32_t* p, uint32_t need) {
+  uint32_t ns = 64;
+  uint64_t t0 = 0;
+  while (ld_acquire_gpu_u32(p) < need) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (t0 == 0) t0 = globaltimer();
+    else if (globaltimer() - t0 > 20ull * 1000000000ull) __trap();
+  }
+}
 
 __device__ __forceinline__ char* res(const BufRef& b, const Ctx& c) {
   switch (b.kind) {
@@ -462,6 +476,31 @@ __device__ __forceinline__ uint32_t stage_bytes_for(int bn) {
   return (uint32_t)kStageBytesA + (uint32_t)((bn * 128 + 1023) & ~1023);
 }
 
+// Barrier-free step join: wait until the producer M blocks holding the A rows
+// of tile mb are complete (acquire by the issuing lane; then the async proxy --
+// the TMA it issues next -- is ordered after the generic stores it observed).
+__device__ __forceinline__ void wait_a_rows(const GemmArgs& g, const Ctx& X, int mb) {
+  const uint32_t* c = X.cnt + g.dep_a_off;
+  const uint32_t need = (uint32_t)g.dep_a_need;
+  const int m0 = mb * 128, m1 = min(g.M, m0 + 128) - 1;
+  int lo, hi;
+  if (g.a_tma == SRC_TMA) {   // [rows, C]: the producer's own rows
+    lo = m0 / 128;
+    hi = m1 / 128;
+  } else {                    // im2col over NHWC [n, H, W, C]: the input rows the window touches
+    const Gather& q = g.ga;
+    const int HoWo = q.Ho * q.Wo;
+    const int n0 = m0 / HoWo, ho0 = (m0 - n0 * HoWo) / q.Wo;
+    const int n1 = m1 / HoWo, ho1 = (m1 - n1 * HoWo) / q.Wo;
+    const int h_lo = max(0, ho0 * q.stride - q.pad), h_hi = min(q.H - 1, ho1 * q.stride - q.pad + q.KH - 1);
+    lo = ((n0 * q.H + h_lo) * q.W) / 128;
+    hi = ((n1 * q.H + h_hi) * q.W + q.W - 1) / 128;
+  }
+  hi = min(hi, g.dep_a_mblk - 1);
+  for (int k = lo; k <= hi; ++k) wait_count(c + k, need);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Epilogue of one warp over the tile columns [c0, c1) (relative to the tile).
 // Waits for the accumulator itself (tfull / parity) after issuing the loads
 // that do not depend on it (bias, first residual chunk).
@@ -470,6 +509,10 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
                                               uint64_t* tfull, uint32_t parity, float* sb, uint32_t key,
                                               uint32_t& bkey) {
   const Epilogue& e = g.ep;
+  if (g.dep_r_off) {   // residual rows written? (lane 0 acquires; the warp barrier orders the others' reads)
+    if (lane == 0) wait_count(X.cnt + g.dep_r_off + mb, (uint32_t)g.dep_r_need);
+    __syncwarp();
+  }
   const int m = mb * 128 + q * 32 + lane;
   const int nend = min(g.N, (nb + 1) * g.BN);
   c1 = min(c1, nend - nb * g.BN);
@@ -672,6 +715,10 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         ich = ho * g.ga.stride - g.ga.pad;
         icw = wo * g.ga.stride - g.ga.padw;
       }
+      if (g.dep_a_off) {   // barrier-free join: this tile's A rows complete (lane 0 issues the TMA)
+        if (lane == 0) wait_a_rows(g, X, mb);
+        __syncwarp();
+      }
       const uint32_t tx = 128 * 128 + g.BN * 128;
       const bool a2d = g.a_tma == SRC_TMA;
       const Im2colGeo q = im2col_geo(g);
@@ -785,6 +832,10 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
       epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane, &S.tfull[acc], use & 1, sbias,
                     ((uint32_t)oi << 16) | (uint32_t)nb, bkey);
+      if (g.pub_off) {   // this warp's stores of the tile are done: one release per warp
+        __syncwarp();
+        if (lane == 0) red_release_gpu_add_u32(X.cnt + g.pub_off + mb, 1u);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cnt(&S.tempty[acc], arrive_n);
@@ -1542,13 +1593,20 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     }
     fence_proxy_async_smem();
     if (threadIdx.x == 0) dbg_mark(S, 6);
-    gridsync(st, epoch, false);
+    if (w.prog[j].local_next)
+      __syncthreads();   // the next GEMM step waits per M block on completion counters
+    else
+      gridsync(st, epoch, false);
     if (P.fix) gemm_finish(P, S);
     if (threadIdx.x == 0) dbg_mark(S, 7);
     ++step;
     if (tr && step < trace_cap) trace[step] = globaltimer();
     i = j + 1;
   }
+  // every increment of this run happened before the final gpu-let barrier:
+  // re-zero the counters for the next run (ordered before it by its dequeue barrier)
+  const int cw = w.n_ops > 0 ? w.prog[0].cnt_words : 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < cw; k += gridDim.x * blockDim.x) X.cnt[k] = 0u;
 }
 
 }  // namespace
@@ -1660,7 +1718,7 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
       w.t_submit_ns = c->t_submit_ns;
     }
     const uint64_t t_start = globaltimer();
-    Ctx X{(const char*)w.in, (char*)w.out, p.ws};
+    Ctx X{(const char*)w.in, (char*)w.out, p.ws, (uint32_t*)(uintptr_t)w.prog[0].cnt_base};
     run_program(w, X, S, P, p.st, epoch, p.trace, p.trace_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t i = p.ring->heartbeat;

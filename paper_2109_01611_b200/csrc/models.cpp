@@ -7,6 +7,8 @@
 // tensor maps and plans the activation workspace (liveness-based first fit).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -279,9 +281,12 @@ class Builder {
   void release_off(uint64_t off) { pending.push_back(off); }
   void step() {
     if (!prog.ops.empty()) prog.ops.back().step_end = 1;
-    for (uint64_t off : pending)
-      for (auto& bl : blocks)
-        if (bl.off == off) bl.free = true;
+    // with barrier-free GEMM step joins (dataflow_enabled) a buffer may still be
+    // read by a slower CTA while a faster one runs ahead: no reuse within a program
+    if (!dataflow_enabled() || std::getenv("GL_DATAFLOW_UNSAFE_REUSE"))   // (unsafe: timing experiments only)
+      for (uint64_t off : pending)
+        for (auto& bl : blocks)
+          if (bl.off == off) bl.free = true;
     pending.clear();
     for (size_t i = 0; i + 1 < blocks.size();) {
       if (blocks[i].free && blocks[i + 1].free) {
@@ -1017,6 +1022,131 @@ static void build_bert(Builder& B, size_t& in_b, size_t& out_b) {
   out_b = (size_t)b * 2 * 4;
 }
 
+// ------------------------------------------------------------------ barrier-free GEMM step joins
+// A step boundary between two GEMM steps whose operands all come by TMA can be
+// CTA-local (no gpu-let barrier) when every workspace operand the second step
+// reads -- its A operand and its residual -- was either complete before the
+// last full barrier or written by a single full-width GEMM op that publishes
+// per-M-block completion counters; the reader then waits for exactly the M
+// blocks it needs.  Off by default (GL_DATAFLOW=1 enables): correct (the GPU
+// parity suite passes with it) but measured no faster -- ResNet-50 / BERT equal
+// with workspace reuse, 3-4 % slower without it (the reuse it needs to be safe),
+// VGG-16 12 % slower (profiles/ab_r1x_dataflow.log): the per-step cost is the
+// dependency chain of the slowest tiles, not the barrier itself.
+bool dataflow_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("GL_DATAFLOW");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return on != 0;
+}
+
+static bool publishes(const OpDesc& op) {
+  const GemmArgs& g = op.g;
+  const Epilogue& e = g.ep;
+  return op.type == OP_GEMM && g.splits <= 1 && e.splitk <= 1 && !e.transpose && !e.out_fp32 &&
+         e.out.kind == BUF_WS && e.rows_per_img >= g.M && e.col_off == 0 && e.ldc == g.N;
+}
+
+static bool tma_gemm(const OpDesc& op) {
+  return op.type == OP_GEMM && op.g.a_tma != SRC_GATHER && op.g.b_tma != SRC_GATHER && !op.g.ep.transpose;
+}
+
+void plan_dataflow(Program& p) {
+  auto& ops = p.ops;
+  const int n = (int)ops.size();
+  if (!dataflow_enabled() || n == 0) return;
+  std::vector<int> step_of(n), first;
+  int s = 0;
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 || ops[i - 1].step_end) first.push_back(i);
+    step_of[i] = s;
+    if (ops[i].step_end) ++s;
+  }
+  const int nsteps = (int)first.size();
+  auto last_of = [&](int st) { return st + 1 < nsteps ? first[st + 1] - 1 : n - 1; };
+  auto step_tma = [&](int st) {
+    for (int i = first[st]; i <= last_of(st); ++i)
+      if (!tma_gemm(ops[i])) return false;
+    return true;
+  };
+  // the op that last wrote workspace buffer `off` before op i (-1: none), and
+  // whether it is the only writer of that buffer
+  auto writer = [&](uint64_t off, int i, bool& single) {
+    int w = -1, cnt = 0;
+    for (int k = 0; k < n; ++k) {
+      const OpDesc& o = ops[k];
+      const BufRef& out = o.type == OP_GEMM ? o.g.ep.out : o.type == OP_SPLITK_FINAL ? o.m.ep.out : o.m.y;
+      if (out.kind == BUF_WS && out.off == off) {
+        ++cnt;
+        if (k < i) w = k;
+      }
+    }
+    single = cnt == 1;
+    return w;
+  };
+  int next_word = 1;
+  std::vector<int> pub(n, 0);
+  auto pub_of = [&](int k) {
+    if (!pub[k]) {
+      pub[k] = next_word;
+      next_word += ops[k].g.n_mblk;
+    }
+    return pub[k];
+  };
+  int sfull = 0;   // first step after the most recent full barrier
+  for (int st = 1; st < nsteps; ++st) {
+    bool local = step_tma(st - 1) && step_tma(st);
+    struct Dep { int op, which, prod; };
+    std::vector<Dep> deps;
+    for (int i = first[st]; local && i <= last_of(st); ++i) {
+      const GemmArgs& g = ops[i].g;
+      for (int which = 0; which < 2 && local; ++which) {
+        const BufRef& r = which == 0 ? g.ga.x : g.ep.res;
+        if (r.kind != BUF_WS) continue;                    // weights / request input / none
+        if (which == 0 && !g.act_tmap) { local = false; break; }
+        bool single = false;
+        const int w = writer(r.off, first[st], single);
+        if (w < 0 || step_of[w] < sfull) continue;         // complete before a full barrier
+        if (!single || !publishes(ops[w])) { local = false; break; }
+        const GemmArgs& pg = ops[w].g;
+        // A read as [rows, C] (2-D TMA) or NHWC im2col over the producer's rows
+        if (which == 0 && !(g.ga.C == pg.N && g.ga.lda == pg.N)) { local = false; break; }
+        if (which == 1 && !(g.M == pg.M && g.ep.ldc == pg.N)) { local = false; break; }
+        deps.push_back(Dep{i, which, w});
+      }
+    }
+    if (!local) {
+      sfull = st;
+      continue;
+    }
+    ops[last_of(st - 1)].local_next = 1;
+    for (const Dep& d : deps) {
+      GemmArgs& g = ops[d.op].g;
+      const OpDesc& po = ops[d.prod];
+      const int producer_step_tma = step_tma(step_of[d.prod]);
+      const int need = po.g.n_nblk * (producer_step_tma ? 8 : 4);   // one release per epilogue warp per tile
+      if (d.which == 0) {
+        g.dep_a_off = pub_of(d.prod);
+        g.dep_a_need = need;
+        g.dep_a_mblk = po.g.n_mblk;
+      } else {
+        g.dep_r_off = pub_of(d.prod);
+        g.dep_r_need = need;
+      }
+    }
+  }
+  for (int k = 0; k < n; ++k)
+    if (pub[k]) ops[k].g.pub_off = pub[k];
+  ops[0].cnt_words = next_word > 1 ? next_word : 0;
+  if (std::getenv("GL_DATAFLOW_LOG")) {
+    int joins = 0;
+    for (const OpDesc& o : ops) joins += o.local_next;
+    std::fprintf(stderr, "[dataflow] ops %d steps %d barrier-free joins %d counter words %d ws %.1f MB\n", n, nsteps,
+                 joins, ops[0].cnt_words, p.ws_bytes / 1e6);
+  }
+}
+
 bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
                    size_t& in_bytes, size_t& out_bytes, std::string& err) {
   (void)gpu;
@@ -1036,6 +1166,7 @@ bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, in
     return false;
   }
   out.ws_bytes = std::max<size_t>(out.ws_bytes, 256);
+  plan_dataflow(out);
   return true;
 }
 

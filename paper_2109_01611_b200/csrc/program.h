@@ -77,6 +77,15 @@ struct GemmArgs {
   int32_t pad0_;
   Gather ga, gb;                // gather geometry (used when *_tma == 0)
   Epilogue ep;
+  // Dataflow between GEMM steps joined without a gpu-let barrier (program.h
+  // OpDesc::local_next): per-M-block completion counters (uint32 words at the
+  // program's counter base; word 0 is unused, so 0 = none).
+  int32_t pub_off;              // this op's counters (one per M block): each epilogue warp adds 1 per tile
+  int32_t dep_a_off;            // counters of the op that wrote the A operand (wait before loading A)
+  int32_t dep_r_off;            // counters of the op that wrote the residual (wait before reading it)
+  int32_t dep_a_need;           // increments per producer M block once it is complete
+  int32_t dep_r_need;
+  int32_t dep_a_mblk;           // producer's M blocks (clamp for the im2col row range)
 };
 
 struct MiscArgs {
@@ -98,6 +107,10 @@ struct alignas(128) OpDesc {
   int32_t step_end;             // 1: gpu-let barrier after this op
   int32_t n_units;              // work units (tiles) of this op
   int32_t step_nops;            // first op of a step: the step's op count (set at bind time; diagnostics)
+  int32_t local_next;           // last op of a step: the next step follows with a CTA-local barrier only
+                                //   (its cross-CTA inputs are covered by completion counters)
+  int32_t cnt_words;            // op 0: the program's counter words (zeroed by the executor at program end)
+  uint64_t cnt_base;            // op 0: device address of the counters (set when the program is uploaded)
   uint64_t pf_addr;             // read-only operand (weights) prefetched into L2 one step ahead (0: none)
   uint64_t pf_bytes;
   GemmArgs g;

@@ -197,15 +197,24 @@ struct Gpulet {
 };
 
 // Upload a program bound to workspace `ws` (tensor maps of workspace operands).
+// The program's completion counters (barrier-free GEMM step joins) follow its
+// descriptors in the same allocation, zeroed here; the executor re-zeroes them
+// at the end of every run of the program.
 static OpDesc* upload_bound(const Program& p, char* ws, std::string& err) {
   std::vector<OpDesc> ops;
   if (!bind_program(p, ws, ops, err)) return nullptr;
   OpDesc* d = nullptr;
-  if (cudaMalloc(&d, ops.size() * sizeof(OpDesc)) != cudaSuccess) {
+  const size_t ob = ops.size() * sizeof(OpDesc);
+  const size_t cb = ops.empty() ? 0 : (size_t)ops[0].cnt_words * 4;
+  if (cudaMalloc(&d, ob + cb) != cudaSuccess) {
     err = "cudaMalloc(program)";
     return nullptr;
   }
-  cudaMemcpy(d, ops.data(), ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice);
+  if (cb) {
+    ops[0].cnt_base = (uint64_t)(uintptr_t)((char*)d + ob);
+    cudaMemset((char*)d + ob, 0, cb);
+  }
+  cudaMemcpy(d, ops.data(), ob, cudaMemcpyHostToDevice);
   return d;
 }
 

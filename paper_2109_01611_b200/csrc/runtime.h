@@ -92,6 +92,8 @@ bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, i
 // Bind a program to a workspace: encode the tensor maps of workspace-resident
 // activation operands (their addresses are only known per workspace).
 bool bind_program(const Program& p, char* ws, std::vector<OpDesc>& out, std::string& err);
+// Barrier-free joins of GEMM steps with completion counters (models.cpp; GL_DATAFLOW=1 enables).
+bool dataflow_enabled();
 bool build_test_misc(int type, const int* iargs, int n_iargs, const uint16_t* w_host, size_t w_len, DevWeights& dw,
                      Program& out, std::string& err);
 
