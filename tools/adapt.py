@@ -152,7 +152,10 @@ def main():
         v = int(((lat_all < 0) | (lat_all > slo_arr[m_idx])).sum())
         return {"policy": policy, "requests": n, "violations": v, "viol_frac": round(v / max(n, 1), 5),
                 "replans": sum(p["replanned"] for p in periods), "reorganisations": len(reorg_ms),
-                "reorg_ms": reorg_ms, "periods": periods}
+                "reorg_ms": reorg_ms,
+                # resources in use (the paper's "sum of scheduled gpu-let sizes")
+                "mean_gpulet_pct": round(sum(sum(p["gpulets"]) for p in periods) / max(len(periods), 1), 1),
+                "periods": periods}
 
     out = {"scenario": a.scenario, "mode": a.mode, "secs": a.secs, "period_s": a.period, "alpha": a.alpha,
            "headroom": a.headroom, "peak_req_s": peak, "x_sched_max": round(xs, 4), "slo_us": slo,
@@ -160,7 +163,8 @@ def main():
            "results": [run(p) for p in ("adaptive", "static-peak", "static-start")]}
     for r in out["results"]:
         print(f"{r['policy']:12s} requests {r['requests']:7d} violated {r['violations']:6d} ({100 * r['viol_frac']:.3f} %)"
-              f"  replans {r['replans']}  reorganisations {r['reorganisations']}  reorg ms {r['reorg_ms'][:6]}",
+              f"  replans {r['replans']}  reorganisations {r['reorganisations']}  reorg ms {r['reorg_ms'][:6]}"
+              f"  mean gpu-let % in use {r['mean_gpulet_pct']}",
               flush=True)
     if a.json:
         with open(a.json, "w") as f:
