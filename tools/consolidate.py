@@ -1,0 +1,103 @@
+"""Consolidation curves for two models on one GPU (partial;
+PAPER.md P:257-276, Fig. slo-violation: SLO violation of LeNet and VGG-16
+when they are consolidated with different resource sharing schemes).
+
+Schemes, on the same kernels and the same Poisson traces:
+  temporal   one 100 % gpu-let, both models as lanes of one executor (the
+             whole-GPU temporal sharing of SBP): each lane's batch
+             is its largest SLO-feasible batch at 100 %, the shared duty cycle
+             is the longest of the two lanes' execution times;
+  spatial    two gpu-lets, 20 % for LeNet and 80 % for VGG-16 (the paper's
+             "MPS(20:80)"): each lane on its own gpu-let with its own duty cycle.
+The paper's third scheme, unpartitioned concurrent kernels ("MPS(default)"),
+has no analogue here: an executor holds a whole SM (1 CTA/SM, ~225 KB of
+shared memory), so two executors cannot share SMs.
+
+For rate multipliers x (the models' B200-scaled paper rates times x), the
+violation fraction (late + dropped) of each model is measured.
+
+    python tools/consolidate.py [--xs 0.1,0.2,...] [--secs 1.0] [--json profiles/consolidate_b200.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+
+def lane(model, rate, batch, exec_us):
+    return {"model": model, "rate": int(rate), "batch": int(batch), "exec_us": int(exec_us), "F": 1000}
+
+
+def b_sat(lat_env, mi, gi, slo_us):
+    """Largest batch with 2 L(b, p) <= SLO (R4), or 1."""
+    best = 1
+    for b in range(1, 33):
+        if 2 * lat_env[mi][b - 1][gi] <= slo_us:
+            best = b
+    return best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--models", default="lenet5,vgg16")
+    ap.add_argument("--xs", default="0.05,0.1,0.2,0.3,0.4,0.6,0.8,1.0")
+    ap.add_argument("--secs", type=float, default=1.0)
+    ap.add_argument("--json", default="")
+    a = ap.parse_args()
+    import bench
+    from paper_2109_01611_b200 import gpulet
+    from tools import common
+
+    ctx = gpulet.Context(1)
+    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
+    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
+    slo = common.slos_from(lat_env)
+    srv = bench.Server(ctx, 0, (lat_env, l2, mem, slo, common.load_coeffs()), False)
+    small, large = a.models.split(",")
+    ms, ml = common.MODELS.index(small), common.MODELS.index(large)
+    g100, g20, g80 = common.GRID.index(100), common.GRID.index(20), common.GRID.index(80)
+    base = [0] * len(common.MODELS)
+    for m in (ms, ml):   # the paper's 100 req/s per model, scaled to B200 (C4.3)
+        ref = common.MODELS[m] if common.MODELS[m] in common.PAPER_SLO_MS else "resnet50"
+        base[m] = 100.0 * common.PAPER_SLO_MS[ref] * 1000.0 / slo[common.MODELS.index(ref)]
+    out = {"models": [small, large], "slo_us": [slo[ms], slo[ml]], "base_req_s": [base[ms], base[ml]],
+           "secs": a.secs, "cite": "P:257-276", "curves": {"temporal": [], "spatial-20:80": []}}
+    for x in [float(v) for v in a.xs.split(",")]:
+        rates = [int(r * x) for r in base]
+        for scheme in ("temporal", "spatial-20:80"):
+            if scheme == "temporal":
+                bs, bl = b_sat(lat_env, ms, g100, slo[ms]), b_sat(lat_env, ml, g100, slo[ml])
+                es, el = lat_env[ms][bs - 1][g100], lat_env[ml][bl - 1][g100]
+                d = max(es, el)
+                gls = [{"gpu": 0, "slot": 0, "size": 100, "sm": 148, "D_us": int(d),
+                        "lanes": [lane(small, rates[ms], bs, es), lane(large, rates[ml], bl, el)]}]
+            else:
+                bs, bl = b_sat(lat_env, ms, g20, slo[ms]), b_sat(lat_env, ml, g80, slo[ml])
+                es, el = lat_env[ms][bs - 1][g20], lat_env[ml][bl - 1][g80]
+                gls = [{"gpu": 0, "slot": 0, "size": 20, "sm": 0, "D_us": int(es),
+                        "lanes": [lane(small, rates[ms], bs, es)]},
+                       {"gpu": 0, "slot": 1, "size": 80, "sm": 0, "D_us": int(el),
+                        "lanes": [lane(large, rates[ml], bl, el)]}]
+            dump = "\n".join(json.dumps(g) for g in gls) + "\n" + json.dumps({"verdict": "Forced"})
+            my = srv.setup(dump, 0)
+            w = srv.window(my, a.secs, 900 + int(100 * x))
+            srv.teardown()
+            per = w["per"]
+            row = {"x": x, "rates": [rates[ms], rates[ml]], "batches": [bs, bl],
+                   "viol_frac": {m: round(per[m]["viol"] / max(per[m]["arrivals"], 1), 4) for m in (small, large)
+                                 if m in per},
+                   "p99_us": {m: per[m]["p99_us"] for m in (small, large) if m in per}}
+            out["curves"][scheme].append(row)
+            print(scheme, json.dumps(row), flush=True)
+    if a.json:
+        with open(a.json, "w") as f:
+            json.dump(out, f, indent=1)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
