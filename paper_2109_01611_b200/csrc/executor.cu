@@ -1668,6 +1668,8 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   Pipe P;
   uint64_t epoch = 0;
   int done = 0;
+  // completions published so far (CTA 0 thread 0 is the only writer of the ring's completion side)
+  uint64_t completions = (blockIdx.x == 0 && threadIdx.x == 0) ? p.ring->heartbeat : 0;
   for (;;) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const uint64_t head = p.st->head;
@@ -1680,22 +1682,18 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
           break;
         }
         __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
+        if (ns < 256) ns <<= 1;
       }
       if (quit) {
         p.st->quit = 1;
       } else {
-        const volatile WorkDesc* src = &p.ring->items[head % kRing];
+        // the item as four 16-B loads over PCIe, ordered after the acquire of
+        // `tail` above (one round trip instead of one per field)
+        const uint4* src = (const uint4*)&p.ring->items[head % kRing];
         WorkDesc w;
-        w.ticket = src->ticket;
-        w.prog = src->prog;
-        w.in = src->in;
-        w.out = src->out;
-        w.n_ops = src->n_ops;
-        w.model = src->model;
-        w.batch = src->batch;
-        w.slo_us = src->slo_us;
-        w.t_submit_ns = src->t_submit_ns;
+        uint4* dst = (uint4*)&w;
+        const uint4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
+        dst[0] = q0, dst[1] = q1, dst[2] = q2, dst[3] = q3;
         p.st->cur = w;
         p.st->t_dequeue = globaltimer();
         p.st->head = head + 1;
@@ -1706,33 +1704,34 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
     if (*(volatile uint64_t*)&p.st->quit) break;
     WorkDesc w;
     {
-      const volatile WorkDesc* c = &p.st->cur;
-      w.ticket = c->ticket;
-      w.prog = c->prog;
-      w.in = c->in;
-      w.out = c->out;
-      w.n_ops = c->n_ops;
-      w.model = c->model;
-      w.batch = c->batch;
-      w.slo_us = c->slo_us;
-      w.t_submit_ns = c->t_submit_ns;
+      // the item CTA 0 broadcast, as four 16-B L2 loads (ordered after the barrier)
+      const uint4* c = (const uint4*)&p.st->cur;
+      uint4* dst = (uint4*)&w;
+      const uint4 q0 = __ldcg(c), q1 = __ldcg(c + 1), q2 = __ldcg(c + 2), q3 = __ldcg(c + 3);
+      dst[0] = q0, dst[1] = q1, dst[2] = q2, dst[3] = q3;
     }
     const uint64_t t_start = globaltimer();
     Ctx X{(const char*)w.in, (char*)w.out, p.ws, (uint32_t*)(uintptr_t)w.prog[0].cnt_base};
     run_program(w, X, S, P, p.st, epoch, p.trace, p.trace_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      const uint64_t i = p.ring->heartbeat;
-      volatile CompRec* c = &p.ring->comp[i % kRing];
-      c->ticket = w.ticket;
-      c->gpulet = p.gpulet;
-      c->model = w.model;
-      c->batch = w.batch;
-      c->status = 0;
-      c->t_submit_ns = w.t_submit_ns;
-      c->t_dequeue_ns = p.st->t_dequeue;
-      c->t_start_ns = t_start;
-      c->t_end_ns = globaltimer();
-      __threadfence_system();
+      // the record as four 16-B stores to the host-mapped ring, published by a
+      // release store of comp_tail (cumulative: it also orders the batch's
+      // outputs, which the final gpu-let barrier made visible to this thread)
+      const uint64_t i = completions++;
+      CompRec r;
+      r.ticket = w.ticket;
+      r.gpulet = p.gpulet;
+      r.model = w.model;
+      r.batch = w.batch;
+      r.status = 0;
+      r.t_submit_ns = w.t_submit_ns;
+      r.t_dequeue_ns = p.st->t_dequeue;
+      r.t_start_ns = t_start;
+      r.t_end_ns = globaltimer();
+      r.pad_ = 0;
+      uint4* dst = (uint4*)&p.ring->comp[i % kRing];
+      const uint4* srcr = (const uint4*)&r;
+      dst[0] = srcr[0], dst[1] = srcr[1], dst[2] = srcr[2], dst[3] = srcr[3];
       p.ring->heartbeat = i + 1;
       st_release_sys_u64(&p.ring->comp_tail, i + 1);
     }

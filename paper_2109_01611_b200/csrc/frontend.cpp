@@ -2,9 +2,10 @@
 // real time against live gpu-lets.  Each model's requests are routed over its
 // lanes by smooth weighted round-robin (weights = the lanes' assigned rates);
 // each lane keeps a FIFO and dispatches "when the desired size of request batch
-// is formed or a duty-cycle is passed", after dropping
-// requests that can no longer meet their SLO (drops count as violations,
-// P:860).  A request's latency is host completion time - arrival time.
+// is formed or a duty-cycle is passed" -- or when its
+// oldest request's remaining slack has shrunk to Leff(1) + a guard (DESIGN R26)
+// -- after dropping requests that can no longer meet their SLO (drops
+// count as violations).  A request's latency is host completion time - arrival time.
 //
 // End-to-end mode (lanes with in_host): a model's i-th request lives in host
 // slot i % host_slots of the lane's pinned ring.  A dispatched batch goes
@@ -25,6 +26,7 @@
 #include <pthread.h>
 #include <sched.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -41,6 +43,9 @@ enum Stage { FREE = 0, H2D, RUN, D2H };
 // memory (LeNet 1.6 KB, BERT 512 B: a copy's fixed latency is most of their
 // SLO); larger ones go through the async copy path.
 constexpr int64_t kZeroCopyMax = 64 * 1024;
+// Deadline guard of the dispatch rule: max(5 us, SLO / 20).
+constexpr int64_t kGuardMinUs = 5;
+constexpr int32_t kGuardDiv = 20;
 
 struct Batch {
   Stage stage = FREE;
@@ -217,7 +222,12 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       if (b < 0) continue;
       const bool full = (int)ln.q.size() >= ln.cfg.batch;
       const bool timeout = now - ln.window_us >= ln.cfg.duty_us;
-      if (!full && !timeout) continue;
+      // deadline guard (DESIGN R26): dispatch early when the oldest queued
+      // request would otherwise keep waiting into its last Leff(1) + guard of slack
+      const int32_t slo_m = slo_us[ln.cfg.model_slot];
+      const int64_t guard = std::max<int64_t>(kGuardMinUs, slo_m / kGuardDiv);
+      const bool urgent = now - arr_us[ln.q.front()] + ln.cfg.drop_us + guard >= slo_m;
+      if (!full && !timeout && !urgent) continue;
       while (!ln.q.empty()) {  // drop hopeless requests
         const int64_t r = ln.q.front();
         if ((now - arr_us[r]) + ln.cfg.drop_us > slo_us[arr_model[r]]) {

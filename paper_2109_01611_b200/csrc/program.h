@@ -118,7 +118,7 @@ struct alignas(128) OpDesc {
 };
 
 // One batch of one model = one work item in a gpu-let's ring (64 B, §8(a) a6).
-struct WorkDesc {
+struct alignas(16) WorkDesc {
   uint64_t ticket;
   const OpDesc* prog;           // device program for (model, batch)
   const void* in;               // device input
@@ -128,10 +128,12 @@ struct WorkDesc {
   int32_t batch;
   int32_t slo_us;
   uint64_t t_submit_ns;         // host clock (CLOCK_MONOTONIC) at submit
+  uint64_t pad_;                // 64 B: the executor reads an item as four 16-B loads
 };
+static_assert(sizeof(WorkDesc) == 64, "WorkDesc is one 64-B ring slot");
 
 // Completion record (§8(a) a13): device -> host-mapped ring.
-struct CompRec {
+struct alignas(16) CompRec {
   uint64_t ticket;
   int32_t gpulet, model, batch, status;
   uint64_t t_submit_ns;         // host clock copied from the WorkDesc
@@ -140,6 +142,7 @@ struct CompRec {
   uint64_t t_end_ns;            // after the last layer's barrier
   uint64_t pad_;
 };
+static_assert(sizeof(CompRec) == 64, "CompRec is one 64-B ring slot");
 
 constexpr int kRing = 256;
 
