@@ -1579,8 +1579,14 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
   if (tr && trace_cap > 0) trace[0] = globaltimer();
   S.dbg = (trace && trace_cap >= 1024 + 8 * 1000) ? trace + 1024 : nullptr;
   while (i < w.n_ops) {
+    // the step's extent: bound programs carry it on the step's first op (one
+    // load instead of one dependent load per op of the step)
+    const int sn = w.prog[i].step_nops;
     int j = i;
-    while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
+    if (sn > 0)
+      j = min(w.n_ops - 1, i + sn - 1);
+    else
+      while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
     S.step = step;
     if (threadIdx.x == 0 && w.prog[i].type != OP_LENET) *S.wtag = 0;   // smem scratch / ring reused
     const int n_next = min(kPfOps, w.n_ops - j - 1);
