@@ -427,6 +427,8 @@ class Builder {
     g.splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;
   }
 
+  static constexpr int kWideStepTiles = 74;   // half of a whole B200's SMs
+
   // Queue the split-K finalize: allocate the partial buffer now.
   struct PendingFinal {
     Epilogue ep;
@@ -453,8 +455,41 @@ class Builder {
   }
 
   // Emit the split-K reduction ops of the previous step (call after step()).
+  // Split-K is chosen per op (too few tiles to fill the GPU); a step of several
+  // GEMM ops whose tiles together fill at least half the GPU runs unsplit
+  // instead -- its finalize step would cost more than the extra tiles save
+  // (measured: GoogLeNet b8 -14 % without split-K in its inception steps).
   void flush_finals() {
     if (finals.empty()) return;
+    const int n = (int)prog.ops.size();
+    int s0 = n - 1;
+    while (s0 > 0 && !prog.ops[s0 - 1].step_end) --s0;
+    int gemms = 0, tiles = 0;
+    for (int k = s0; k < n; ++k)
+      if (prog.ops[k].type == OP_GEMM) {
+        ++gemms;
+        tiles += prog.ops[k].g.n_mblk * prog.ops[k].g.n_nblk;
+      }
+    if (gemms > 1 && tiles >= kWideStepTiles && !g_tune[TUNE_SPLIT]) {
+      for (int k = s0; k < n; ++k) {
+        OpDesc& op = prog.ops[k];
+        GemmArgs& g = op.g;
+        if (op.type != OP_GEMM || g.splits <= 1) continue;
+        const uint64_t ws = g.ep.ws.off;
+        for (size_t f = 0; f < finals.size(); ++f)
+          if (finals[f].ws == ws) {
+            release_off(ws);
+            finals.erase(finals.begin() + f);
+            break;
+          }
+        g.splits = 1;
+        g.kb_per_split = g.K_pad / 64;
+        g.ep.splitk = 1;
+        g.ep.ws = BufRef{0, BUF_NONE, 0};
+        op.n_units = g.n_mblk * g.n_nblk;
+      }
+      if (finals.empty()) return;
+    }
     for (auto& f : finals) {
       OpDesc& op = add(OP_SPLITK_FINAL);
       op.m.rows = f.M;

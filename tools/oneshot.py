@@ -23,12 +23,18 @@ def main():
     ap.add_argument("--n_sm", type=int, default=0)
     ap.add_argument("--json", default="")
     ap.add_argument("--flags", type=int, default=0, help="executor dbg_flags (tuning experiments)")
+    ap.add_argument("--split", type=int, default=0, help="force split-K count when building programs (tuning)")
+    ap.add_argument("--bn", type=int, default=0, help="force the UMMA N tile when building programs (tuning)")
     a = ap.parse_args()
     import torch
     from paper_2109_01611_b200 import gpulet
     ctx = gpulet.Context(1)
     if a.flags:
         gpulet.Context.set_tuning(2, a.flags)
+    if a.split:
+        gpulet.Context.set_tuning(1, a.split)
+    if a.bn:
+        gpulet.Context.set_tuning(0, a.bn)
     mid = ctx.load_model(0, a.model, synthgen.weight_file(a.model))
     x = common.device_input(a.model, a.batch)
     y = torch.empty(ctx.model_io(mid, a.batch)[1] // 4, device="cuda")
