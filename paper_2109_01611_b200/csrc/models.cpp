@@ -401,16 +401,21 @@ class Builder {
   }
 
   // UMMA N tile: the widest balanced tile (<= 256 columns) that still gives
-  // about one wave of tiles over a whole B200 (148 SMs); narrower tiles are
+  // half a wave of tiles over a whole B200 (74 of 148 SMs); narrower tiles are
   // preferred to split-K, which costs an extra reduction step (measured:
-  // tools/gemm_micro.py, ResNet-50 b=32 layer3/4 shapes).
+  // tools/gemm_micro.py, ResNet-50 b=32 layer3/4 shapes).  (A long-K variant
+  // preferring 128-column tiles plus deeper split-K was measured and rejected:
+  // ResNet-50 b15 -0.6 %, SSD b8 +3.9 %, profiles/ab_r2n_longk_bn.log.)
   static int pick_bn(int N, int n_mblk) {
     if (g_tune[TUNE_BN] >= 16 && g_tune[TUNE_BN] <= 256) return std::min(rup(N, 16), rup(g_tune[TUNE_BN], 16));
     int bn = 0;
     for (int cap = 256; cap >= 64; cap /= 2) {
       const int nnb = (N + cap - 1) / cap;
       bn = std::max(16, rup((N + nnb - 1) / nnb, 16));
-      if (n_mblk * ((N + bn - 1) / bn) >= 96) break;
+      // half a B200 of tiles is enough: a narrower tile that spills into a
+      // second, partial wave costs more (ResNet-50 b15 layer-2 3x3: 92 tiles
+      // of 128 columns 16.5 us vs 184 of 64 columns 24 us)
+      if (n_mblk * ((N + bn - 1) / bn) >= 74) break;
     }
     return bn;
   }

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+D=paper_2109_01611_b200/_ab
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/gputests_r2m.log 2>&1; echo "rc=$?" >> gpurun_out/gputests_r2m.log
+VARIANTS="N=$D/libgpulet_N.so P=$D/libgpulet_P.so" bash scripts/ab_oneshot.sh m resnet50:15 resnet50:8 resnet50:32 resnet50:1 googlenet:8 googlenet:15 ssd_mobilenet_v1:8 vgg16:8 bert_base:8 > gpurun_out/ab_m2.log 2>&1
+echo done
