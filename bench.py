@@ -497,10 +497,15 @@ def lane_util(srv, wins):
         ib, ob = srv.req_bytes[m]
         t = ns * 1e-9
         fl, by = f1 * r, wb * b + (ib + ob) * r
-        peak_t = ln["sm"] / 148.0 * sus
+        # LeNet-5 runs on CUDA cores (fp32 FMA): its compute
+        # roof is the SM share's fp32 rate (128 lanes x 2 FLOP per clock per SM
+        # at the 1965 MHz boost clock), not the tensor pipe's
+        alu = m == "lenet5"
+        peak_t = ln["sm"] * 128 * 2 * 1.965e9 / 1e12 if alu else ln["sm"] / 148.0 * sus
         ach_t = fl / t / 1e12 if t else 0.0
         ach_b = by / t / 1e9 if t else 0.0
         out.append({"model": m, "gpulet_pct": ln["size"], "sm": ln["sm"], "planned_batch": ln["batch"],
+                    "compute": "alu (fp32 FMA)" if alu else "tensor (bf16 tcgen05)",
                     "batches": b, "requests": r, "busy_s": round(t, 4),
                     "mean_batch": round(r / b, 2) if b else 0.0, "mean_batch_us": round(t / b * 1e6, 1) if b else 0.0,
                     "tflops": round(ach_t, 2), "tensor_frac": round(ach_t / peak_t, 4) if peak_t else 0.0,
@@ -515,17 +520,21 @@ def roofline_serving(util):
     windows.  Tensor-bound when its FLOP per algorithmic byte exceeds the ridge."""
     if not util:
         return None
-    u = max(util, key=lambda d: d["busy_s"])
+    # the lane that used the most of the GPU: device busy time x SMs of its gpu-let
+    u = max(util, key=lambda d: d["busy_s"] * d["sm"])
     if not u["busy_s"]:
         return None
     hbm, _burst, sus, src = _peaks()
-    tensor = u["tflops"] * 1e12 / max(u["gbs"] * 1e9, 1.0) > sus * 1e12 / (hbm * 1e9)
+    alu = u.get("compute", "").startswith("alu")
+    ridge = (u["tensor_peak_tflops"] * 1e12) / (hbm * 1e9)
+    tensor = u["tflops"] * 1e12 / max(u["gbs"] * 1e9, 1.0) > ridge
     traffic = None
     ncu_path = os.path.join(ROOT, "profiles", f"ncu_{u['model']}_b{u['planned_batch']}.json")
     if os.path.exists(ncu_path):
         with open(ncu_path) as f:
             traffic = json.load(f).get("dram_bytes")
-    return {"bound": "tensor" if tensor else "hbm", "achieved": u["tflops"] if tensor else u["gbs"],
+    return {"bound": ("alu" if alu else "tensor") if tensor else "hbm",
+            "achieved": u["tflops"] if tensor else u["gbs"],
             "peak": u["tensor_peak_tflops"] if tensor else u["hbm_peak_gbs"],
             "unit": "TFLOP/s" if tensor else "GB/s",
             "frac": u["tensor_frac"] if tensor else u["hbm_frac"], "traffic": traffic,

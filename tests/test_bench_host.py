@@ -57,6 +57,10 @@ def test_roofline_serving_picks_busiest_lane_and_bound():
     assert abs(r["frac"] - 80.0 / 1173.0) < 1e-3
     util[1]["gbs"] = 1e6    # FLOP per byte below the ridge -> HBM-bound
     assert bench.roofline_serving(util)["bound"] == "hbm"
+    # the dominant lane is the one that used the most GPU (busy time x SMs), not the busiest clock
+    util[1]["gbs"] = 60.0
+    util[0]["busy_s"] = 0.02
+    assert bench.roofline_serving(util)["kernel"].startswith("gl_executor serving resnet50")
 
 
 def test_poisson_trace_rates_and_order():
