@@ -85,6 +85,37 @@ def main():
             # schedules must also be schedulable by the ideal
             out["results"][f"gpulet_int_not_ideal@{N}"] = sum(
                 1 for x, y in zip(g["_flags"], i["_flags"]) if x and not y)
+    # scheduler-level maximum rates (the paper's Fig. "maximum achievable
+    # throughput", before serving validation): per scenario, GPU
+    # count and mode, the largest rate multiplier the scheduler accepts
+    cap = {}
+    full_l2, full_mem = l2, mem
+    for scen in ("game", "traffic", "equal", "long-only", "short-skew"):
+        for N in (1, 2, 4, 8):
+            for mode in ("sbp", "gpulet", "gpulet+int"):
+                def ok(x):
+                    rates = common.scenario_rates(scen, slo, x)
+                    return gpulet.schedule(common.MODELS, lat_env, full_l2, full_mem, slo, [r * N for r in rates],
+                                           N, mode, coeffs)[1] and sum(rates) > 0
+                lo, hi = 0.0, 0.25
+                while ok(hi) and hi < 1e4:
+                    lo, hi = hi, hi * 2
+                for _ in range(30):
+                    mid = (lo + hi) / 2
+                    lo, hi = (mid, hi) if ok(mid) else (lo, mid)
+                rates = common.scenario_rates(scen, slo, lo)
+                cap[f"{scen}@{N}/{mode}"] = {"x": round(lo, 4), "model_req_s": sum(rates) * N}
+        for N in (1, 2, 4, 8):
+            b = cap[f"{scen}@{N}/sbp"]["model_req_s"]
+            for mode in ("gpulet", "gpulet+int"):
+                g = cap[f"{scen}@{N}/{mode}"]["model_req_s"]
+                cap[f"{scen}@{N}/{mode}"]["vs_sbp"] = round(g / b, 3) if b else None
+    out["max_schedulable_rate"] = cap
+    out["paper_max_rate"] = {"cite": "P:833-852 (4 x 2080 Ti)", "gpulet_vs_sbp": "+106.0 %",
+                             "gpulet_int_vs_sbp": "+102.6 %"}
+    for k, v in cap.items():
+        if k.endswith("gpulet+int") or k.endswith("gpulet"):
+            print(f"{k:28s} {v}", flush=True)
     # oracle replay of a seeded sample (byte-identical plan dumps)
     from oracle import sched as osched
     P = osched.Profile(names, L, L2, ME)
