@@ -1129,7 +1129,17 @@ __device__ __noinline__ void lenet(const OpDesc* op, const Ctx& X, uint8_t* scra
   float* h2 = h1 + 120;           // 84
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int n = blockIdx.x; n < a.N; n += gridDim.x) {
-    for (int i = threadIdx.x; i < 784; i += blockDim.x) img[i] = __bfloat162float(x[(int64_t)n * 784 + i]);
+    // the image as 98 16-B loads (one round trip when it is read over PCIe
+    // from a pinned host ring, gl_serve's zero-copy path)
+    if (threadIdx.x < 98) {
+      const uint4 u = ((const uint4*)(x + (int64_t)n * 784))[threadIdx.x];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        img[threadIdx.x * 8 + 2 * k] = bf_lo(w4[k]);
+        img[threadIdx.x * 8 + 2 * k + 1] = bf_hi(w4[k]);
+      }
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < 4704; i += blockDim.x) {   // conv1 5x5 pad 2 + relu + bf16
       const int co = i % 6, ox = (i / 6) % 28, oy = i / 168;
