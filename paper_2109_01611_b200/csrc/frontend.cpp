@@ -43,6 +43,7 @@ enum Stage { FREE = 0, H2D, RUN, D2H };
 // memory (LeNet 1.6 KB, BERT 512 B: a copy's fixed latency is most of their
 // SLO); larger ones go through the async copy path.
 constexpr int64_t kZeroCopyMax = 64 * 1024;
+constexpr int kZeroCopyBuf = -2;   // Inflight::buf of a zero-copy batch
 // Deadline guard of the dispatch rule: max(5 us, SLO / 20).
 constexpr int64_t kGuardMinUs = 5;
 constexpr int32_t kGuardDiv = 20;
@@ -53,12 +54,11 @@ struct Batch {
   std::vector<int64_t> slots;  // their host slots (end-to-end mode)
   cudaEvent_t ev = nullptr;
   uint64_t ticket = 0;
-  bool zero_copy = false;      // inputs / outputs read / written in the host ring by the executor
 };
 
 struct Inflight {
   int lane;
-  int buf;                     // end-to-end buffer index, -1 in plain mode
+  int buf;                     // end-to-end buffer index; -1 plain mode, kZeroCopyBuf zero-copy batch
   std::vector<int64_t> reqs;   // plain mode: the batch's request indices
 };
 
@@ -219,7 +219,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       LaneState& ln = L[li];
       if (ln.q.empty()) continue;
       const int b = ln.cfg.in_host ? ln.free_buf() : 0;
-      if (b < 0) continue;
+      if (b < 0 && !ln.zero_copy) continue;   // zero-copy batches need no device buffer
       const bool full = (int)ln.q.size() >= ln.cfg.batch;
       const bool timeout = now - ln.window_us >= ln.cfg.duty_us;
       // deadline guard (DESIGN R26): dispatch early when the oldest queued
@@ -238,39 +238,38 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
           break;
         }
       }
+      const int64_t window0 = ln.window_us;
       ln.window_us = now;
       if (ln.q.empty()) continue;
       const int k = std::min<int>((int)ln.q.size(), ln.cfg.batch);
       if (ln.cfg.in_host) {
-        Batch& bt = ln.buf[b];
-        bt.reqs.assign(ln.q.begin(), ln.q.begin() + k);
-        bt.slots.resize(k);
-        for (int i = 0; i < k; ++i) bt.slots[i] = seq_of[bt.reqs[i]] % ln.cfg.host_slots;
+        std::vector<int64_t> slots(k);
+        for (int i = 0; i < k; ++i) slots[i] = seq_of[ln.q[i]] % ln.cfg.host_slots;
         bool contiguous = true;
-        for (int i = 1; i < k; ++i) contiguous &= bt.slots[i] == bt.slots[0] + i;
+        for (int i = 1; i < k; ++i) contiguous &= slots[i] == slots[0] + i;
         if (ln.zero_copy && contiguous) {
           // small requests: the executor reads the inputs from / writes the
           // outputs to the pinned host ring itself (UVA-mapped), no copy stage
-          const char* in = (const char*)ln.cfg.in_host + bt.slots[0] * ln.cfg.in_req_bytes;
-          char* out = (char*)ln.cfg.out_host + bt.slots[0] * ln.cfg.out_req_bytes;
+          // and no device buffer (any number of such batches in flight)
+          const char* in = (const char*)ln.cfg.in_host + slots[0] * ln.cfg.in_req_bytes;
+          char* out = (char*)ln.cfg.out_host + slots[0] * ln.cfg.out_req_bytes;
           uint64_t ticket = 0;
           const gl_status s = gl_submit_batch(ctx, ln.cfg.gpulet, ln.cfg.model_id, in, out, k,
                                               (float)slo_us[ln.cfg.model_slot] / 1000.f, &ticket);
-          if (s == GL_E_QUEUE_FULL) {   // retry next iteration (the requests are still queued)
-            bt.reqs.clear();
-            bt.slots.clear();
-            continue;
-          }
+          if (s == GL_E_QUEUE_FULL) continue;   // retry next iteration (the requests are still queued)
           if (s != GL_OK) return s;
           h2d += (int64_t)k * ln.cfg.in_req_bytes;
-          bt.zero_copy = true;
-          bt.ticket = ticket;
-          bt.stage = RUN;
-          inflight.emplace(ticket, Inflight{li, b, {}});
+          inflight.emplace(ticket, Inflight{li, kZeroCopyBuf, std::vector<int64_t>(ln.q.begin(), ln.q.begin() + k)});
           ln.q.erase(ln.q.begin(), ln.q.begin() + k);
           continue;
         }
-        bt.zero_copy = false;
+        if (b < 0) {                            // copy path: wait for a device buffer
+          ln.window_us = window0;
+          continue;
+        }
+        Batch& bt = ln.buf[b];
+        bt.reqs.assign(ln.q.begin(), ln.q.begin() + k);
+        bt.slots = std::move(slots);
         ln.q.erase(ln.q.begin(), ln.q.begin() + k);
         if (!copy_slots((void*)ln.in_dev(b), ln.cfg.in_host, bt.slots, ln.cfg.in_req_bytes, true, ln.stream, &h2d) ||
             cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
@@ -328,7 +327,8 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       }
       LaneState& ln = L[it->second.lane];
       const int b = it->second.buf;
-      if (b < 0) {
+      if (b < 0) {   // plain mode, or a zero-copy batch (outputs already in the host ring)
+        if (b == kZeroCopyBuf) d2h += (int64_t)it->second.reqs.size() * ln.cfg.out_req_bytes;
         const int64_t t = now_us();
         for (int64_t r : it->second.reqs) {
           lat_us[r] = t - arr_us[r];
@@ -339,11 +339,6 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       }
       inflight.erase(it);
       Batch& bt = ln.buf[b];
-      if (bt.zero_copy) {   // outputs already in the host ring
-        d2h += (int64_t)bt.reqs.size() * ln.cfg.out_req_bytes;
-        complete(bt, now_us(), outstanding);
-        continue;
-      }
       if (!copy_slots(ln.out_dev(b), ln.cfg.out_host, bt.slots, ln.cfg.out_req_bytes, false, ln.stream, &d2h) ||
           cudaEventRecord(bt.ev, ln.stream) != cudaSuccess)
         return GL_E_CUDA;
