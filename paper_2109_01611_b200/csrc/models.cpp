@@ -238,9 +238,12 @@ struct Act {
   int ld = 0;  // pixel stride in elements
 };
 
+
 class Builder {
  public:
-  Builder(const ParamMap& P, DevWeights& dw, int batch, Program& prog) : P(P), dw(dw), b(batch), prog(prog) {
+  Builder(const ParamMap& P, DevWeights& dw, int batch, Program& prog, int sm_target_)
+      : P(P), dw(dw), b(batch), prog(prog),
+        sm_target(g_tune[TUNE_SMS] >= 8 ? g_tune[TUNE_SMS] : sm_target_) {
     alloc(64 * 1024);   // offset 0: split-K tile counters (zeroed with the workspace, self-resetting)
   }
 
@@ -248,6 +251,9 @@ class Builder {
   DevWeights& dw;
   int b;
   Program& prog;
+  // SMs the tile decomposition (N tile, split-K) targets: the SM count of the
+  // gpu-let the program is built for (a whole B200 = 148)
+  const int sm_target;
   Err e;
   int step_first = 0;
 
@@ -406,7 +412,7 @@ class Builder {
   // tools/gemm_micro.py, ResNet-50 b=32 layer3/4 shapes).  (A long-K variant
   // preferring 128-column tiles plus deeper split-K was measured and rejected:
   // ResNet-50 b15 -0.6 %, SSD b8 +3.9 %, profiles/ab_r2n_longk_bn.log.)
-  static int pick_bn(int N, int n_mblk) {
+  int pick_bn(int N, int n_mblk) const {
     if (g_tune[TUNE_BN] >= 16 && g_tune[TUNE_BN] <= 256) return std::min(rup(N, 16), rup(g_tune[TUNE_BN], 16));
     int bn = 0;
     for (int cap = 256; cap >= 64; cap /= 2) {
@@ -415,7 +421,7 @@ class Builder {
       // half a B200 of tiles is enough: a narrower tile that spills into a
       // second, partial wave costs more (ResNet-50 b15 layer-2 3x3: 92 tiles
       // of 128 columns 16.5 us vs 184 of 64 columns 24 us)
-      if (n_mblk * ((N + bn - 1) / bn) >= 74) break;
+      if (n_mblk * ((N + bn - 1) / bn) >= sm_target / 2) break;
     }
     return bn;
   }
@@ -432,15 +438,14 @@ class Builder {
     // (convolutions only: the linears keep the plain rule -- BERT's logits sit
     // at the parity bound and change with the summation order)
     const bool conv = g.ga.H > 1 || g.ga.W > 1;
-    if (allow && tiles < 74 && (conv ? (nkb >= 40 || (tiles <= 16 && nkb >= 8)) : nkb >= 8))
-      splits = std::min(nkb / 4, std::max(1, 148 / tiles));
+    if (allow && tiles < sm_target / 2 && (conv ? (nkb >= 40 || (tiles <= 16 && nkb >= 8)) : nkb >= 8))
+      splits = std::min(nkb / 4, std::max(1, sm_target / tiles));
     if (allow && g_tune[TUNE_SPLIT] > 0) splits = std::min(nkb, g_tune[TUNE_SPLIT]);
     splits = std::max(1, splits);
     g.kb_per_split = (nkb + splits - 1) / splits;
     g.splits = (nkb + g.kb_per_split - 1) / g.kb_per_split;
   }
 
-  static constexpr int kWideStepTiles = 74;   // half of a whole B200's SMs
 
   // Queue the split-K finalize: allocate the partial buffer now.
   struct PendingFinal {
@@ -483,7 +488,7 @@ class Builder {
         ++gemms;
         tiles += prog.ops[k].g.n_mblk * prog.ops[k].g.n_nblk;
       }
-    if (gemms > 1 && tiles >= kWideStepTiles && !g_tune[TUNE_SPLIT]) {
+    if (gemms > 1 && tiles >= sm_target / 2 && !g_tune[TUNE_SPLIT]) {
       for (int k = s0; k < n; ++k) {
         OpDesc& op = prog.ops[k];
         GemmArgs& g = op.g;
@@ -1196,10 +1201,10 @@ void plan_dataflow(Program& p) {
 }
 
 bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
-                   size_t& in_bytes, size_t& out_bytes, std::string& err) {
+                   size_t& in_bytes, size_t& out_bytes, std::string& err, int sm_target) {
   (void)gpu;
   out = Program();
-  Builder B(host, dw, batch, out);
+  Builder B(host, dw, batch, out, sm_target);
   switch (kind) {
     case 0: build_lenet(B, in_bytes, out_bytes); break;
     case 1: build_googlenet(B, in_bytes, out_bytes); break;
@@ -1230,7 +1235,7 @@ bool build_test_gemm(int M, int N, int K, int act, int swap_ab, int splitk, int 
   bb.data.assign(b_host, b_host + N);
   P["t.w"] = w;
   P["t.b"] = bb;
-  Builder B(P, dw, M, out);
+  Builder B(P, dw, M, out, 148);
   WRef wr = fc_weight(dw, P, "t", B.e);
   void* bias = raw_param(dw, P, "t.b", B.e);
   // input: [M, K] bf16 (BUF_IN, or copied to workspace offset 0); output BUF_OUT [M, N]
@@ -1269,7 +1274,7 @@ bool build_test_conv(int N, int H, int W, int C, int Cout, int KH, int stride, i
   bb.data.assign(b_host, b_host + Cout);
   P["t.w"] = w;
   P["t.b"] = bb;
-  Builder B(P, dw, N, out);
+  Builder B(P, dw, N, out, 148);
   Act x = input_act(N, H, W, C);
   if (in_ws) {
     out.in_copy_bytes = (size_t)N * H * W * C * 2;
@@ -1306,7 +1311,7 @@ bool build_test_misc(int type, const int* ia, int n, const uint16_t* w_host, siz
     P["t.w"] = w;
     P["t.b"] = bb;
   }
-  Builder B(P, dw, 1, out);
+  Builder B(P, dw, 1, out, 148);
   auto need = [&](int k) {
     if (n < k) {
       err = "too few int args";

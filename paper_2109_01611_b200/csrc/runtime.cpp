@@ -227,7 +227,9 @@ struct SlotRes {
   HostRing* ring_dev = nullptr;
   ExecState* st = nullptr;
   int* smid = nullptr;
-  std::map<int, std::vector<OpDesc*>> progs;  // model id -> [batch] programs bound to ws
+  std::map<int, std::vector<OpDesc*>> progs;  // model id -> [batch] programs bound to ws (148-SM tiling)
+  // (model id, SM count) -> [batch] programs tiled for that gpu-let size, bound to ws
+  std::map<std::pair<int, int>, std::vector<OpDesc*>> progs_sm;
 };
 
 struct GpuState {
@@ -536,6 +538,8 @@ gl_status gl_shutdown(gl_ctx* ctx) {
       if (!R.ready) continue;
       for (auto& kv : R.progs)
         for (OpDesc* p : kv.second) release_device(p, false);
+      for (auto& kv : R.progs_sm)
+        for (OpDesc* p : kv.second) release_device(p, false);
       release_device(R.ws, false);
       release_device(R.st, false);
       release_device(R.smid, false);
@@ -567,7 +571,8 @@ gl_status gl_load_model(gl_ctx* ctx, int gpu, int kind, const char* weight_file,
     CK(cudaMalloc(&p.dev, p.ops.size() * sizeof(OpDesc)), "cudaMalloc(program)");
     CK(cudaMemcpy(p.dev, p.ops.data(), p.ops.size() * sizeof(OpDesc), cudaMemcpyHostToDevice), "upload program");
   }
-  m->host.clear();  // device copies are all that is needed from here on
+  // (the host copy stays: programs tiled for other gpu-let sizes are built when
+  // such a gpu-let is first created, gl_create_gpulets)
   *model_id = (int32_t)ctx->models.size();
   ctx->models.push_back(std::move(m));
   return GL_OK;
@@ -587,6 +592,86 @@ gl_status gl_model_cost(gl_ctx* ctx, int32_t id, int32_t batch, double* flops, d
   if (flops) *flops = ctx->models[id]->prog[batch].flops;
   if (wbytes) *wbytes = ctx->models[id]->prog[batch].weight_bytes;
   return GL_OK;
+}
+
+// Per-slot resources (workspace, bound programs, rings) are allocated for
+// both slots the first time a gpu-let is created on this GPU, while no
+// executor runs there: device allocations can synchronise the device and
+// would block behind a persistent executor.  The workspace has 25 % headroom
+// for programs tiled for smaller gpu-lets (more split-K partials).
+static gl_status ensure_slot_res(gl_ctx* ctx, GpuState& G, int gpu) {
+  if (G.slot_res[0].ready) return GL_OK;
+  size_t ws = 256;
+  for (auto& m : ctx->models)
+    if (m && m->gpu == gpu)
+      for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
+  ws = (ws + ws / 4 + 255) / 256 * 256;
+  for (int s = 0; s < 2; ++s) {
+    SlotRes& R = G.slot_res[s];
+    R.ws_bytes = ws;
+    CK(cudaMalloc(&R.ws, ws), "cudaMalloc(workspace)");
+    CK(cudaMemset(R.ws, 0, ws), "memset(workspace)");
+    for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+      auto& m = ctx->models[mi];
+      if (!m || m->gpu != gpu) continue;
+      std::vector<OpDesc*>& v = R.progs[(int)mi];
+      v.assign(33, nullptr);
+      for (int b = 1; b <= 32; ++b) {
+        std::string berr;
+        v[b] = upload_bound(m->prog[b], R.ws, berr);
+        if (!v[b]) return fail(GL_E_CUDA, "gl_create_gpulet: " + berr);
+      }
+    }
+    CK(cudaHostAlloc((void**)&R.ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
+    CK(cudaHostGetDevicePointer((void**)&R.ring_dev, R.ring, 0), "cudaHostGetDevicePointer");
+    CK(cudaMalloc(&R.st, sizeof(ExecState)), "cudaMalloc(state)");
+    CK(cudaMalloc(&R.smid, 160 * sizeof(int)), "cudaMalloc(smid)");
+    R.ready = true;
+  }
+  CK(cudaDeviceSynchronize(), "slot resources");
+  return GL_OK;
+}
+
+// Programs tiled for a gpu-let of `nsm` SMs (N tile and split-K chosen for
+// that SM count instead of a whole B200: measured -3 to -10 % on 56- and
+// 96-SM gpu-lets), built and bound for `slot` once, while no executor runs on
+// the GPU (gl_create_gpulets).  A model whose programs do not fit the slot's
+// workspace keeps the whole-GPU tiling.
+static void bind_sized(gl_ctx* ctx, GpuState& G, int gpu, int slot, int nsm) {
+  if (nsm <= 0 || nsm >= G.nsm) return;
+  SlotRes& R = G.slot_res[slot];
+  for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
+    auto& m = ctx->models[mi];
+    if (!m || m->gpu != gpu || R.progs_sm.count({(int)mi, nsm})) continue;
+    std::vector<Program>& vp = m->prog_sm[nsm];
+    if (vp.empty()) {
+      vp.resize(33);
+      std::string err;
+      size_t ib = 0, ob = 0;
+      for (int b = 1; b <= 32; ++b)
+        if (!build_program(m->kind, b, m->host, *m->w, gpu, vp[b], ib, ob, err, nsm)) {
+          vp.clear();
+          break;
+        }
+      if (vp.empty()) continue;
+    }
+    bool fits = true;
+    for (int b = 1; b <= 32; ++b) fits &= vp[b].ws_bytes <= R.ws_bytes;
+    if (!fits) continue;
+    std::vector<OpDesc*> v(33, nullptr);
+    bool ok = true;
+    for (int b = 1; b <= 32 && ok; ++b) {
+      std::string berr;
+      v[b] = upload_bound(vp[b], R.ws, berr);
+      ok = v[b] != nullptr;
+    }
+    if (!ok) {
+      for (OpDesc* p : v)
+        if (p) cudaFree(p);
+      continue;
+    }
+    R.progs_sm[{(int)mi, nsm}] = std::move(v);
+  }
 }
 
 gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, int32_t* sm_count) {
@@ -632,38 +717,9 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     g->stream = G.gstream[slot][gi];
     g->nsm = G.gnsm[slot][gi];
   }
-  // Per-slot resources (workspace, bound programs, rings) are allocated for
-  // both slots the first time a gpu-let is created on this GPU, while no
-  // executor runs there: device allocations can synchronise the device and
-  // would block behind a persistent executor.
-  if (!G.slot_res[0].ready) {
-    size_t ws = 256;
-    for (auto& m : ctx->models)
-      if (m && m->gpu == gpu)
-        for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
-    for (int s = 0; s < 2; ++s) {
-      SlotRes& R = G.slot_res[s];
-      R.ws_bytes = ws;
-      CK(cudaMalloc(&R.ws, ws), "cudaMalloc(workspace)");
-      CK(cudaMemset(R.ws, 0, ws), "memset(workspace)");
-      for (size_t mi = 0; mi < ctx->models.size(); ++mi) {
-        auto& m = ctx->models[mi];
-        if (!m || m->gpu != gpu) continue;
-        std::vector<OpDesc*>& v = R.progs[(int)mi];
-        v.assign(33, nullptr);
-        for (int b = 1; b <= 32; ++b) {
-          std::string berr;
-          v[b] = upload_bound(m->prog[b], R.ws, berr);
-          if (!v[b]) return fail(GL_E_CUDA, "gl_create_gpulet: " + berr);
-        }
-      }
-      CK(cudaHostAlloc((void**)&R.ring, sizeof(HostRing), cudaHostAllocMapped), "cudaHostAlloc(ring)");
-      CK(cudaHostGetDevicePointer((void**)&R.ring_dev, R.ring, 0), "cudaHostGetDevicePointer");
-      CK(cudaMalloc(&R.st, sizeof(ExecState)), "cudaMalloc(state)");
-      CK(cudaMalloc(&R.smid, 160 * sizeof(int)), "cudaMalloc(smid)");
-      R.ready = true;
-    }
-    CK(cudaDeviceSynchronize(), "slot resources");
+  {
+    gl_status rc = ensure_slot_res(ctx, G, gpu);
+    if (rc) return rc;
   }
   dbg_log("create_gpulet: slot resources ready");
   SlotRes& R = G.slot_res[slot];
@@ -773,18 +829,26 @@ gl_status gl_submit_batch(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_
   if (mid < 0 || mid >= (int)ctx->models.size() || ctx->models[mid]->gpu != g.gpu)
     return fail(GL_E_MODEL, "gl_submit_batch: model not loaded on this gpu-let's GPU");
   Model& m = *ctx->models[mid];
-  auto& progs = ctx->gpus[g.gpu].slot_res[g.slot].progs;
-  auto pit = progs.find(mid);
-  if (pit == progs.end() || m.prog[batch].ws_bytes > g.ws_bytes)
+  SlotRes& SR = ctx->gpus[g.gpu].slot_res[g.slot];
+  auto pit = SR.progs.find(mid);
+  if (pit == SR.progs.end() || m.prog[batch].ws_bytes > g.ws_bytes)
     return fail(GL_E_STATE, "gl_submit_batch: model loaded after the gpu-let was created");
+  // the program tiled for this gpu-let's SM count when one is bound (else the whole-GPU tiling)
+  const OpDesc* prog = pit->second[batch];
+  int n_ops = (int)m.prog[batch].ops.size();
+  auto sit = SR.progs_sm.find({mid, g.nsm});
+  if (sit != SR.progs_sm.end()) {
+    prog = sit->second[batch];
+    n_ops = (int)m.prog_sm[g.nsm][batch].ops.size();
+  }
   if (g.tail - g.comp_seen >= (uint64_t)kRing - 1) return fail(GL_E_QUEUE_FULL, "gl_submit_batch: ring full");
   WorkDesc& w = g.ring->items[g.tail % kRing];
   const uint64_t t = ctx->next_ticket++;
   w.ticket = t;
-  w.prog = pit->second[batch];
+  w.prog = prog;
   w.in = in_dev;
   w.out = out_dev;
-  w.n_ops = (int)m.prog[batch].ops.size();
+  w.n_ops = n_ops;
   w.model = mid;
   w.batch = batch;
   w.slo_us = (int32_t)(slo_ms * 1000.0f);
@@ -1091,6 +1155,15 @@ extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const in
       gl_status rc = ensure_green(ctx, G, i, grid_index(pcts[i]));
       if (rc) return rc;
     }
+  // slot resources and the programs tiled for these gpu-let sizes, before any
+  // executor of this GPU runs (gpu-let i takes slot i)
+  {
+    gl_status rc = ensure_slot_res(ctx, G, gpu);
+    if (rc) return rc;
+  }
+  for (int i = 0; i < n; ++i)
+    bind_sized(ctx, G, gpu, i, pcts[i] == 100 ? G.nsm : G.gnsm[i][grid_index(pcts[i])]);
+  CK(cudaDeviceSynchronize(), "sized programs");
   for (int i = 0; i < n; ++i) {
     int32_t sm = 0;
     gl_status rc = gl_create_gpulet(ctx, gpu, pcts[i], &ids[i], &sm);

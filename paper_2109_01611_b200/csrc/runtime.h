@@ -68,19 +68,22 @@ struct Program {
 struct Model {
   int kind = 0;
   int gpu = 0;
-  ParamMap host;                 // host copy of the file (kept for repacking)
+  ParamMap host;                 // host copy of the file (kept: programs for other gpu-let sizes are built later)
   std::unique_ptr<DevWeights> w;
-  Program prog[33];              // per batch 1..32
+  Program prog[33];              // per batch 1..32, tiles for a whole B200 (148 SMs)
   size_t in_bytes[33] = {0}, out_bytes[33] = {0};
+  std::map<int, std::vector<Program>> prog_sm;   // SM count -> [batch] programs tiled for that gpu-let size
 };
 
 // Program-builder tuning overrides (gl_set_tuning; 0 = automatic choice).
-enum TuneKey { TUNE_BN = 0, TUNE_SPLIT = 1, TUNE_MISC = 2, TUNE_WARM = 3, TUNE_GATHER = 4, kTuneKeys = 8 };
+enum TuneKey { TUNE_BN = 0, TUNE_SPLIT = 1, TUNE_MISC = 2, TUNE_WARM = 3, TUNE_GATHER = 4, TUNE_SMS = 5, kTuneKeys = 8 };
 extern int g_tune[kTuneKeys];
 
 // Build the layer program of model `kind` at batch b (models.cpp).
+// sm_target: the SM count of the gpu-let the program is built for (tile
+// decomposition: N tile, split-K); 148 = a whole B200.
 bool build_program(int kind, int batch, const ParamMap& host, DevWeights& dw, int gpu, Program& out,
-                   size_t& in_bytes, size_t& out_bytes, std::string& err);
+                   size_t& in_bytes, size_t& out_bytes, std::string& err, int sm_target = 148);
 
 // Single-op programs for kernel unit tests (models.cpp).
 // in_ws: the input is first copied into the workspace so the TMA operand paths run.

@@ -16,13 +16,14 @@ def main():
     from paper_2109_01611_b200 import gpulet
     ctx = gpulet.Context(1)
     out = {"lib": os.environ.get("GL_LIB", "in-tree")}
-    mids = {m: ctx.load_model(0, m, synthgen.weight_file(m)) for m in ("lenet5", "resnet50")}
-    for pct in (20, 100):
+    mids = {m: ctx.load_model(0, m, synthgen.weight_file(m)) for m in ("lenet5", "resnet50", "vgg16", "googlenet")}
+    for pct in (20, 40, 80, 100):
         (gid, _n), = ctx.create_gpulets(0, [pct])
-        for m, b in (("lenet5", 1), ("lenet5", 24), ("resnet50", 1)):
+        for m, b in (("lenet5", 1), ("resnet50", 1), ("resnet50", 15), ("resnet50", 32), ("vgg16", 8),
+                     ("googlenet", 15)):
             x = common.device_input(m, 32)
             y = torch.empty(ctx.model_io(mids[m], 32)[1] // 4, device="cuda")
-            out[f"{m}_b{b}_p{pct}_us"] = round(ctx.profile(gid, mids[m], b, x, y, warmup=20, reps=200), 1)
+            out[f"{m}_b{b}_p{pct}_us"] = round(ctx.profile(gid, mids[m], b, x, y, warmup=5, reps=30), 1)
         ctx.destroy_gpulet(gid)
     print(json.dumps(out))
     ctx.close()

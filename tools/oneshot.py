@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="executor dbg_flags (tuning experiments)")
     ap.add_argument("--split", type=int, default=0, help="force split-K count when building programs (tuning)")
     ap.add_argument("--bn", type=int, default=0, help="force the UMMA N tile when building programs (tuning)")
+    ap.add_argument("--sm-target", type=int, default=0, help="SM count the tile decomposition targets (tuning)")
     a = ap.parse_args()
     import torch
     from paper_2109_01611_b200 import gpulet
@@ -35,6 +36,8 @@ def main():
         gpulet.Context.set_tuning(1, a.split)
     if a.bn:
         gpulet.Context.set_tuning(0, a.bn)
+    if a.sm_target:
+        gpulet.Context.set_tuning(5, a.sm_target)
     mid = ctx.load_model(0, a.model, synthgen.weight_file(a.model))
     x = common.device_input(a.model, a.batch)
     y = torch.empty(ctx.model_io(mid, a.batch)[1] // 4, device="cuda")
