@@ -351,15 +351,6 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& g, int lt, int& mb, 
   kb1 = min(nkb, kb0 + g.kb_per_split);
 }
 
-__device__ __forceinline__ int locate(const OpDesc* ops, int nops, int t, int& lt) {
-  int i = 0;
-  while (i < nops - 1 && t >= ops[i].n_units) {
-    t -= ops[i].n_units;
-    ++i;
-  }
-  lt = t;
-  return i;
-}
 
 // The ops of a GEMM step with their args served from the shared-memory cache
 // (read once per step instead of from global memory on every tile).
@@ -756,7 +747,6 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const int oi = so.locate(tile, lt);
-      const OpDesc* op = ops + oi;
       const GemmArgs& g = so.g(oi);
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);
@@ -815,7 +805,6 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const int oi = so.locate(tile, lt);
-      const OpDesc* op = ops + oi;
       const GemmArgs& g = so.g(oi);
       int mb, nb, kb0, kb1;
       decode_tile(g, lt, mb, nb, kb0, kb1);

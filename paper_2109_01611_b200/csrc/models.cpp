@@ -289,7 +289,7 @@ class Builder {
     if (!prog.ops.empty()) prog.ops.back().step_end = 1;
     // with barrier-free GEMM step joins (dataflow_enabled) a buffer may still be
     // read by a slower CTA while a faster one runs ahead: no reuse within a program
-    if (!dataflow_enabled() || std::getenv("GL_DATAFLOW_UNSAFE_REUSE"))   // (unsafe: timing experiments only)
+    if (!dataflow_enabled())
       for (uint64_t off : pending)
         for (auto& bl : blocks)
           if (bl.off == off) bl.free = true;

@@ -688,7 +688,6 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     }
   if (nlive >= 2 || used + pct > 100) return fail(GL_E_PARTITION, "gl_create_gpulet: gpu-let sizes on a GPU must sum to <= 100, at most 2");
   const int slot = G.slots[0] < 0 ? 0 : 1;
-  Driver& D = driver();
   CK(cudaSetDevice(G.dev), "cudaSetDevice");
   dbg_log("create_gpulet: begin");
   auto g = std::make_unique<Gpulet>();
