@@ -251,6 +251,44 @@ gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* 
  * test that path.  GL_E_ARG for an unknown key. */
 gl_status gl_set_tuning(int32_t key, int32_t value);
 
+/* ---- F3: the `traffic` application's detection -> recognition hand-off ----
+ * PAPER.md P:788-790 ("traffic": SSD-MobileNet detects objects, GoogLeNet and
+ * VGG-16 recognise them) and SURVEY §8(f) F3.  The paper does not define the
+ * detector's output stage; these calls implement the textbook SSD one with the
+ * readings of DESIGN.md §2 R27 (priors, variances 0.1/0.2, per-class greedy
+ * NMS, merge order, half-pixel bilinear crops).  They are stand-alone stream
+ * kernels (no gl_ctx): every pointer is a device pointer on the current
+ * device, owned by the caller; the calls are asynchronous on `stream` (a
+ * cudaStream_t, NULL = legacy default stream).  GL_E_ARG (with
+ * gl_last_error text) for a bad size or NULL pointer, GL_E_CUDA if a launch
+ * fails.  n_img == 0 is a no-op. */
+
+/* Workspace bytes gl_ssd_detect needs for n_img images and top_k (1..400). */
+gl_status gl_ssd_detect_workspace(int32_t n_img, int32_t top_k, size_t* bytes);
+
+/* SSD post-processing of the ssd_mobilenet_v1 model output (its layout,
+ * gl_model_io): loc [n_img][3000][4] fp32 (offsets per prior, head order map,
+ * row, column, prior) and conf [n_img][3000][21] fp32 softmax scores (class 0 =
+ * background).  Per image and class 1..20: priors with score > score_thr,
+ * ordered by (score desc, prior asc), the first top_k decoded and greedily
+ * suppressed (IoU > iou_thr, fp32); then all classes' survivors ordered by
+ * (score desc, class asc, prior asc), the first max_det written to det
+ * [n_img][max_det][7] = (x1, y1, x2, y2 in [0, 1], score, class, prior) and
+ * their number to count [n_img].  Rows past count are left untouched. */
+gl_status gl_ssd_detect(const float* loc_dev, const float* conf_dev, int32_t n_img, float score_thr, float iou_thr,
+                        int32_t top_k, int32_t max_det, float* det_dev, int32_t* count_dev, void* ws_dev,
+                        size_t ws_bytes, void* stream);
+
+/* Crops for the recognisers: for image n and slot k < per_img, detection k of
+ * gl_ssd_detect's output (det/count/max_det as written there) is cut from img
+ * [n_img][H][W][C] bf16 (NHWC, C == 8: the models' padded input layout) and
+ * resized to [OH][OW][C] by bilinear sampling with half-pixel centres (R27),
+ * written to out [n_img * per_img][OH][OW][C] bf16 at crop n * per_img + k;
+ * slots k >= count[n] are zero-filled. */
+gl_status gl_crop_resize(const void* img_dev, int32_t n_img, int32_t H, int32_t W, int32_t C, const float* det_dev,
+                         const int32_t* count_dev, int32_t max_det, int32_t per_img, int32_t OH, int32_t OW,
+                         void* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 
 SOURCES = [
     ("executor.cu", []),
+    ("detect.cu", []),
     ("runtime.cpp", []),
     ("models.cpp", []),
     ("frontend.cpp", []),

@@ -40,6 +40,9 @@ static gl_status fail(gl_status s, const std::string& m) {
   return s;
 }
 
+// the same thread-local error text for the stand-alone stage kernels (detect.cu)
+gl_status set_error(gl_status s, const char* m) { return fail(s, m); }
+
 Driver& driver() {
   static Driver d;
   static std::once_flag once;

@@ -22,7 +22,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3}
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
            "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
-           "gl_test_stats", "gl_set_tuning"]
+           "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
 
 
 class GpuletError(RuntimeError):
@@ -94,6 +94,9 @@ def lib():
             "gl_test_misc": [P, ctypes.c_int, I32, ctypes.POINTER(I32), I32, P, I64, P, P],
             "gl_test_stats": [ctypes.POINTER(U64), ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
             "gl_set_tuning": [I32, I32],
+            "gl_ssd_detect_workspace": [I32, I32, ctypes.POINTER(ctypes.c_size_t)],
+            "gl_ssd_detect": [P, P, I32, ctypes.c_float, ctypes.c_float, I32, I32, P, P, P, ctypes.c_size_t, P],
+            "gl_crop_resize": [P, I32, I32, I32, I32, P, P, I32, I32, I32, I32, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -304,6 +307,25 @@ class Context:
         ia = (ctypes.c_int32 * len(iargs))(*iargs)
         n = 0 if params is None else int(params.size)
         _check(lib().gl_test_misc(self.h, gpu, op, ia, len(iargs), _ptr(params), n, _ptr(x), _ptr(y)))
+
+
+def ssd_detect_workspace(n_img, top_k):
+    n = ctypes.c_size_t()
+    _check(lib().gl_ssd_detect_workspace(int(n_img), int(top_k), ctypes.byref(n)))
+    return n.value
+
+
+def ssd_detect(loc, conf, n_img, det, count, ws, score_thr=0.05, iou_thr=0.45, top_k=200, max_det=100, stream=0):
+    """gl_ssd_detect (F3, R27) on device tensors; asynchronous on `stream`."""
+    _check(lib().gl_ssd_detect(_ptr(loc), _ptr(conf), int(n_img), float(score_thr), float(iou_thr), int(top_k),
+                               int(max_det), _ptr(det), _ptr(count), _ptr(ws), int(ws.numel() * ws.element_size()),
+                               stream or None))
+
+
+def crop_resize(img, n_img, H, W, det, count, max_det, per_img, out, OH=224, OW=224, C=8, stream=0):
+    """gl_crop_resize (F3, R27) on device tensors; asynchronous on `stream`."""
+    _check(lib().gl_crop_resize(_ptr(img), int(n_img), int(H), int(W), int(C), _ptr(det), _ptr(count), int(max_det),
+                                int(per_img), int(OH), int(OW), _ptr(out), stream or None))
 
 
 def schedule(names, lat_us, l2, mem, slo_us, rates, num_gpus, mode, coeffs=(0, 0, 0, 0, 0), cap=1 << 20):
