@@ -308,11 +308,13 @@ __global__ void __launch_bounds__(128) crop_kernel(const __nv_bfloat16* __restri
                                                    int max_det, int per_img, int OH, int OW,
                                                    __nv_bfloat16* __restrict__ out) {
   const int crop = blockIdx.y, n = crop / per_img, k = crop % per_img;
-  const int pix0 = (blockIdx.x * blockDim.x + threadIdx.x) * kCropPix;
+  // pixel q of this thread: blockIdx.x * 4 * blockDim + q * blockDim + tid, so
+  // one warp store covers 32 consecutive pixels (512 contiguous bytes)
+  const int pix0 = blockIdx.x * blockDim.x * kCropPix + threadIdx.x, step = blockDim.x;
   if (pix0 >= OH * OW) return;
   uint4* dst = (uint4*)(out + ((int64_t)crop * OH * OW) * 8);
   if (k >= __ldg(count + n)) {
-    for (int q = 0; q < kCropPix && pix0 + q < OH * OW; ++q) dst[pix0 + q] = make_uint4(0, 0, 0, 0);
+    for (int q = 0; q < kCropPix && pix0 + q * step < OH * OW; ++q) dst[pix0 + q * step] = make_uint4(0, 0, 0, 0);
     return;
   }
   const float* d = det + ((int64_t)n * max_det + k) * 7;
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(128) crop_kernel(const __nv_bfloat16* __restri
   float wxs[kCropPix], wys[kCropPix];
 #pragma unroll
   for (int q = 0; q < kCropPix; ++q) {   // issue all tap loads first
-    const int pix = min(pix0 + q, OH * OW - 1), oy = pix / OW, ox = pix % OW;
+    const int pix = min(pix0 + q * step, OH * OW - 1), oy = pix / OW, ox = pix % OW;
     float sy = __fsub_rn(__fadd_rn(__fmul_rn(y1, fH), __fmul_rn(__fadd_rn((float)oy, 0.5f), sh)), 0.5f);
     float sx = __fsub_rn(__fadd_rn(__fmul_rn(x1, fW), __fmul_rn(__fadd_rn((float)ox, 0.5f), sw)), 0.5f);
     sy = fminf(fmaxf(sy, 0.f), (float)(H - 1));
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(128) crop_kernel(const __nv_bfloat16* __restri
   }
 #pragma unroll
   for (int q = 0; q < kCropPix; ++q) {
-    if (pix0 + q >= OH * OW) break;
+    if (pix0 + q * step >= OH * OW) break;
     const __nv_bfloat16 *v0 = (const __nv_bfloat16*)&q4[q][0], *v1 = (const __nv_bfloat16*)&q4[q][1],
                         *v2 = (const __nv_bfloat16*)&q4[q][2], *v3 = (const __nv_bfloat16*)&q4[q][3];
     uint4 r;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(128) crop_kernel(const __nv_bfloat16* __restri
       const float bot = lerp_rn(__bfloat162float(v2[ch]), __bfloat162float(v3[ch]), wxs[q]);
       rb[ch] = __float2bfloat16_rn(lerp_rn(top, bot, wys[q]));
     }
-    dst[pix0 + q] = r;
+    dst[pix0 + q * step] = r;
   }
 }
 
