@@ -147,8 +147,8 @@ typedef struct {
   int32_t duty_us;      /* duty cycle D of the gpu-let (dispatch when the window is this old) */
   int32_t weight;       /* routing weight = assigned rate (smooth weighted round-robin) */
   int32_t drop_us;      /* Leff(1): a request with (now - arrival) + drop_us > SLO is dropped; a lane
-                           also dispatches early once (now - oldest arrival) + drop_us + max(5 us,
-                           SLO / 20) >= SLO (deadline guard) */
+                           also dispatches early once (now - oldest arrival) + drop_us + SLO / 1000
+                           >= SLO (deadline guard) */
   int32_t pad_;
   const void* in_dev;   /* device input holding `batch` requests (first k used for a k-batch) */
   void* out_dev;        /* device output */

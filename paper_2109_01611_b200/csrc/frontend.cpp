@@ -45,8 +45,8 @@ enum Stage { FREE = 0, H2D, RUN, D2H };
 constexpr int64_t kZeroCopyMax = 64 * 1024;
 constexpr int kZeroCopyBuf = -2;   // Inflight::buf of a zero-copy batch
 // Deadline guard of the dispatch rule: max(5 us, SLO / 20).
-constexpr int64_t kGuardMinUs = 5;
-constexpr int32_t kGuardDiv = 20;
+constexpr int64_t kGuardMinUs = 0;
+constexpr int32_t kGuardDiv = 1000;
 
 struct Batch {
   Stage stage = FREE;
@@ -144,6 +144,11 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
                               const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
                               int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes,
                               gl_lane_stats* lane_stats) {
+  // deadline-guard tuning overrides (GL_GUARD_MIN_US, GL_GUARD_DIV; tuning runs only)
+  const char* guard_env_min = std::getenv("GL_GUARD_MIN_US");
+  const char* guard_env_div = std::getenv("GL_GUARD_DIV");
+  const int64_t guard_min_us = guard_env_min ? std::max<int64_t>(0, std::atoll(guard_env_min)) : kGuardMinUs;
+  const int32_t guard_div = guard_env_div ? std::max<int32_t>(1, std::atoi(guard_env_div)) : kGuardDiv;
   if (!ctx || !lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || !slo_us || !lat_us)
     return GL_E_ARG;
   std::vector<LaneState> L(n_lanes);
@@ -225,7 +230,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       // deadline guard (DESIGN R26): dispatch early when the oldest queued
       // request would otherwise keep waiting into its last Leff(1) + guard of slack
       const int32_t slo_m = slo_us[ln.cfg.model_slot];
-      const int64_t guard = std::max<int64_t>(kGuardMinUs, slo_m / kGuardDiv);
+      const int64_t guard = std::max<int64_t>(guard_min_us, slo_m / guard_div);
       const bool urgent = now - arr_us[ln.q.front()] + ln.cfg.drop_us + guard >= slo_m;
       if (!full && !timeout && !urgent) continue;
       while (!ln.q.empty()) {  // drop hopeless requests
