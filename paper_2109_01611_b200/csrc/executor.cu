@@ -129,8 +129,10 @@ __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
   }
   ++epoch;
   __syncthreads();
-  // the next step's TMA (async proxy) reads what other CTAs stored (generic proxy)
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+  // The next step's TMA (async proxy) reads what other CTAs stored (generic
+  // proxy): the thread that issues a step's TMA loads executes
+  // fence.proxy.async.global itself before its first load (tma_role_fence),
+  // so the other threads do not wait on the proxy fence here.
 }
 
 // ------------------------------------------------------------------ epilogue helpers
@@ -621,7 +623,10 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   if (gstep && warp < 4) {
     // ---------------- gather producers (128 threads; thread 0 also issues the TMA half)
     const int t = threadIdx.x;
-    if (t == 0) dbg_mark(S, 0);
+    if (t == 0) {
+      tma_role_fence();
+      dbg_mark(S, 0);
+    }
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const int oi = so.locate(tile, lt);
@@ -690,6 +695,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     if (t == 0) dbg_mark(S, 1);
   } else if (!gstep && warp == 9) {
     // ---------------- TMA producer (whole warp walks the loop; one elected lane issues)
+    tma_role_fence();
     if (lane == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
@@ -1436,6 +1442,7 @@ __device__ __noinline__ void attention_tc(const OpDesc* op, const Ctx& X, const 
   uint8_t *sQ = S.a[0], *sK = S.a[1], *sV = S.a[2], *sP = S.b[0];
   const uint32_t tbase = *S.tmem_base;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) tma_role_fence();
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int seq = u / H, h = u - seq * H, row0 = seq * 128;
     const uint32_t ph = P.att_phase & 1;

@@ -95,6 +95,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// Generic-proxy global stores observed (through the gpu-let barrier's
+// release/acquire) before this fence are visible to the async-proxy (TMA)
+// operations this thread issues after it.
+__device__ __forceinline__ void tma_role_fence() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -245,8 +245,9 @@ struct GpuState {
   int dev = 0;
   int nsm = 0;
   bool split = false;
-  CUdevResource groups[32];
+  CUdevResource groups[160];
   unsigned ngroups = 0;
+  bool fine = false;               // SM-pair split (no co-scheduling groups)
   CUdevResource rem;
   uint32_t used_groups = 0;
   bool rem_used = false;
@@ -280,14 +281,14 @@ static gl_status cu_check(gl_ctx* c, CUresult r, const char* what) {
     if (_s != GL_OK) return _s;                      \
   } while (0)
 
-static int sm_for_pct(int pct) {
+// SMs of a p % gpu-let on a GPU of `total` SMs: p % of the SMs rounded to an
+// even count (SM pairs), so the paper's pairs (p, 100 - p) split the
+// GPU exactly: 148 -> 20 %: 30, 40 %: 60, 50 %: 74, 60 %: 88, 80 %: 118, 100 %: 148.
+static int sm_for_pct(int pct, int total = 148) {
   switch (pct) {
-    case 20: return 32;
-    case 40: return 56;
-    case 50: return 72;
-    case 60: return 92;
-    case 80: return 116;
-    case 100: return 148;
+    case 20: case 40: case 50: case 60: case 80:
+      return 2 * ((pct * (total / 2) + 50) / 100);
+    case 100: return total;
     default: return -1;
   }
 }
@@ -315,10 +316,21 @@ static gl_status prepare_green(gl_ctx* ctx, GpuState& G) {
   CUdevResource all;
   rc = cu_check(ctx, D.deviceGetDevResource(cud, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
   if (rc) return rc;
-  G.ngroups = 32;
-  rc = cu_check(ctx, D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem, 0, 8),
-                "cuDevSmResourceSplitByCount");
-  if (rc) return rc;
+  // The executor uses no thread-block clusters, so the split ignores SM
+  // co-scheduling: SM pairs instead of 8-SM groups, which lets every grid size
+  // take exactly its share (8-SM groups on this pool's B200s come as 15 groups
+  // + a 28-SM remainder, i.e. 24/48/56/72/96 SMs).  Drivers that refuse the
+  // flag get the co-scheduled 8-SM split.
+  G.ngroups = 160;
+  CUresult r = D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem,
+                                           CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING, 2);
+  G.fine = r == CUDA_SUCCESS;
+  if (!G.fine) {
+    G.ngroups = 160;
+    rc = cu_check(ctx, D.devSmResourceSplitByCount(G.groups, &G.ngroups, &all, &G.rem, 0, 8),
+                  "cuDevSmResourceSplitByCount");
+    if (rc) return rc;
+  }
   G.split = true;
   cudaStream_t s;
   if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return fail(GL_E_CUDA, "stream");
@@ -335,27 +347,27 @@ static gl_status ensure_green(gl_ctx* ctx, GpuState& G, int slot, int gi) {
   CUdevice cud;
   gl_status rc = cu_check(ctx, D.deviceGet(&cud, G.dev), "cuDeviceGet");
   if (rc) return rc;
-  const int want = sm_for_pct(pcts[gi]);
+  const int want = sm_for_pct(pcts[gi], G.nsm);
   std::vector<CUdevResource> res;
   int have = 0;
-  // The split yields `ngroups` co-schedulable 8-SM groups plus a remainder
-  // whose size depends on the physical GPU's floorsweeping (measured: 15
-  // groups + 28 SMs on this pool's B200s, not 18 + 4).  Slot 0 takes
-  // k = floor(p * ngroups / 100) groups from the front; slot 1 takes the
-  // remainder + floor(q * ngroups / 100) groups from the back, so any pair with
-  // p + q <= 100 is disjoint (scripts/diag_pairs.py audits the SM ids).
-  (void)want;
-  const int k_groups = pcts[gi] * (int)G.ngroups / 100;
-  if (slot == 1 && G.rem.sm.smCount > 0) {
-    res.push_back(G.rem);
-    have += (int)G.rem.sm.smCount;
+  // Slot 0 takes groups from the front of the split, slot 1 from the back
+  // (the remainder first), each until it holds `want` SMs; for shares p + q
+  // <= 100 the two sets are disjoint (the %smid audit of
+  // tests/test_gpu_executor.py checks it).  With the SM-pair split every size
+  // is exact; with 8-SM groups it is the smallest group count reaching `want`
+  // minus one group (sizes never exceed their share).
+  std::vector<CUdevResource> order;
+  if (slot == 1 && G.rem.sm.smCount > 0) order.push_back(G.rem);
+  for (unsigned k = 0; k < G.ngroups; ++k) order.push_back(G.groups[slot == 0 ? k : G.ngroups - 1 - k]);
+  for (const CUdevResource& r : order) {
+    if (have >= want) break;
+    if (!G.fine && have + (int)r.sm.smCount > want) break;
+    res.push_back(r);
+    have += (int)r.sm.smCount;
   }
-  for (int k = 0; k < k_groups && k < (int)G.ngroups; ++k) {
-    const unsigned i = slot == 0 ? (unsigned)k : G.ngroups - 1 - (unsigned)k;
-    res.push_back(G.groups[i]);
-    have += (int)G.groups[i].sm.smCount;
-  }
-  if (have < 8 * k_groups) return fail(GL_E_PARTITION, "ensure_green: not enough SM groups");
+  if (have <= 0 || (G.fine && have != want))
+    return fail(GL_E_PARTITION, "ensure_green: the SM split cannot give " + std::to_string(want) + " SMs (got " +
+                                    std::to_string(have) + ")");
   CUdevResourceDesc desc;
   rc = cu_check(ctx, D.devResourceGenerateDesc(&desc, res.data(), (unsigned)res.size()), "cuDevResourceGenerateDesc");
   if (rc) return rc;
@@ -699,10 +711,8 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
   g->pct = pct;
   // Green contexts are cached per (slot, size).  cuGreenCtxCreate can block
   // behind a running persistent kernel, so gl_create_gpulets creates a whole
-  // GPU partition's contexts before launching any executor.  Slot 0 takes
-  // 8-SM groups from the front, slot 1 from the back; shares >= 60 % add the
-  // 4-SM remainder, so any pair with sizes summing to <= 100 is disjoint
-  // (k(20)=4, k(40)=7, k(50)=9, k(60)=11, k(80)=14 of 18 groups).
+  // GPU partition's contexts before launching any executor.  Slot 0 takes SM
+  // pairs from the front of the split, slot 1 from the back (ensure_green).
   if (!G.green_ready) {
     gl_status rc = prepare_green(ctx, G);
     if (rc) return rc;
@@ -769,12 +779,25 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
       cudaMemcpy(sm.data(), g->smid, 160 * sizeof(int), cudaMemcpyDeviceToHost);
       std::string ids;
       for (int i = 0; i < g->nsm; ++i) ids += (g->ring->resident[i] ? std::to_string(sm[i]) : std::string("-")) + " ";
+      // drain the partly resident kernel before the slot's ring / state can be
+      // reused: resident CTAs see quit and leave, freeing SMs for the rest; a
+      // kernel that does not drain poisons the context
+      const auto td = std::chrono::steady_clock::now();
+      cudaError_t qe;
+      while ((qe = cudaStreamQuery((cudaStream_t)g->stream)) == cudaErrorNotReady &&
+             std::chrono::steady_clock::now() - td < std::chrono::seconds(20))
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+      --g_live_exec;
+      if (qe != cudaSuccess) ctx->poisoned = true;
       return fail(GL_E_NOT_CONCURRENT, "gl_create_gpulet: executor CTAs not co-resident (" + std::to_string(n) + "/" +
                                             std::to_string(g->nsm) + ") slot " + std::to_string(slot) + " pct " +
                                             std::to_string(pct) + " smids: " + ids);
     }
     cudaError_t e = cudaStreamQuery((cudaStream_t)g->stream);
-    if (e != cudaErrorNotReady && e != cudaSuccess) return cuda_check(ctx, e, "executor launch");
+    if (e != cudaErrorNotReady && e != cudaSuccess) {
+      --g_live_exec;
+      return cuda_check(ctx, e, "executor launch");
+    }
     std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
   g->alive = true;

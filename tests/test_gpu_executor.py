@@ -23,10 +23,10 @@ def c():
 def test_pair_confinement(c, p, q):
     (a, na), (b, nb) = c.create_gpulets(0, [p, q])
     try:
-        # slot 0: floor(p * ngroups / 100) 8-SM groups from the front; slot 1: the
-        # remainder + floor(q * ngroups / 100) groups from the back (ngroups and the
-        # remainder depend on the physical GPU)
-        assert na % 8 == 0 and na >= 8 and nb >= 8 and na + nb <= 148
+        # SM-pair split (no co-scheduling groups): a p % gpu-let holds p % of the
+        # 148 SMs rounded to an even count, so (p, 100 - p) pairs split exactly
+        share = {20: 30, 40: 60, 50: 74, 60: 88, 80: 118}
+        assert (na, nb) == (share[p], share[q]) and na + nb == 148
         sa, sb = c.gpulet_smids(a), c.gpulet_smids(b)
         assert len(set(sa)) == na and len(set(sb)) == nb      # one CTA per SM
         assert not set(sa) & set(sb)                          # disjoint SM sets

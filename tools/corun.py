@@ -93,7 +93,10 @@ def main():
                     solo[(side, m, b)] = float(np.median(L))
         for m1, m2 in itertools.combinations(models, 2):
             for b1, b2 in itertools.product(batches, batches):
-                for (mA, bA, mB, bB) in ((m1, b1, m2, b2), (m2, b2, m1, b1)):
+                # with both p and 100 - p in the split list the swapped placement is
+                # the other split's sample (slots of one size are the same size)
+                orders = ((m1, b1, m2, b2),) if (100 - p) in splits else ((m1, b1, m2, b2), (m2, b2, m1, b1))
+                for (mA, bA, mB, bB) in orders:
                     LA, LB = run_loop(ctx, [(ga, mids[mA], bA, xs[mA], ys[(mA, 0)]),
                                             (gb, mids[mB], bB, xs[mB], ys[(mB, 1)])], a.ms)
                     fA = float(np.median(LA)) / solo[(0, mA, bA)]
