@@ -233,11 +233,22 @@ class Server:
     HOST_SLOTS = 64
     HOST_SLOTS_SMALL = 1024
 
-    def __init__(self, ctx, gpu, prof, e2e):
+    def __init__(self, ctx, gpu, e2e, profile_csv=None, coeffs_json=None, slo_mode="rule"):
         import torch
+        from paper_2109_01611_b200 import gpulet
         from tools import common
         self.ctx, self.gpu = ctx, gpu
-        self.lat, self.l2, self.mem, self.slo, self.coeffs = prof
+        # SPEC-format files, parsed and post-processed (C4.1 envelope, C4.2 SLOs)
+        # natively by libgpulet; every plan comes from gl_schedule_files
+        self.profile_csv = profile_csv or common.PROFILE_CSV
+        self.coeffs_json = coeffs_json or common.COEFFS_JSON
+        self.slo_mode = slo_mode
+        if not os.path.exists(self.profile_csv):
+            raise SystemExit(f"missing {self.profile_csv}: run tools/profile_sweep.py on the GPU first")
+        lat, l2, mem, sm = gpulet.profile_load(self.profile_csv)
+        self.lat, self.l2, self.mem = lat.tolist(), l2.tolist(), mem.tolist()
+        self.sm_of = dict(zip(common.GRID, sm.tolist()))
+        self.slo = gpulet.workload_rates(lat, "equal", 1.0, 1, slo_mode)[0]
         self.mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
         self.x, self.y, self.xh, self.yh, self.req_bytes = {}, {}, {}, {}, {}
         self.x2, self.y2 = {}, {}
@@ -268,21 +279,24 @@ class Server:
         self.made, self.lanes = [], []
         self.made_sizes, self.made_nsm, self.reorganised = None, [], False
 
-    def plan(self, scen, mode, n_gpus, x):
+    def _schedule(self, workload):
         from paper_2109_01611_b200 import gpulet
-        from tools import common
-        rates = [r * n_gpus for r in common.scenario_rates(scen, self.slo, x)]
-        dump, ok = gpulet.schedule(common.MODELS, self.lat, self.l2, self.mem, self.slo, rates, n_gpus, mode,
-                                   self.coeffs)
-        return rates, dump, ok
+        workload = dict(workload, slo_mode=self.slo_mode)
+        head, dump, ok, _text = gpulet.schedule_files(self.profile_csv, self.coeffs_json, workload)
+        return head["rates"], dump, ok
+
+    def plan(self, scen, mode, n_gpus, x):
+        """gl_schedule_files on the scenario at multiplier x (rates scaled natively, C4.3-C4.4).
+        A multiplier at which a model of the scenario truncates to rate 0 is not schedulable."""
+        return self._schedule({"scenario": scen, "x": float(x), "num_gpus": n_gpus, "mode": mode})
 
     def plan_rates(self, rates, n_gpus=1, mode="gpulet"):
         """Plan for explicit per-model rates (periodic rescheduling, tools/adapt.py)."""
+        return self._schedule({"rates": [int(r) for r in rates], "num_gpus": n_gpus, "mode": mode})
+
+    def scenario_rates(self, scen, x, n_gpus=1):
         from paper_2109_01611_b200 import gpulet
-        from tools import common
-        dump, ok = gpulet.schedule(common.MODELS, self.lat, self.l2, self.mem, self.slo, list(rates), n_gpus, mode,
-                                   self.coeffs)
-        return list(rates), dump, ok
+        return gpulet.workload_rates(self.lat, scen, x, n_gpus, self.slo_mode)[1]
 
     def max_sched_x(self, scen, mode, n_gpus):
         lo, hi = 0.0, 0.25
@@ -315,6 +329,12 @@ class Server:
             made = self.ctx.create_gpulets(self.gpu, sizes) if used else []
             self.made = [gid for gid, _n in made]
             self.made_sizes, self.made_nsm = sizes, [n for _g, n in made]
+            for p, (_gid, n) in zip(sizes, made):
+                # the plan's latencies are the profile's, measured on sm_count SMs of this size
+                if n != self.sm_of[p]:
+                    self.teardown()
+                    raise SystemExit(f"gpu-let of {p}% has {n} SMs but {self.profile_csv} was measured on "
+                                     f"{self.sm_of[p]}: re-run tools/profile_sweep.py on this GPU")
         my_rates = [0] * len(common.MODELS)
         if not used:
             return my_rates
@@ -322,7 +342,7 @@ class Server:
             for ln in g["lanes"]:
                 m = ln["model"]
                 mi = common.MODELS.index(m)
-                drop = (self.lat[mi][0][common.GRID.index(g["size"])] * ln["F"] + 999) // 1000
+                drop = (self.lat[mi][0][common.GRID.index(g["size"])] * ln["F"] + 999) // 1000   # Leff(1)
                 ib, ob = self.req_bytes[m]
                 self.lanes.append(dict(gpulet=gid, model_id=self.mids[m], model_slot=mi, batch=ln["batch"],
                                        duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.x[m, g["slot"]],
@@ -371,10 +391,10 @@ def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
     """Rate search + timed windows for one (scenario, mode).  Returns a dict."""
     from tools import common
     xs = srv.max_sched_x(scen, mode, world)
-    if sum(srv.plan(scen, mode, world, xs)[0]) == 0:
-        # no positive rate vector of this scenario is schedulable on `world` GPU(s)
-        return {"value": 0.0, "x_sched": xs, "x": 0.0, "probes": [], "rates": [0] * len(common.MODELS),
-                "note": f"not schedulable on {world} GPU(s) at any positive rate"}
+    if not srv.plan(scen, mode, world, xs)[2]:
+        # no multiplier gives every model of the scenario a positive, schedulable rate on `world` GPU(s)
+        return {"value": None, "x_sched": xs, "x": 0.0, "probes": [], "rates": [0] * len(common.MODELS),
+                "note": f"not schedulable on {world} GPU(s) at any multiplier that keeps every model of the scenario"}
     best, probes = search(srv, dist, rank, world, scen, mode, a, xs, e2e=False)
     if best is None:
         return {"value": 0.0, "x_sched": xs, "x": 0.0, "probes": probes, "rates": [0] * len(common.MODELS)}
@@ -587,13 +607,8 @@ def our_arm(a, world, rank, local, dist):
 
     torch.cuda.set_device(local)
     ctx = gpulet.Context(local + 1)
-    if not os.path.exists(common.PROFILE_CSV):
-        raise SystemExit(f"missing {common.PROFILE_CSV}: run tools/profile_sweep.py on the GPU first")
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
-    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
-    slo = common.slos_from(lat_env)
-    prof = (lat_env, l2, mem, slo, common.load_coeffs())
-    srv = Server(ctx, local, prof, a.e2e)
+    srv = Server(ctx, local, a.e2e)
+    slo = srv.slo
     head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, timed=True, clocks=True)
     extra = {}
     if not a.headline_only:

@@ -82,8 +82,12 @@ gl_status gl_model_cost(gl_ctx* ctx, int32_t model_id, int32_t batch, double* fl
 
 /* ---- gpu-lets (§2.3) ------------------------------------------- */
 /* Create a gpu-let of sm_pct in {20,40,50,60,80,100} % on `gpu`: a green context
- * over 8-SM groups (20->32, 40->56, 50->72, 60->92, 80->116, 100->148 SMs) running
- * one persistent executor kernel (1 CTA per SM).  At most two per GPU, sizes summing
+ * over SM pairs split without co-scheduling groups (the executor uses no clusters),
+ * so every share is exact: 2 * round(p * SMs / 200) SMs = 30, 60, 74, 88, 118 of
+ * 148 (100 % = the whole GPU, no green context), slot 0 from the front of the split
+ * and slot 1 from the back (disjoint for p + q <= 100).  Drivers that refuse the
+ * flag get co-scheduled 8-SM groups (never more than the share).  Runs one
+ * persistent executor kernel (1 CTA per SM).  At most two per GPU, sizes summing
  * to <= 100.  Waits (<= 5 s) until every executor CTA is resident.
  * Out: *gpulet_id, *sm_count (actual SMs).  Errors: GL_E_GRID, GL_E_PARTITION,
  * GL_E_NOT_CONCURRENT, GL_E_CUDA. */
@@ -146,9 +150,7 @@ typedef struct {
   int32_t batch;        /* planned batch b_i (dispatch when this many are queued) */
   int32_t duty_us;      /* duty cycle D of the gpu-let (dispatch when the window is this old) */
   int32_t weight;       /* routing weight = assigned rate (smooth weighted round-robin) */
-  int32_t drop_us;      /* Leff(1): a request with (now - arrival) + drop_us > SLO is dropped; a lane
-                           also dispatches early once (now - oldest arrival) + drop_us + SLO / 1000
-                           >= SLO (deadline guard) */
+  int32_t drop_us;      /* Leff(1): a request with (now - arrival) + drop_us > SLO is dropped */
   int32_t pad_;
   const void* in_dev;   /* device input holding `batch` requests (first k used for a k-batch) */
   void* out_dev;        /* device output */
@@ -161,6 +163,11 @@ typedef struct {
   int32_t pad2_;
   const void* in_dev2;  /* end-to-end mode, optional second device input/output pair: with it a lane keeps */
   void* out_dev2;       /*   two batches in flight (one copying while the other runs); NULL = one */
+  const int32_t* leff_us; /* [32] Leff(k) = ceil(L(k, p) F / 1000) µs of this lane for k = 1..32, or NULL
+                           (every k costs drop_us).  Deadline guard (DESIGN R26): a lane also dispatches
+                           when (now - oldest arrival) + Leff(min(queued, batch)) >= SLO, i.e. at the
+                           last moment the batch it would send can still finish in time; gl_serve_sim
+                           uses it as the service time */
 } gl_lane;
 /* Replay an arrival trace in real time (host clock): arr_us[n_req] sorted arrival
  * times (us from the call), arr_model[n_req] model slot of each request.  Returns
@@ -178,9 +185,32 @@ typedef struct {
  * one batch in flight, two with in_dev2/out_dev2.  *h2d_bytes / *d2h_bytes (may
  * be NULL) return the bytes copied; lane_stats (may be NULL; n_lanes entries) the
  * per-lane execution record.  The frontend thread never blocks on a copy
- * (GL_SERVE_RT=1: it runs SCHED_FIFO priority 10 during the call when permitted).
+ * (gl_set_tuning(7, 1): it runs SCHED_FIFO priority 10 during the call when permitted).
  * Blocks until every request is completed or dropped.  Errors: GL_E_ARG,
  * GL_E_TIMEOUT, GL_E_CUDA, errors of submit/poll. */
+/* Dispatch rule (SURVEY §8(c) C2.11 + DESIGN R26), shared by gl_serve and gl_serve_sim:
+ * at time t a lane with a non-empty FIFO dispatches when (a) it holds >= batch requests,
+ * (b) t - window_open >= duty_us, or (c) t - arrival(oldest) + Leff(min(queued, batch))
+ * >= SLO.  Dispatching first drops every queued request with (t - arrival) + Leff(1) > SLO
+ * (a drop is a violation), reopens the window at t and sends the
+ * min(queued, batch) oldest requests.  Arrivals are routed (smooth weighted round-robin
+ * over the model's lanes, weights = assigned rates, first maximum wins) before the lanes
+ * are checked in lane order; a lane re-checks at the same t after a dispatch. */
+
+/* Virtual-clock replay of the same frontend (no GPU; the fake backend of SURVEY §8(c)
+ * C5): the dispatch rule above, evaluated at every arrival and at every lane deadline
+ * (window_open + duty_us, arrival(oldest) + SLO - Leff(min(queued, batch))), against
+ * gpu-lets that run their batches FIFO, each taking Leff(k) of its lane (leff_us must
+ * be set).  Lanes with the same `gpulet` id share one FIFO.  Only the lane fields
+ * gpulet, model_slot, batch, duty_us, weight, drop_us, leff_us are read.  Out:
+ * lat_us[n_req] = completion - arrival (µs; -1 dropped or no lane for the model);
+ * batch_log (optional, cap rows of 4 int64: lane, dispatch time, k, index of the
+ * batch's first request in the trace) and *n_log (rows produced; rows past cap are
+ * counted, not written).  Errors: GL_E_ARG. */
+gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                       const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
+                       int64_t* batch_log, int64_t cap, int64_t* n_log);
+
 /* Per-lane execution record of one gl_serve call: batches and requests run, and
  * the summed device time of its batches (t_end - t_start, %globaltimer ns: the
  * executor's own clock, since a persistent kernel has no per-batch launch). */
@@ -205,13 +235,83 @@ typedef struct {
   const int32_t* rates;      /* [n_models] req/s */
   double coeffs[5];          /* c1..c5 of P:641 (used by mode 1) */
   int32_t num_gpus;
-  int32_t mode;              /* 0 gpulet, 1 gpulet+int, 2 sbp (whole-GPU temporal), 3 ideal */
+  int32_t mode;              /* 0 gpulet, 1 gpulet+int, 2 sbp (whole-GPU temporal), 3 ideal, 4 sbp50 (SBP on
+                                the two 50 % gpu-lets of every GPU, Fig. success-case) */
+  const int32_t* sm_count;   /* [6] SMs of each grid size (printed as "sm" in the plan dump); NULL = the
+                                exact shares of 148 SMs in SM pairs: 30, 60, 74, 88, 118, 148 */
 } gl_sched_input;
-/* Produce the canonical plan dump (JSON lines) into plan_buf (cap
- * bytes, NUL-terminated); *len = bytes written (excluding NUL); *verdict = 1
- * Schedulable / 0 NotSchedulable.  Integer maths except the knee and the factor
- * (IEEE double, fixed order).  Errors: GL_E_ARG, GL_E_BUDGET (buffer too small). */
+/* Array form of the scheduler (callers that already hold the tables, e.g. the
+ * scheduler sweeps).  Produce the canonical plan dump (JSON lines)
+ * into plan_buf (cap bytes, NUL-terminated); *len = bytes written (excluding
+ * NUL); *verdict = 1 Schedulable / 0 NotSchedulable.  Integer maths except the
+ * knee and the factor (IEEE double, fixed order).  Errors: GL_E_ARG, GL_E_BUDGET
+ * (buffer too small). */
 gl_status gl_schedule(const gl_sched_input* in, char* plan_buf, size_t cap, size_t* len, int32_t* verdict);
+
+/* ---- SPEC-format files: profile CSV, coeffs JSON, workload JSON ------
+ * Profile CSV (SPEC S:130 + sm_count): header row naming at least
+ *   model,batch,partition_pct and latency_us (integer or decimal µs) or latency_ms
+ *   (decimal ms, SPEC's unit); optional sm_count, l2_util, mem_bw_util (blank allowed;
+ *   read at the stat batches 1,2,4,8,16,32 only).  Decimal latencies are converted
+ *   exactly (decimal shift) and rounded UP to whole µs.  Every one of the
+ *   six canonical models (lenet5, googlenet, resnet50, ssd_mobilenet_v1, vgg16,
+ *   bert_base) needs all 32 x 6 (batch 1..32, p in {20,40,50,60,80,100}) rows.
+ * C4.1: unless `flags` bit 0 (strict, SPEC S:41-42 / S:58) is set the
+ *   latencies are replaced by their min-envelope L*(b,p) = min over b' >= b, p' <= p
+ *   (realisable: pad the batch / run on fewer SMs); strict mode keeps the raw table
+ *   and reports a monotonicity violation as GL_E_DATA.
+ * Errors: GL_E_ARG (NULL), GL_E_PARSE (unreadable file, malformed row: gl_last_error
+ *   names the line), GL_E_DATA (unknown model, p off the grid, batch outside 1..32,
+ *   duplicate or missing row, latency <= 0, utilisation outside [0,1], inconsistent
+ *   sm_count, strict-mode monotonicity violation naming (model, b, p)).
+ * Out (host arrays, all optional): lat_us [6][32][6] int µs; l2, mem [6][6 stat
+ *   batches][6] doubles (0 where blank); sm_count [6] (from the CSV, else the defaults
+ *   of gl_sched_input). */
+gl_status gl_profile_load(const char* profile_csv, int32_t flags, int32_t* lat_us, double* l2, double* mem,
+                          int32_t* sm_count);
+
+/* SLOs and rates of a workload from an enveloped table
+ * lat_us [6][32][6]:
+ *  slo_mode 0 = rule: SLO_m = 2 * L*_m(32, 100 %) ("set by doubling the
+ *    solo execution latency ... batch size of 32"); 1 = table: Table tab:ml-models
+ *    constants (goo 44, le 5, res 95, ssd 136, vgg 130 ms; BERT 95 ms).
+ *  scenario (C4.4): "equal"/"mix6" (50 x 6), "long-only" (0,0,100,100,100,100),
+ *    "short-skew" (100,100,100,50,50,50), "game" (app rate 100 -> 600 LeNet + 100
+ *    ResNet-50), "traffic" (100 SSD + 100 GoogLeNet + 100 VGG-16).
+ *  rate_m = floor(((double)(base_m * SLO_paper_ref_us) * x) / (double)SLO_ref_us) * num_gpus
+ *    in IEEE double, this order (C4.3: the B200 time compression; ref = the model
+ *    itself, ResNet-50 for BERT; for game / traffic one scale for the whole app, its
+ *    app-SLO model's: ResNet-50 / SSD, DESIGN R23).  In table mode the scale is 1.
+ * Out: slo_us[6], rates[6].  Errors: GL_E_ARG (NULL, unknown scenario or slo_mode,
+ *   x < 0 or not finite, num_gpus < 1). */
+gl_status gl_workload_rates(const int32_t* lat_us, int32_t slo_mode, const char* scenario, double x,
+                            int32_t num_gpus, int32_t* slo_us, int32_t* rates);
+
+/* The scheduler driven by files (SPEC S:130 profile, S:346 workload,
+ * S:272 plan dump).  profile_csv: a path.  coeffs_json: a path or inline JSON text
+ * (first non-blank character '{') holding "coeffs": [c1..c5]; NULL = no
+ * interference model (only mode gpulet+int needs it).  workload_json: a path or inline
+ * JSON object with
+ *   "num_gpus": N (default 1), "mode": "gpulet" | "gpulet+int" | "sbp" | "ideal" | "sbp50",
+ *   "slo_mode": "rule" (default) | "table", "envelope": true (default) | false (strict),
+ *   and the rates as one of
+ *     "scenario": name + optional "x" (multiplier, default 1.0)  -> gl_workload_rates;
+ *     "base_rates": [6 ints] paper-scale rates + optional "x": scaled per model as a
+ *       non-application scenario of gl_workload_rates (the paper's sweep);
+ *     "rates": [6 ints] (total req/s, canonical order);
+ *     "models": [{"name", "rate", optional "slo_ms"}]  (SPEC S:346 form; models not
+ *       listed get rate 0; slo_ms overrides the slo_mode SLO, rounded up to µs).
+ * Output (plan_buf, cap bytes, NUL-terminated, *len without the NUL): a header line
+ *   {"slo_us":[..],"rates":[..],"num_gpus":N,"mode":"..","slo_mode":".."}
+ * followed by gl_schedule's canonical plan dump with the profile's sm_count.  In
+ * scenario / base_rates form a model whose base rate is positive but whose scaled rate truncates
+ * to 0 makes the workload NotSchedulable without running the scheduler (header +
+ * {"verdict":"NotSchedulable","failed_model":name,"reason":"rate_truncated"}): the
+ * scenario's composition would be lost.  *verdict = 1 Schedulable / 0 not.
+ * Errors: those of gl_profile_load; GL_E_PARSE (malformed JSON: gl_last_error names the
+ *   offset), GL_E_ARG (bad field value), GL_E_BUDGET (buffer too small). */
+gl_status gl_schedule_files(const char* profile_csv, const char* coeffs_json, const char* workload_json,
+                            char* plan_buf, size_t cap, size_t* len, int32_t* verdict);
 /* Ordinary least squares for the interference model (§4.4): X [n][5] row-major,
  * y [n]; out c[5].  Householder QR.  Errors: GL_E_ARG, GL_E_DATA (rank < 5). */
 gl_status gl_fit_interference(const double* X, const double* y, int32_t n, double* c);
@@ -248,7 +348,9 @@ gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* 
  * <= 256); key 1: split-K factor (1 = off); key 2: executor debug flags (tuning
  * experiments, see ExecParams::dbg_flags); key 3: warm-up launches of the kernel-unit
  * tests; key 4: 1 = gather every activation operand with cp.async (no TMA), to
- * test that path.  GL_E_ARG for an unknown key. */
+ * test that path; key 5: SM count the programs are tiled for (>= 8); key 6: 1 =
+ * barrier-free GEMM step joins, 2 = also log the plan to stderr; key 7:
+ * 1 = gl_serve polls SCHED_FIFO when the process may.  GL_E_ARG for an unknown key. */
 gl_status gl_set_tuning(int32_t key, int32_t value);
 
 /* ---- F3: the `traffic` application's detection -> recognition hand-off ----

@@ -4,14 +4,17 @@ Arrivals (deterministic at exactly the plan rates, or Poisson with PCG64
 inverse-CDF exponentials) -> per-model smooth weighted round-robin over
 the model's lanes (weights = lane rates) -> per-lane FIFO with the duty-cycle
 dispatch rule (C2.11: dispatch when the desired batch is formed or a
-duty cycle D has passed since the window opened) -> hopeless requests dropped
+duty cycle D has passed since the window opened; plus the deadline guard of
+DESIGN R26: or when the batch it would send could otherwise not finish within
+its oldest request's SLO) -> hopeless requests dropped
 ((now - t_arr) + Leff(1) > SLO; drops are violations) -> the
 gpu-let runs batches FIFO with Leff(b) = ceil(L(b,p) F / 1000) -> a request is
 violated if t_end - t_arr > SLO.  Integer microseconds throughout.
 
-Pinned in tests/test_oracle_des.py (Poisson mean within 3 sigma, determinism
-for a fixed seed, soundness replay: deterministic arrivals at the plan rates
-give 0 violations for Schedulable plans).
+Pinned in tests/test_oracle_sched.py / tests/test_oracle_des.py (Poisson mean
+within 3 sigma, determinism for a fixed seed, soundness replay: deterministic
+arrivals at the plan rates give 0 violations for Schedulable plans, S:504;
+hand-traced event sequences for each dispatch condition and the drop rule).
 """
 import heapq
 import math
@@ -40,95 +43,118 @@ def arrivals_poisson(rate, duration_us, seed):
 
 
 class Lane:
-    def __init__(self, gl, m, rate, batch, F, D):
-        self.gl, self.m, self.rate, self.b, self.F, self.D = gl, m, rate, batch, F, D
-        self.q = []
-        self.window = 0
-        self.cur = 0
+    def __init__(self, gl, m, rate, batch, F, D, size):
+        self.gl, self.m, self.rate, self.b, self.F, self.D, self.size = gl, m, rate, batch, F, D, size
+        self.q = []          # request indices, oldest first
+        self.window = 0      # the duty-cycle window opened at the previous dispatch
+        self.cur = 0         # smooth weighted round-robin credit
+
+
+def simulate_trace(plan_gpulets, prof, slo, trace):
+    """The frontend + FIFO gpu-lets on a merged arrival trace, event by event.
+
+    plan_gpulets: [(size, D_us, [(m, rate, batch, F), ...]), ...] (plan order);
+    trace: [(t_us, m), ...] sorted by time.  Returns (lat, log): lat[i] =
+    completion - arrival of request i (µs, -1 dropped / no lane), log = [(lane,
+    t_dispatch, k, first request index), ...] in dispatch order.
+
+    Rules (C2.11; DESIGN R26; include/gpulet.h "Dispatch rule"):
+      * routing: each arrival goes to the lane of its model with the largest
+        credit after every lane of the model gained its rate (first maximum
+        wins); the chosen lane then loses the model's total rate;
+      * at time t a lane with queued requests dispatches if it holds >= b
+        requests, or t - window >= D, or t - arrival(oldest) + Leff(min(q, b))
+        >= SLO (the batch it would send could otherwise not finish in time);
+      * a dispatch drops every queued request with (t - arrival) + Leff(1) >
+        SLO, reopens the window at t, and sends the min(q, b) oldest
+        requests; the lane is checked again at the same t;
+      * the times considered are the arrival times and, for every lane, the
+        first time its timeout or deadline condition becomes true; at each such
+        time the arrivals up to it are routed first, then the lanes are
+        checked in order;
+      * a gpu-let runs its batches in dispatch order; a batch of k starts at
+        max(t, when the gpu-let is free) and takes Leff(k) = ceil(L(k,p) F / 1000).
+    """
+    lanes, by_model = [], {}
+    for gi, (size, D, ls) in enumerate(plan_gpulets):
+        for (m, rate, b, F) in ls:
+            ln = Lane(gi, m, rate, b, F, D, size)
+            lanes.append(ln)
+            by_model.setdefault(m, []).append(ln)
+    free = [0] * len(plan_gpulets)
+    lat = [-1] * len(trace)
+    log = []
+
+    def leff(ln, k):
+        return (prof.L(ln.m, k, ln.size) * ln.F + 999) // 1000
+
+    def ready(ln, t):
+        if not ln.q:
+            return False
+        k = min(len(ln.q), ln.b)
+        return (len(ln.q) >= ln.b or t - ln.window >= ln.D
+                or t - trace[ln.q[0]][0] + leff(ln, k) >= slo[ln.m])
+
+    def first_ready_time(ln):
+        if not ln.q:
+            return None
+        k = min(len(ln.q), ln.b)
+        return min(ln.window + ln.D, trace[ln.q[0]][0] + slo[ln.m] - leff(ln, k))
+
+    nxt = 0
+    while True:
+        times = [first_ready_time(ln) for ln in lanes]
+        times = [x for x in times if x is not None]
+        if nxt < len(trace):
+            times.append(trace[nxt][0])
+        if not times:
+            break
+        t = min(times)
+        while nxt < len(trace) and trace[nxt][0] <= t:
+            m = trace[nxt][1]
+            cand = by_model.get(m, [])
+            if cand:
+                total = sum(ln.rate for ln in cand)
+                for ln in cand:
+                    ln.cur += ln.rate
+                best = cand[0]
+                for ln in cand[1:]:
+                    if ln.cur > best.cur:
+                        best = ln
+                best.cur -= total
+                best.q.append(nxt)
+            nxt += 1
+        for li, ln in enumerate(lanes):
+            while ready(ln, t):
+                ln.q = [r for r in ln.q if (t - trace[r][0]) + leff(ln, 1) <= slo[ln.m]]
+                ln.window = t
+                if not ln.q:
+                    break
+                k = min(len(ln.q), ln.b)
+                batch, ln.q = ln.q[:k], ln.q[k:]
+                end = max(t, free[ln.gl]) + leff(ln, k)
+                free[ln.gl] = end
+                log.append((li, t, k, batch[0]))
+                for r in batch:
+                    lat[r] = end - trace[r][0]
+    return lat, log
 
 
 def simulate(plan_gpulets, prof, slo, arrivals, names=None):
-    """plan_gpulets: [(size, D_us, [(m, rate, batch, F), ...]), ...];
-    arrivals: {m: sorted list of int us}; returns per-model stats dict."""
-    lanes, free = [], []
-    by_model = {}
-    for gi, (size, D, ls) in enumerate(plan_gpulets):
-        free.append(0)
-        for (m, rate, b, F) in ls:
-            ln = Lane(gi, m, rate, b, F, D)
-            ln.size = size
-            lanes.append(ln)
-            by_model.setdefault(m, []).append(ln)
-    stats = {m: {"arrivals": 0, "late": 0, "dropped": 0, "served": 0, "lat": []} for m in arrivals}
-
-    def leff(m, b, p, F):
-        return (prof.L(m, b, p) * F + 999) // 1000
-
-    def dispatch(ln, now):
-        keep = []
-        for t in ln.q:
-            if (now - t) + leff(ln.m, 1, ln.size, ln.F) > slo[ln.m]:
-                stats[ln.m]["dropped"] += 1
-            else:
-                keep.append(t)
-        ln.q = keep
-        ln.window = now
-        if not ln.q:
-            return
-        k = min(len(ln.q), ln.b)
-        batch, ln.q = ln.q[:k], ln.q[k:]
-        start = max(now, free[ln.gl])
-        end = start + leff(ln.m, k, ln.size, ln.F)
-        free[ln.gl] = end
-        for t in batch:
-            lat = end - t
-            st = stats[ln.m]
+    """plan_gpulets as simulate_trace; arrivals: {m: sorted list of int us} (merged by
+    (time, model, index)); returns per-model stats dict."""
+    trace = sorted((t, m, j) for m, ts in arrivals.items() for j, t in enumerate(ts))
+    lat, _log = simulate_trace(plan_gpulets, prof, slo, [(t, m) for t, m, _j in trace])
+    stats = {m: {"arrivals": len(ts), "late": 0, "dropped": 0, "served": 0, "lat": []} for m, ts in arrivals.items()}
+    for (t, m, _j), x in zip(trace, lat):
+        st = stats[m]
+        if x < 0:
+            st["dropped"] += 1
+        else:
             st["served"] += 1
-            st["lat"].append(lat)
-            if lat > slo[ln.m]:
+            st["lat"].append(x)
+            if x > slo[m]:
                 st["late"] += 1
-
-    events = []
-    for m, ts in arrivals.items():
-        for j, t in enumerate(ts):
-            events.append((t, m, j))
-        stats[m]["arrivals"] = len(ts)
-    events.sort()
-    timers = []          # (deadline, lane index)
-
-    def arm(i):
-        ln = lanes[i]
-        if ln.q:
-            heapq.heappush(timers, (ln.window + ln.D, i))
-
-    def fire_until(t):
-        while timers and timers[0][0] <= t:
-            dl, i = heapq.heappop(timers)
-            ln = lanes[i]
-            if ln.q and ln.window + ln.D == dl:
-                dispatch(ln, dl)
-                arm(i)
-
-    for t, m, _j in events:
-        fire_until(t)
-        cand = by_model.get(m)
-        if not cand:
-            stats[m]["dropped"] += 1
-            continue
-        total = sum(ln.rate for ln in cand)
-        for ln in cand:
-            ln.cur += ln.rate
-        best = max(cand, key=lambda ln: ln.cur)   # first max wins ties
-        best.cur -= total
-        was_empty = not best.q
-        best.q.append(t)
-        i = lanes.index(best)
-        if len(best.q) >= best.b or t - best.window >= best.D:
-            dispatch(best, t)
-            arm(i)
-        elif was_empty:
-            arm(i)
-    fire_until(float("inf"))
     for m, st in stats.items():
         st["violations"] = st["late"] + st["dropped"]
     return stats

@@ -22,11 +22,12 @@ from dataclasses import dataclass, field
 from itertools import combinations_with_replacement, product
 
 GRID = (20, 40, 50, 60, 80, 100)
-SM_OF = {20: 32, 40: 56, 50: 72, 60: 92, 80: 116, 100: 148}
+# exact shares of 148 SMs in SM pairs (DESIGN R15); a Profile may carry measured counts
+SM_OF = {20: 30, 40: 60, 50: 74, 60: 88, 80: 118, 100: 148}
 BMAX = 32
 STAT_B = (1, 2, 4, 8, 16, 32)
 EPS_KNEE = 1e-9
-MODES = ("gpulet", "gpulet+int", "sbp")
+MODES = ("gpulet", "gpulet+int", "sbp", "sbp50")
 
 
 class Profile:
@@ -35,8 +36,9 @@ class Profile:
     lat[m][b-1][gi], l2[m][si][gi], mem[m][si][gi]; models are indices into
     `names` (canonical order le, goo, res, ssd, vgg, bert — C6 #22)."""
 
-    def __init__(self, names, lat, l2=None, mem=None):
+    def __init__(self, names, lat, l2=None, mem=None, sm=None):
         self.names = list(names)
+        self.sm = dict(zip(GRID, sm)) if sm is not None else dict(SM_OF)
         self.lat = lat
         M = len(names)
         self.l2 = l2 if l2 is not None else [[[0.0] * 6 for _ in STAT_B] for _ in range(M)]
@@ -345,7 +347,7 @@ class Scheduler:
         gl = sorted(self.remain + self.alloc, key=lambda g: (g.gpu, g.slot))
         lines = []
         for g in gl:
-            d = {"gpu": g.gpu, "slot": g.slot, "size": g.size, "sm": SM_OF[g.size], "D_us": 0, "lanes": []}
+            d = {"gpu": g.gpu, "slot": g.slot, "size": g.size, "sm": self.P.sm[g.size], "D_us": 0, "lanes": []}
             if g.lanes:
                 ev = self.eval_lanes(g, self.aggregate(self.sibling(g)))
                 assert ev is not None, "committed lane set became infeasible"
@@ -408,30 +410,35 @@ def curvatures(rates):
 
 
 # ---- C2.9 SBP baseline (whole-GPU temporal sharing) --------------------------------
-def sbp(prof, slo, rates, num_gpus):
-    """Squishy bin packing (Nexus) on 100 % gpu-lets, reading C2.9."""
+def sbp(prof, slo, rates, num_gpus, size=100):
+    """Squishy bin packing (Nexus), reading C2.9, with every bin a gpu-let
+    of `size` %: whole GPUs (100, the temporal-sharing baseline) or both halves of
+    evenly split GPUs (50: "SBP algorithm that independently schedules two evenly
+    split gpu-lets", Fig. success-case) -> num_gpus * 100 // size bins."""
     S = Scheduler(prof, slo, None, "sbp")
+    per = 100 // size
+    bins = num_gpus * per
     order = sorted([m for m in range(len(rates)) if rates[m] > 0], key=lambda m: (-rates[m], m))
     gpus = []          # list of lane lists
     residual = []
     failed = None
     for m in order:
-        b = S.b_sat(m, 100)
+        b = S.b_sat(m, size)
         if b is None:
             failed = m
             break
-        L = prof.L(m, b, 100)
+        L = prof.L(m, b, size)
         cap = b * 1_000_000 // L
         k, r = divmod(rates[m], cap)
         for _ in range(k):
             gpus.append([Lane(m, cap)])
-        if len(gpus) > num_gpus:
+        if len(gpus) > bins:
             failed = m
             break
         if r > 0:
             D = L
             bp = (r * D + 999_999) // 1_000_000
-            residual.append((m, r, prof.L(m, bp, 100), D))
+            residual.append((m, r, prof.L(m, bp, size), D))
     if failed is None:
         # occupancy e/D descending; exact cross-multiplication; stable in model order
         import functools
@@ -444,7 +451,7 @@ def sbp(prof, slo, rates, num_gpus):
         for m, r, _e, _D in residual:
             best, best_occ = None, None
             for gi, lanes in enumerate(rgpus):
-                ev = S.eval_lanes(Gpulet(0, 0, 100), None, lanes=lanes + [Lane(m, r)])
+                ev = S.eval_lanes(Gpulet(0, 0, size), None, lanes=lanes + [Lane(m, r)])
                 if ev is None:
                     continue
                 D, recs = ev
@@ -455,13 +462,13 @@ def sbp(prof, slo, rates, num_gpus):
                 rgpus.append([Lane(m, r)])
             else:
                 rgpus[best].append(Lane(m, r))
-            if len(gpus) + len(rgpus) > num_gpus:
+            if len(gpus) + len(rgpus) > bins:
                 failed = m
                 break
         gpus += rgpus
     S.remain, S.alloc = [], []
-    for i in range(num_gpus):
-        g = Gpulet(i, 0, 100, list(gpus[i]) if i < len(gpus) else [])
+    for i in range(bins):
+        g = Gpulet(i // per, i % per, size, list(gpus[i]) if i < len(gpus) else [])
         (S.alloc if g.lanes else S.remain).append(g)
     return S.result(failed is None, failed)
 
@@ -470,6 +477,8 @@ def schedule(prof, slo, rates, num_gpus, mode, coeffs=None):
     """Top-level: mode in {gpulet, gpulet+int, sbp}."""
     if mode == "sbp":
         return sbp(prof, slo, rates, num_gpus)
+    if mode == "sbp50":
+        return sbp(prof, slo, rates, num_gpus, size=50)
     return Scheduler(prof, slo, coeffs, mode).run(rates, num_gpus)
 
 

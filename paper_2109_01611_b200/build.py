@@ -27,6 +27,7 @@ SOURCES = [
     ("models.cpp", []),
     ("frontend.cpp", []),
     ("sched.cpp", ["-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fno-fast-math"]),
+    ("workload.cpp", ["-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fno-fast-math"]),
 ]
 HEADERS = ["program.h", "ptx.cuh", "runtime.h"]
 

@@ -2,10 +2,15 @@
 // real time against live gpu-lets.  Each model's requests are routed over its
 // lanes by smooth weighted round-robin (weights = the lanes' assigned rates);
 // each lane keeps a FIFO and dispatches "when the desired size of request batch
-// is formed or a duty-cycle is passed" -- or when its
-// oldest request's remaining slack has shrunk to Leff(1) + a guard (DESIGN R26)
-// -- after dropping requests that can no longer meet their SLO (drops
-// count as violations).  A request's latency is host completion time - arrival time.
+// is formed or a duty-cycle is passed" -- or when the batch
+// it would send could otherwise no longer finish within its oldest request's SLO
+// (deadline guard, DESIGN R26) -- after dropping requests that can no longer meet
+// their SLO (drops count as violations).  A request's latency is
+// host completion time - arrival time.
+//
+// The routing and dispatch rule (struct Policy) is shared with gl_serve_sim, a
+// virtual-clock replay against FIFO gpu-lets whose batch sequence the tests
+// compare with the discrete-event simulator oracle (oracle/des.py).
 //
 // End-to-end mode (lanes with in_host): a model's i-th request lives in host
 // slot i % host_slots of the lane's pinned ring.  A dispatched batch goes
@@ -35,6 +40,7 @@
 #include <vector>
 
 #include "../../include/gpulet.h"
+#include "runtime.h"
 
 namespace {
 enum Stage { FREE = 0, H2D, RUN, D2H };
@@ -44,9 +50,6 @@ enum Stage { FREE = 0, H2D, RUN, D2H };
 // SLO); larger ones go through the async copy path.
 constexpr int64_t kZeroCopyMax = 64 * 1024;
 constexpr int kZeroCopyBuf = -2;   // Inflight::buf of a zero-copy batch
-// Deadline guard of the dispatch rule: max(5 us, SLO / 20).
-constexpr int64_t kGuardMinUs = 0;
-constexpr int32_t kGuardDiv = 1000;
 
 struct Batch {
   Stage stage = FREE;
@@ -62,11 +65,76 @@ struct Inflight {
   std::vector<int64_t> reqs;   // plain mode: the batch's request indices
 };
 
-struct LaneState {
+// ---- routing + dispatch rule (C2.11 + R26; include/gpulet.h "Dispatch rule") ------------
+struct PLane {
   gl_lane cfg;
   std::deque<int64_t> q;  // request indices
-  int64_t window_us = 0;
+  int64_t window_us = 0;  // the duty-cycle window opened at the previous dispatch
   int64_t cur = 0;        // smooth WRR credit
+  int32_t leff(int k) const { return cfg.leff_us ? cfg.leff_us[k - 1] : cfg.drop_us; }
+  int next_k() const { return std::min<int>((int)q.size(), cfg.batch); }
+};
+
+template <class LaneT>
+struct Policy {
+  std::vector<LaneT>& L;
+  std::vector<std::vector<int>> by_model;
+  const int64_t* arr;
+  const int32_t* arr_model;
+  const int32_t* slo;
+  Policy(std::vector<LaneT>& L, int n_models, const int64_t* arr, const int32_t* arr_model, const int32_t* slo)
+      : L(L), by_model(n_models), arr(arr), arr_model(arr_model), slo(slo) {
+    for (int i = 0; i < (int)L.size(); ++i) by_model[L[i].cfg.model_slot].push_back(i);
+  }
+  // smooth weighted round-robin over the request's model lanes; -1: no lane serves the model
+  int route(int64_t r) {
+    auto& cand = by_model[arr_model[r]];
+    if (cand.empty()) return -1;
+    int64_t total = 0;
+    int best = -1;
+    for (int li : cand) {
+      L[li].cur += L[li].cfg.weight;
+      total += L[li].cfg.weight;
+      if (best < 0 || L[li].cur > L[best].cur) best = li;
+    }
+    L[best].cur -= total;
+    L[best].q.push_back(r);
+    return best;
+  }
+  int32_t slo_of(const LaneT& ln) const { return slo[ln.cfg.model_slot]; }
+  bool ready(int li, int64_t now) const {
+    const LaneT& ln = L[li];
+    if (ln.q.empty()) return false;
+    if ((int)ln.q.size() >= ln.cfg.batch) return true;                    // batch formed
+    if (now - ln.window_us >= ln.cfg.duty_us) return true;                // duty cycle passed
+    return now - arr[ln.q.front()] + ln.leff(ln.next_k()) >= slo_of(ln);  // deadline guard (R26)
+  }
+  // earliest time > now at which ready() turns true with no new arrival (INT64_MAX: never)
+  int64_t deadline(int li) const {
+    const LaneT& ln = L[li];
+    if (ln.q.empty()) return INT64_MAX;
+    return std::min<int64_t>(ln.window_us + ln.cfg.duty_us, arr[ln.q.front()] + slo_of(ln) - ln.leff(ln.next_k()));
+  }
+  // the dispatch itself: drop hopeless requests (-> dropped), reopen the window;
+  // returns the batch size k (the caller takes the k oldest from q; 0 = emptied)
+  template <class F>
+  int open(int li, int64_t now, F&& drop) {
+    LaneT& ln = L[li];
+    while (!ln.q.empty()) {
+      const int64_t r = ln.q.front();
+      if ((now - arr[r]) + ln.leff(1) > slo[arr_model[r]]) {
+        drop(r);
+        ln.q.pop_front();
+      } else {
+        break;
+      }
+    }
+    ln.window_us = now;
+    return ln.next_k();
+  }
+};
+
+struct LaneState : PLane {
   int nbuf = 1;           // device buffers (batches in flight)
   bool zero_copy = false; // requests small enough for the executor to read / write the host ring directly
   Batch buf[2];
@@ -106,17 +174,16 @@ bool copy_slots(void* dev, const void* host, const std::vector<int64_t>& slots, 
   return true;
 }
 
-// Optional (GL_SERVE_RT=1): run the busy-polling frontend loop SCHED_FIFO for
-// the duration of the call when the process may (root / CAP_SYS_NICE).  Off by
-// default: measured no better than the default policy on the B200 boxes
+// Optional (gl_set_tuning(7, 1)): run the busy-polling frontend loop SCHED_FIFO
+// for the duration of the call when the process may (root / CAP_SYS_NICE).  Off
+// by default: measured no better than the default policy on the B200 boxes
 // (profiles/ab_r1r_*.log).
 struct RtGuard {
   int policy = 0;
   sched_param old{};
   bool set = false;
   RtGuard() {
-    const char* e = std::getenv("GL_SERVE_RT");
-    if (!e || e[0] != '1') return;
+    if (gl::g_tune[gl::TUNE_SERVE_RT] != 1) return;
     if (pthread_getschedparam(pthread_self(), &policy, &old) != 0) return;
     sched_param p{};
     p.sched_priority = 10;
@@ -144,20 +211,15 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
                               const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
                               int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes,
                               gl_lane_stats* lane_stats) {
-  // deadline-guard tuning overrides (GL_GUARD_MIN_US, GL_GUARD_DIV; tuning runs only)
-  const char* guard_env_min = std::getenv("GL_GUARD_MIN_US");
-  const char* guard_env_div = std::getenv("GL_GUARD_DIV");
-  const int64_t guard_min_us = guard_env_min ? std::max<int64_t>(0, std::atoll(guard_env_min)) : kGuardMinUs;
-  const int32_t guard_div = guard_env_div ? std::max<int32_t>(1, std::atoi(guard_env_div)) : kGuardDiv;
   if (!ctx || !lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || !slo_us || !lat_us)
     return GL_E_ARG;
   std::vector<LaneState> L(n_lanes);
   Cleanup cleanup{L};
   RtGuard rt;
-  std::vector<std::vector<int>> by_model(n_models);
   for (int i = 0; i < n_lanes; ++i) {
     L[i].cfg = lanes[i];
-    if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models) return GL_E_ARG;
+    if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models || lanes[i].batch < 1 || lanes[i].batch > 32)
+      return GL_E_ARG;
     if (lanes[i].in_host) {
       if (!lanes[i].out_host || lanes[i].in_req_bytes <= 0 || lanes[i].out_req_bytes <= 0 || lanes[i].host_slots < 1)
         return GL_E_ARG;
@@ -167,8 +229,8 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       for (int b = 0; b < L[i].nbuf; ++b)
         if (cudaEventCreateWithFlags(&L[i].buf[b].ev, cudaEventDisableTiming) != cudaSuccess) return GL_E_CUDA;
     }
-    by_model[lanes[i].model_slot].push_back(i);
   }
+  Policy<LaneState> pol(L, n_models, arr_us, arr_model, slo_us);
   for (int64_t r = 0; r < n_req; ++r) lat_us[r] = -2;
   if (lane_stats)
     for (int i = 0; i < n_lanes; ++i) lane_stats[i] = gl_lane_stats{0, 0, 0, 0};
@@ -201,22 +263,11 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
     while (next < n_req && arr_us[next] <= now) {
       const int m = arr_model[next];
       seq_of[next] = model_seq[m]++;
-      auto& cand = by_model[m];
-      if (cand.empty()) {
+      if (pol.route(next) < 0) {
         lat_us[next] = -1;
-        ++next;
-        continue;
+      } else {
+        ++outstanding;
       }
-      int64_t total = 0;
-      int best = -1;
-      for (int li : cand) {
-        L[li].cur += L[li].cfg.weight;
-        total += L[li].cfg.weight;
-        if (best < 0 || L[li].cur > L[best].cur) best = li;
-      }
-      L[best].cur -= total;
-      L[best].q.push_back(next);
-      ++outstanding;
       ++next;
     }
     // 2. duty-cycle dispatch
@@ -225,28 +276,13 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       if (ln.q.empty()) continue;
       const int b = ln.cfg.in_host ? ln.free_buf() : 0;
       if (b < 0 && !ln.zero_copy) continue;   // zero-copy batches need no device buffer
-      const bool full = (int)ln.q.size() >= ln.cfg.batch;
-      const bool timeout = now - ln.window_us >= ln.cfg.duty_us;
-      // deadline guard (DESIGN R26): dispatch early when the oldest queued
-      // request would otherwise keep waiting into its last Leff(1) + guard of slack
-      const int32_t slo_m = slo_us[ln.cfg.model_slot];
-      const int64_t guard = std::max<int64_t>(guard_min_us, slo_m / guard_div);
-      const bool urgent = now - arr_us[ln.q.front()] + ln.cfg.drop_us + guard >= slo_m;
-      if (!full && !timeout && !urgent) continue;
-      while (!ln.q.empty()) {  // drop hopeless requests
-        const int64_t r = ln.q.front();
-        if ((now - arr_us[r]) + ln.cfg.drop_us > slo_us[arr_model[r]]) {
-          lat_us[r] = -1;
-          ln.q.pop_front();
-          --outstanding;
-        } else {
-          break;
-        }
-      }
+      if (!pol.ready(li, now)) continue;
       const int64_t window0 = ln.window_us;
-      ln.window_us = now;
-      if (ln.q.empty()) continue;
-      const int k = std::min<int>((int)ln.q.size(), ln.cfg.batch);
+      const int k = pol.open(li, now, [&](int64_t r) {
+        lat_us[r] = -1;
+        --outstanding;
+      });
+      if (k == 0) continue;
       if (ln.cfg.in_host) {
         std::vector<int64_t> slots(k);
         for (int i = 0; i < k; ++i) slots[i] = seq_of[ln.q[i]] % ln.cfg.host_slots;
@@ -356,5 +392,57 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
   }
   if (h2d_bytes) *h2d_bytes = h2d;
   if (d2h_bytes) *d2h_bytes = d2h;
+  return GL_OK;
+}
+
+extern "C" gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                                  const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
+                                  int64_t* batch_log, int64_t cap, int64_t* n_log) {
+  if (!lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || (!arr_model && n_req) || !slo_us ||
+      (!lat_us && n_req) || n_req < 0 || (!batch_log && cap > 0))
+    return gl::set_error(GL_E_ARG, "gl_serve_sim: bad arguments");
+  std::vector<PLane> L(n_lanes);
+  std::unordered_map<int32_t, int64_t> free_at;   // gpu-let id -> time its FIFO drains
+  for (int i = 0; i < n_lanes; ++i) {
+    L[i].cfg = lanes[i];
+    if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models || !lanes[i].leff_us || lanes[i].batch < 1 ||
+        lanes[i].batch > 32 || lanes[i].duty_us < 0)
+      return gl::set_error(GL_E_ARG, "gl_serve_sim: bad lane");
+    free_at[lanes[i].gpulet] = 0;
+  }
+  for (int64_t r = 1; r < n_req; ++r)
+    if (arr_us[r] < arr_us[r - 1]) return gl::set_error(GL_E_ARG, "gl_serve_sim: arrivals must be sorted");
+  Policy<PLane> pol(L, n_models, arr_us, arr_model, slo_us);
+  int64_t logged = 0, next = 0;
+  for (int64_t r = 0; r < n_req; ++r) lat_us[r] = -1;
+  for (;;) {
+    int64_t t = next < n_req ? arr_us[next] : INT64_MAX;
+    for (int li = 0; li < n_lanes; ++li) t = std::min(t, pol.deadline(li));
+    if (t == INT64_MAX) break;
+    while (next < n_req && arr_us[next] <= t) pol.route(next++);   // no lane: stays -1 (dropped)
+    for (int li = 0; li < n_lanes; ++li) {
+      PLane& ln = L[li];
+      while (pol.ready(li, t)) {
+        const int k = pol.open(li, t, [&](int64_t r) { lat_us[r] = -1; });
+        if (k == 0) break;
+        int64_t& fr = free_at[ln.cfg.gpulet];
+        const int64_t end = std::max(t, fr) + ln.leff(k);
+        fr = end;
+        if (logged < cap) {
+          int64_t* row = batch_log + 4 * logged;
+          row[0] = li;
+          row[1] = t;
+          row[2] = k;
+          row[3] = ln.q.front();
+        }
+        ++logged;
+        for (int i = 0; i < k; ++i) {
+          lat_us[ln.q.front()] = end - arr_us[ln.q.front()];
+          ln.q.pop_front();
+        }
+      }
+    }
+  }
+  if (n_log) *n_log = logged;
   return GL_OK;
 }

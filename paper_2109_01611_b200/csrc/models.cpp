@@ -1081,18 +1081,12 @@ static void build_bert(Builder& B, size_t& in_b, size_t& out_b) {
 // reads -- its A operand and its residual -- was either complete before the
 // last full barrier or written by a single full-width GEMM op that publishes
 // per-M-block completion counters; the reader then waits for exactly the M
-// blocks it needs.  Off by default (GL_DATAFLOW=1 enables): correct (the GPU
+// blocks it needs.  Off by default (gl_set_tuning(6, 1) enables): correct (the GPU
 // parity suite passes with it) but measured no faster -- ResNet-50 / BERT equal
 // with workspace reuse, 3-4 % slower without it (the reuse it needs to be safe),
 // VGG-16 12 % slower (profiles/ab_r1x_dataflow.log): the per-step cost is the
 // dependency chain of the slowest tiles, not the barrier itself.
-bool dataflow_enabled() {
-  static const int on = [] {
-    const char* e = std::getenv("GL_DATAFLOW");
-    return (e && e[0] == '1') ? 1 : 0;
-  }();
-  return on != 0;
-}
+bool dataflow_enabled() { return g_tune[TUNE_DATAFLOW] != 0; }
 
 static bool publishes(const OpDesc& op) {
   const GemmArgs& g = op.g;
@@ -1192,7 +1186,7 @@ void plan_dataflow(Program& p) {
   for (int k = 0; k < n; ++k)
     if (pub[k]) ops[k].g.pub_off = pub[k];
   ops[0].cnt_words = next_word > 1 ? next_word : 0;
-  if (std::getenv("GL_DATAFLOW_LOG")) {
+  if (g_tune[TUNE_DATAFLOW] >= 2) {
     int joins = 0;
     for (const OpDesc& o : ops) joins += o.local_next;
     std::fprintf(stderr, "[dataflow] ops %d steps %d barrier-free joins %d counter words %d ws %.1f MB\n", n, nsteps,

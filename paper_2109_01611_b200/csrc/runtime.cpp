@@ -306,7 +306,7 @@ static int grid_index(int pct) {
   }
 }
 
-// One SM split per GPU (8-SM groups + remainder), then one green context and
+// One SM split per GPU (SM pairs; 8-SM groups + remainder as a fallback), then one green context and
 // stream per (slot, size): slot 0 uses groups from the front, slot 1 from the back.
 static gl_status prepare_green(gl_ctx* ctx, GpuState& G) {
   Driver& D = driver();

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/gpulet.h"
 #include "program.h"
 
 namespace gl {
@@ -76,8 +77,15 @@ struct Model {
 };
 
 // Program-builder tuning overrides (gl_set_tuning; 0 = automatic choice).
-enum TuneKey { TUNE_BN = 0, TUNE_SPLIT = 1, TUNE_MISC = 2, TUNE_WARM = 3, TUNE_GATHER = 4, TUNE_SMS = 5, kTuneKeys = 8 };
+enum TuneKey {
+  TUNE_BN = 0, TUNE_SPLIT = 1, TUNE_MISC = 2, TUNE_WARM = 3, TUNE_GATHER = 4, TUNE_SMS = 5,
+  TUNE_DATAFLOW = 6,   // 1: barrier-free GEMM step joins in programs built afterwards; 2: also log the plan
+  TUNE_SERVE_RT = 7,   // 1: gl_serve runs its polling loop SCHED_FIFO when permitted
+  kTuneKeys = 8
+};
 extern int g_tune[kTuneKeys];
+// thread-local gl_last_error text (runtime.cpp); returns s
+gl_status set_error(gl_status s, const char* m);
 
 // Build the layer program of model `kind` at batch b (models.cpp).
 // sm_target: the SM count of the gpu-let the program is built for (tile

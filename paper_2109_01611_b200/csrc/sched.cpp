@@ -19,7 +19,9 @@
 namespace {
 
 constexpr int kGrid[6] = {20, 40, 50, 60, 80, 100};
-constexpr int kSm[6] = {32, 56, 72, 92, 116, 148};
+// SMs per grid size when the caller gives none: the exact shares of 148 SMs in
+// SM pairs (runtime.cpp sm_for_pct); the plan dump prints in.sm_count otherwise.
+constexpr int kSm[6] = {30, 60, 74, 88, 118, 148};
 constexpr int kStatB[6] = {1, 2, 4, 8, 16, 32};
 constexpr int kBmax = 32;
 constexpr double kEps = 1e-9;
@@ -407,7 +409,7 @@ class Sched {
       std::vector<Rec> recs;
       if (!pool[g].lanes.empty()) eval(pool[g].lanes, pool[g].size, aggregate(sibling(g)), D, recs);
       snprintf(buf, sizeof buf, "{\"gpu\":%d,\"slot\":%d,\"size\":%d,\"sm\":%d,\"D_us\":%lld,\"lanes\":[", pool[g].gpu,
-               pool[g].slot, pool[g].size, kSm[gidx(pool[g].size)], (long long)D);
+               pool[g].slot, pool[g].size, (in.sm_count ? in.sm_count[gidx(pool[g].size)] : kSm[gidx(pool[g].size)]), (long long)D);
       out += buf;
       for (size_t i = 0; i < recs.size(); ++i) {
         snprintf(buf, sizeof buf, "%s{\"model\":\"%s\",\"rate\":%lld,\"batch\":%d,\"exec_us\":%lld,\"F\":%d}",
@@ -430,9 +432,13 @@ class Sched {
   }
 };
 
-// SBP (Nexus squishy bin packing) on whole GPUs, reading C2.9.
-bool sbp(const gl_sched_input& in, std::string& out) {
+// SBP (Nexus squishy bin packing), reading C2.9, on bins of `size` %: whole GPUs
+// (size 100, the temporal-sharing baseline) or the two halves of evenly split GPUs
+// (size 50: "SBP algorithm that independently schedules two evenly split gpu-lets",
+// Fig. success-case); num_gpus * 100 / size bins.
+bool sbp(const gl_sched_input& in, std::string& out, int size = 100) {
   Sched S(in, 2);
+  const int per = 100 / size, bins = in.num_gpus * per;
   std::vector<std::vector<Lane>> gpus;
   struct Resid {
     int m;
@@ -441,22 +447,22 @@ bool sbp(const gl_sched_input& in, std::string& out) {
   std::vector<Resid> resid;
   int failed = -1;
   for (int m : S.order()) {
-    const int b = S.bsat(m, 100);
+    const int b = S.bsat(m, size);
     if (!b) {
       failed = m;
       break;
     }
-    const int64_t L = S.L(m, b, 100);
+    const int64_t L = S.L(m, b, size);
     const int64_t cap = (int64_t)b * 1000000 / L;
     const int64_t k = in.rates[m] / cap, r = in.rates[m] % cap;
     for (int64_t i = 0; i < k; ++i) gpus.push_back({Lane{m, cap}});
-    if ((int)gpus.size() > in.num_gpus) {
+    if ((int)gpus.size() > bins) {
       failed = m;
       break;
     }
     if (r > 0) {
       const int64_t bp = (r * L + 999999) / 1000000;
-      resid.push_back(Resid{m, r, S.L(m, (int)bp, 100), L});
+      resid.push_back(Resid{m, r, S.L(m, (int)bp, size), L});
     }
   }
   if (failed < 0) {
@@ -470,7 +476,7 @@ bool sbp(const gl_sched_input& in, std::string& out) {
         ls.push_back(Lane{x.m, x.r});
         int64_t D;
         std::vector<Rec> recs;
-        if (!S.eval(ls, 100, Agg{false, 0, 0}, D, recs)) continue;
+        if (!S.eval(ls, size, Agg{false, 0, 0}, D, recs)) continue;
         int64_t s = 0;
         for (const Rec& rc : recs) s += rc.e;
         if (best < 0 || s * bD > bs * D) best = i, bs = s, bD = D;
@@ -479,15 +485,15 @@ bool sbp(const gl_sched_input& in, std::string& out) {
         rg.push_back({Lane{x.m, x.r}});
       else
         rg[best].push_back(Lane{x.m, x.r});
-      if ((int)(gpus.size() + rg.size()) > in.num_gpus) {
+      if ((int)(gpus.size() + rg.size()) > bins) {
         failed = x.m;
         break;
       }
     }
     gpus.insert(gpus.end(), rg.begin(), rg.end());
   }
-  for (int i = 0; i < in.num_gpus; ++i) {
-    const int id = S.add(i, 0, 100, 0);
+  for (int i = 0; i < bins; ++i) {
+    const int id = S.add(i / per, i % per, size, 0);
     if (i < (int)gpus.size()) {
       S.pool[id].lanes = gpus[i];
       S.pool[id].state = 1;
@@ -501,7 +507,7 @@ bool sbp(const gl_sched_input& in, std::string& out) {
 
 extern "C" gl_status gl_schedule(const gl_sched_input* in, char* plan_buf, size_t cap, size_t* len, int32_t* verdict) {
   if (!in || !plan_buf || !len || !verdict || in->n_models < 1 || in->n_models > 8 || !in->lat_us || !in->slo_us ||
-      !in->rates || !in->names || in->num_gpus < 1 || in->mode < 0 || in->mode > 3)
+      !in->rates || !in->names || in->num_gpus < 1 || in->mode < 0 || in->mode > 4)
     return GL_E_ARG;
   if ((in->mode == 1) && (!in->l2 || !in->mem)) return GL_E_ARG;
   static const double zeros[8 * 36] = {0};
@@ -510,8 +516,8 @@ extern "C" gl_status gl_schedule(const gl_sched_input* in, char* plan_buf, size_
   if (!local.mem) local.mem = zeros;
   std::string out;
   bool ok;
-  if (in->mode == 2) {
-    ok = sbp(local, out);
+  if (in->mode == 2 || in->mode == 4) {
+    ok = sbp(local, out, in->mode == 2 ? 100 : 50);
   } else if (in->mode == 3) {
     // ideal: every multiset of per-GPU layouts {100}, {20,80}, {40,60}, {50,50}
     static const std::vector<int> L4[4] = {{100}, {20, 80}, {40, 60}, {50, 50}};

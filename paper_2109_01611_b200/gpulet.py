@@ -16,12 +16,13 @@ ERRORS = {-1: "GL_E_ARG", -2: "GL_E_GRID", -3: "GL_E_CAPACITY", -4: "GL_E_PARTIT
           -6: "GL_E_MODEL", -7: "GL_E_QUEUE_FULL", -8: "GL_E_NOT_CONCURRENT", -9: "GL_E_PARSE",
           -10: "GL_E_DATA", -11: "GL_E_BUDGET", -12: "GL_E_CUDA", -13: "GL_E_TIMEOUT"}
 MODELS = ["lenet5", "googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"]
-MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3}
+MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3, "sbp50": 4}
 
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
-           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_schedule", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
+           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_schedule", "gl_profile_load",
+           "gl_workload_rates", "gl_schedule_files", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
            "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
 
 
@@ -42,7 +43,7 @@ class SchedInput(ctypes.Structure):
                 ("lat_us", ctypes.POINTER(ctypes.c_int32)), ("l2", ctypes.POINTER(ctypes.c_double)),
                 ("mem", ctypes.POINTER(ctypes.c_double)), ("slo_us", ctypes.POINTER(ctypes.c_int32)),
                 ("rates", ctypes.POINTER(ctypes.c_int32)), ("coeffs", ctypes.c_double * 5),
-                ("num_gpus", ctypes.c_int32), ("mode", ctypes.c_int32)]
+                ("num_gpus", ctypes.c_int32), ("mode", ctypes.c_int32), ("sm_count", ctypes.POINTER(ctypes.c_int32))]
 
 
 class Lane(ctypes.Structure):
@@ -51,7 +52,8 @@ class Lane(ctypes.Structure):
                 ("drop_us", ctypes.c_int32), ("pad_", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
                 ("out_dev", ctypes.c_void_p), ("in_host", ctypes.c_void_p), ("out_host", ctypes.c_void_p),
                 ("in_req_bytes", ctypes.c_int64), ("out_req_bytes", ctypes.c_int64), ("host_slots", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32), ("in_dev2", ctypes.c_void_p), ("out_dev2", ctypes.c_void_p)]
+                ("pad2_", ctypes.c_int32), ("in_dev2", ctypes.c_void_p), ("out_dev2", ctypes.c_void_p),
+                ("leff_us", ctypes.POINTER(ctypes.c_int32))]
 
 
 _lib = None
@@ -86,8 +88,16 @@ def lib():
             "gl_serve": [P, ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
                          ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(U64), ctypes.POINTER(I64),
                          ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int64)],
+            "gl_serve_sim": [ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
+                             ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64), I64, ctypes.POINTER(I64)],
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
+            "gl_profile_load": [ctypes.c_char_p, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(D),
+                                ctypes.POINTER(I32)],
+            "gl_workload_rates": [ctypes.POINTER(I32), I32, ctypes.c_char_p, D, I32, ctypes.POINTER(I32),
+                                  ctypes.POINTER(I32)],
+            "gl_schedule_files": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t,
+                                  ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
             "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32],
             "gl_test_conv": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32, I32, I32],
@@ -124,6 +134,41 @@ def _ptr(x):
     if hasattr(x, "ctypes"):
         return x.ctypes.data
     raise TypeError(type(x))
+
+
+def _lanes(lanes):
+    """gl_lane array from lane dicts (routing / dispatch fields; leff_us: 32 ints or absent)."""
+    import numpy as np
+    L = (Lane * len(lanes))()
+    keep = []
+    for i, d in enumerate(lanes):
+        L[i].gpulet, L[i].model_id, L[i].model_slot = d["gpulet"], d.get("model_id", 0), d["model_slot"]
+        L[i].batch, L[i].duty_us, L[i].weight, L[i].drop_us = d["batch"], d["duty_us"], d["weight"], d["drop_us"]
+        if d.get("leff_us") is not None:
+            a = np.ascontiguousarray(d["leff_us"], dtype=np.int32)
+            assert a.size == 32
+            keep.append(a)
+            L[i].leff_us = a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    return L, keep
+
+
+def serve_sim(lanes, n_models, arr_us, arr_model, slo_us, cap=1 << 20):
+    """gl_serve_sim (virtual clock, no GPU) -> (lat_us int64 ndarray, batch log [(lane, t, k, first)])."""
+    import numpy as np
+    L, keep = _lanes(lanes)
+    a = np.ascontiguousarray(arr_us, dtype=np.int64)
+    m = np.ascontiguousarray(arr_model, dtype=np.int32)
+    s = np.ascontiguousarray(slo_us, dtype=np.int32)
+    lat = np.zeros(len(a), np.int64)
+    log = np.zeros((cap, 4), np.int64)
+    n = ctypes.c_int64()
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    _check(lib().gl_serve_sim(L, len(lanes), n_models, a.ctypes.data_as(P64),
+                              m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
+                              s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), lat.ctypes.data_as(P64),
+                              log.ctypes.data_as(P64), cap, ctypes.byref(n)))
+    assert n.value <= cap
+    return lat, [tuple(int(v) for v in row) for row in log[:n.value]]
 
 
 class Context:
@@ -240,10 +285,8 @@ class Context:
         returns per-request latency (us, -1 dropped), and with stats also
         {"dev_ns": (first dequeue, last end), "h2d_bytes", "d2h_bytes"}."""
         import numpy as np
-        L = (Lane * len(lanes))()
+        L, keep = _lanes(lanes)
         for i, d in enumerate(lanes):
-            L[i].gpulet, L[i].model_id, L[i].model_slot = d["gpulet"], d["model_id"], d["model_slot"]
-            L[i].batch, L[i].duty_us, L[i].weight, L[i].drop_us = d["batch"], d["duty_us"], d["weight"], d["drop_us"]
             L[i].in_dev, L[i].out_dev = _ptr(d["x"]), _ptr(d["y"])
             if d.get("x_host") is not None:
                 L[i].in_host, L[i].out_host = _ptr(d["x_host"]), _ptr(d["y_host"])
@@ -328,9 +371,10 @@ def crop_resize(img, n_img, H, W, det, count, max_det, per_img, out, OH=224, OW=
                                 int(per_img), int(OH), int(OW), _ptr(out), stream or None))
 
 
-def schedule(names, lat_us, l2, mem, slo_us, rates, num_gpus, mode, coeffs=(0, 0, 0, 0, 0), cap=1 << 20):
+def schedule(names, lat_us, l2, mem, slo_us, rates, num_gpus, mode, coeffs=(0, 0, 0, 0, 0), cap=1 << 20,
+             sm_count=None):
     """gl_schedule: returns (plan_dump_text, schedulable).  lat_us [M][32][6] ints,
-    l2/mem [M][6][6] floats (or None), slo_us/rates [M] ints."""
+    l2/mem [M][6][6] floats (or None), slo_us/rates [M] ints, sm_count [6] or None."""
     import numpy as np
     M = len(names)
     nm = (ctypes.c_char_p * M)(*[n.encode() for n in names])
@@ -351,10 +395,59 @@ def schedule(names, lat_us, l2, mem, slo_us, rates, num_gpus, mode, coeffs=(0, 0
         si.coeffs[i] = float(coeffs[i]) if coeffs is not None else 0.0
     si.num_gpus = num_gpus
     si.mode = MODES[mode] if isinstance(mode, str) else mode
+    if sm_count is not None:
+        sma = np.ascontiguousarray(sm_count, dtype=np.int32)
+        si.sm_count = sma.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     buf = ctypes.create_string_buffer(cap)
     ln, verdict = ctypes.c_size_t(), ctypes.c_int32()
     _check(lib().gl_schedule(ctypes.byref(si), buf, cap, ctypes.byref(ln), ctypes.byref(verdict)))
     return buf.value.decode(), bool(verdict.value)
+
+
+def profile_load(path, strict=False):
+    """gl_profile_load -> (lat_us [6][32][6] int32 ndarray, l2 [6][6][6], mem [6][6][6], sm_count [6])."""
+    import numpy as np
+    lat = np.zeros((6, 32, 6), np.int32)
+    l2 = np.zeros((6, 6, 6), np.float64)
+    mem = np.zeros((6, 6, 6), np.float64)
+    sm = np.zeros(6, np.int32)
+    _check(lib().gl_profile_load(os.fsencode(path), 1 if strict else 0,
+                                 lat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                 l2.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 mem.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 sm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return lat, l2, mem, sm
+
+
+def workload_rates(lat_us, scenario, x=1.0, num_gpus=1, slo_mode="rule"):
+    """gl_workload_rates -> (slo_us [6], rates [6]) as Python int lists."""
+    import numpy as np
+    lat = np.ascontiguousarray(lat_us, dtype=np.int32)
+    slo = np.zeros(6, np.int32)
+    rates = np.zeros(6, np.int32)
+    _check(lib().gl_workload_rates(lat.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                   {"rule": 0, "table": 1}[slo_mode], scenario.encode(), float(x), num_gpus,
+                                   slo.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                   rates.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return [int(v) for v in slo], [int(v) for v in rates]
+
+
+def schedule_files(profile_csv, coeffs_json, workload_json, cap=1 << 20):
+    """gl_schedule_files: paths (or inline JSON text for coeffs / workload; dicts are
+    serialised) -> (header dict, plan dump text without the header, schedulable)."""
+    import json
+    if isinstance(workload_json, dict):
+        workload_json = json.dumps(workload_json)
+    if isinstance(coeffs_json, dict):
+        coeffs_json = json.dumps(coeffs_json)
+    buf = ctypes.create_string_buffer(cap)
+    ln, verdict = ctypes.c_size_t(), ctypes.c_int32()
+    _check(lib().gl_schedule_files(os.fsencode(profile_csv),
+                                   None if coeffs_json is None else os.fsencode(coeffs_json),
+                                   os.fsencode(workload_json), buf, cap, ctypes.byref(ln), ctypes.byref(verdict)))
+    text = buf.value.decode()
+    head, _, dump = text.partition("\n")
+    return json.loads(head), dump, bool(verdict.value), text
 
 
 def fit_interference(X, y):

@@ -1,0 +1,161 @@
+"""Frontend routing + dispatch + drop decisions (SURVEY §8(a) a5/a6, §8(c) C2.11,
+DESIGN R26): libgpulet's gl_serve_sim — the dispatch rule gl_serve runs, driven
+by a virtual clock against FIFO gpu-lets — must produce exactly the oracle DES's
+batch sequence (lane, dispatch time, size, first request) and per-request
+latencies on seeded traces.  Plus hand-traced DES pins for every condition of
+the rule.  CPU only."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import des
+from oracle import sched as osched
+from oracle import workload as W
+from paper_2109_01611_b200 import gpulet
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROFILE = os.path.join(ROOT, "profiles", "profile_b200.csv")
+COEFFS = os.path.join(ROOT, "profiles", "coeffs_b200.json")
+native_lib = pytest.mark.skipif(not os.path.exists(gpulet.LIB_PATH), reason="libgpulet.so not built")
+
+
+class Flat:
+    """Profile with L(k, p) = lat[k - 1] on every p (hand-traced pins)."""
+
+    def __init__(self, lat):
+        self.lat = lat
+
+    def L(self, m, k, p):
+        return self.lat[k - 1]
+
+
+def trace_of(pairs):
+    return [(t, m) for t, m in pairs]
+
+
+# ---- hand-traced pins of the DES (C2.11 + R26) --------------------------------------------
+def test_batch_formed():
+    """b = 2, long duty cycle: the second arrival (t = 10) completes the batch; end = 10 + 100."""
+    lat, log = des.simulate_trace([(100, 10**6, [(0, 1, 2, 1000)])], Flat([100] * 32), [10_000],
+                                  trace_of([(0, 0), (10, 0)]))
+    assert log == [(0, 10, 2, 0)] and lat == [110, 100]
+
+
+def test_duty_cycle_timeout():
+    """b = 4, D = 1000: a lone request at t = 100 waits for the window (opened at 0) to pass."""
+    lat, log = des.simulate_trace([(100, 1000, [(0, 1, 4, 1000)])], Flat([100] * 32), [10_000],
+                                  trace_of([(100, 0)]))
+    assert log == [(0, 1000, 1, 0)] and lat == [1000]
+
+
+def test_deadline_guard_uses_the_batch_it_would_send():
+    """SLO 500, Leff(1) = 100, Leff(2) = 200: after the second arrival the lane must go by
+    0 + 500 - Leff(2) = 300 (R26), and both requests finish at exactly their SLO."""
+    lat, log = des.simulate_trace([(100, 10**6, [(0, 1, 4, 1000)])], Flat([100, 200] + [300] * 30), [500],
+                                  trace_of([(0, 0), (50, 0)]))
+    assert log == [(0, 300, 2, 0)] and lat == [500, 450]
+
+
+def test_hopeless_requests_dropped():
+    """SLO below Leff(1): nothing can be served, every request dropped (-1)."""
+    lat, log = des.simulate_trace([(100, 1000, [(0, 1, 4, 1000)])], Flat([600] * 32), [500],
+                                  trace_of([(0, 0), (5, 0), (7, 0)]))
+    assert log == [] and lat == [-1, -1, -1]
+
+
+def test_fifo_gpulet_and_smooth_wrr():
+    """Two lanes of model 0 on one gpu-let with weights 2:1 -> A, B, A; batches of 1 queue
+    behind each other on the gpu-let (start = max(t, free))."""
+    lat, log = des.simulate_trace([(100, 10**6, [(0, 2, 1, 1000)]), (0, 10**6, [])], Flat([100] * 32), [10**6],
+                                  trace_of([(0, 0), (0, 0), (0, 0)]))
+    # a single gpu-let hosting one lane: 3 batches at t = 0 back to back
+    assert log == [(0, 0, 1, 0), (0, 0, 1, 1), (0, 0, 1, 2)] and lat == [100, 200, 300]
+    plan = [(50, 10**6, [(0, 2, 1, 1000), (1, 5, 1, 1000)]), (50, 10**6, [(0, 1, 1, 1000)])]
+    lat, log = des.simulate_trace(plan, Flat([100] * 32), [10**6, 10**6],
+                                  trace_of([(0, 0), (1, 0), (2, 0), (3, 1)]))
+    assert [row[0] for row in log] == [0, 2, 0, 1]          # model 0: lanes 0, 2, 0 (weights 2:1); model 1: lane 1
+    assert lat == [100, 100, 198, 297]                      # lanes 0 and 1 share gpu-let 0's FIFO
+
+
+def test_model_without_lane_dropped():
+    lat, log = des.simulate_trace([(100, 10, [(0, 1, 1, 1000)])], Flat([5] * 32), [100, 100],
+                                  trace_of([(0, 1), (3, 0)]))
+    assert lat == [-1, 5] and log == [(0, 3, 1, 1)]
+
+
+# ---- native gl_serve_sim == oracle DES ------------------------------------------------------------
+def _lanes_from_plan(dump, prof_lat):
+    plan, lanes = [], []
+    for gi, line in enumerate(ln for ln in dump.splitlines() if '"gpu"' in ln):
+        d = json.loads(line)
+        if not d["lanes"]:
+            continue
+        ls = []
+        for ln in d["lanes"]:
+            m = W.NAMES.index(ln["model"])
+            g = W.GRID.index(d["size"])
+            leff = [(prof_lat[m][k - 1][g] * ln["F"] + 999) // 1000 for k in range(1, 33)]
+            ls.append((m, ln["rate"], ln["batch"], ln["F"]))
+            lanes.append(dict(gpulet=100 + len(plan), model_slot=m, batch=ln["batch"], duty_us=d["D_us"],
+                              weight=ln["rate"], drop_us=leff[0], leff_us=leff))
+        plan.append((d["size"], d["D_us"], ls))
+    return plan, lanes
+
+
+def _poisson(rates, secs, seed):
+    ts, ms = [], []
+    for m, r in enumerate(rates):
+        if r <= 0:
+            continue
+        rng = np.random.Generator(np.random.PCG64(seed * 131 + m))
+        t = np.cumsum(-np.log(1.0 - rng.random(int(r * secs * 1.3) + 20)) / r * 1e6)
+        t = t[t < secs * 1e6].astype(np.int64)
+        ts.append(t)
+        ms.append(np.full(len(t), m, np.int32))
+    t, m = np.concatenate(ts), np.concatenate(ms)
+    o = np.argsort(t, kind="stable")
+    return t[o], m[o]
+
+
+@native_lib
+@pytest.mark.parametrize("scen,mode,x,n", [("game", "gpulet", 1.0, 1), ("game", "gpulet", 3.0, 1),
+                                           ("traffic", "gpulet", 0.4, 1), ("equal", "gpulet+int", 0.7, 4),
+                                           ("mix6", "sbp", 0.2, 8), ("short-skew", "gpulet", 1.5, 2)])
+@pytest.mark.parametrize("load", [0.8, 1.3])
+def test_serve_sim_equals_des(scen, mode, x, n, load):
+    """Plans from the measured profile (n GPUs: every GPU's gpu-lets in one replay);
+    Poisson traffic at 0.8x and 1.3x (overload: the deadline guard and the drop rule
+    fire) of the planned rates."""
+    prof = W.parse_profile(open(PROFILE).read())
+    for _ in range(12):   # halve x until schedulable on one GPU
+        head, dump, ok, _ = gpulet.schedule_files(PROFILE, COEFFS, {"scenario": scen, "x": x, "mode": mode, "num_gpus": n})
+        if ok:
+            break
+        x /= 2
+    assert ok
+    plan, lanes = _lanes_from_plan(dump, prof["lat"])
+    rates = [r * load for r in head["rates"]]
+    t, m = _poisson(rates, 0.2, seed=int(100 * x) + int(10 * load))
+    lat_n, log_n = gpulet.serve_sim(lanes, 6, t, m, head["slo_us"])
+    lat_o, log_o = des.simulate_trace(plan, osched.Profile(W.NAMES, prof["lat"]), head["slo_us"],
+                                      list(zip(t.tolist(), m.tolist())))
+    assert log_n == log_o
+    assert lat_n.tolist() == lat_o
+    assert len(log_o) > 10
+
+
+@native_lib
+def test_serve_sim_edge_cases():
+    lanes = [dict(gpulet=0, model_slot=0, batch=2, duty_us=100, weight=1, drop_us=10, leff_us=[10] * 32)]
+    lat, log = gpulet.serve_sim(lanes, 2, [], [], [50, 50])
+    assert lat.tolist() == [] and log == []
+    lat, log = gpulet.serve_sim(lanes, 2, [0, 0, 0, 5], [0, 1, 0, 0], [50, 50])
+    lat_o, log_o = des.simulate_trace([(100, 100, [(0, 1, 2, 1000)])], Flat([10] * 32), [50, 50],
+                                      [(0, 0), (0, 1), (0, 0), (5, 0)])
+    assert lat.tolist() == lat_o and log == log_o
+    with pytest.raises(gpulet.GpuletError):
+        gpulet.serve_sim([dict(lanes[0], leff_us=None)], 2, [0], [0], [50, 50])
+    with pytest.raises(gpulet.GpuletError):
+        gpulet.serve_sim(lanes, 2, [5, 0], [0, 0], [50, 50])

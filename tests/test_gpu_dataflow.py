@@ -1,7 +1,7 @@
-"""Barrier-free GEMM step joins (GL_DATAFLOW=1, off by default):
+"""Barrier-free GEMM step joins (gl_set_tuning(6, 1), off by default):
 the same parity bar with the gpu-let barrier replaced by per-M-block
 completion counters between consecutive TMA GEMM steps.  Runs in a child
-process because the switch is read when programs are built."""
+process because the switch applies to programs built afterwards."""
 import os
 import subprocess
 import sys
@@ -18,6 +18,7 @@ from oracle import models as om
 from paper_2109_01611_b200 import gpulet
 from tools import common
 from tests.gpu_util import rel_err, REL_TOL
+gpulet.set_tuning(6, 2)   # dataflow joins + plan log
 ctx = gpulet.Context(1)
 for m, b in (("resnet50", 3), ("vgg16", 2)):
     mid = ctx.load_model(0, m, synthgen.weight_file(m))
@@ -35,7 +36,7 @@ ctx.close()
 
 
 def test_dataflow_joins_parity():
-    env = dict(os.environ, GL_DATAFLOW="1", GL_DATAFLOW_LOG="1", PYTHONPATH=ROOT)
+    env = dict(os.environ, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "barrier-free joins" in r.stderr          # the joins were planned

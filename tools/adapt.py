@@ -79,12 +79,10 @@ def main():
     from tools import common
 
     ctx = gpulet.Context(1)
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
-    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
-    slo = common.slos_from(lat_env)
-    srv = bench.Server(ctx, 0, (lat_env, l2, mem, slo, common.load_coeffs()), False)
+    srv = bench.Server(ctx, 0, False)
+    slo = srv.slo
     xs = srv.max_sched_x(a.scenario, a.mode, 1)
-    peak = common.scenario_rates(a.scenario, slo, xs * a.peak_frac)
+    peak = srv.scenario_rates(a.scenario, xs * a.peak_frac)
     t_us, m_idx = trace(peak, a.secs, 42)
     nper = int(round(a.secs / a.period))
     M = len(common.MODELS)

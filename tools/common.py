@@ -4,7 +4,6 @@ Device inputs are built from synthgen (seeded) and moved to the GPU once; all
 compute goes through libgpulet's C-ABI via the thin binding.
 """
 import csv
-import io
 import json
 import os
 
@@ -14,12 +13,10 @@ import synthgen
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GRID = (20, 40, 50, 60, 80, 100)
-SM_OF = {20: 32, 40: 56, 50: 72, 60: 92, 80: 116, 100: 148}
 STAT_B = (1, 2, 4, 8, 16, 32)
 MODELS = synthgen.MODELS
 PROFILE_CSV = os.path.join(ROOT, "profiles", "profile_b200.csv")
 COEFFS_JSON = os.path.join(ROOT, "profiles", "coeffs_b200.json")
-PAPER_SLO_MS = {"googlenet": 44, "lenet5": 5, "resnet50": 95, "ssd_mobilenet_v1": 136, "vgg16": 130}
 
 
 def device_input(model, batch, batch_id=0):
@@ -63,57 +60,21 @@ def write_profile_csv(path, lat, nsm, l2, mem):
                         w.writerow([name, b, p, nsm[gi], lat[m][b - 1][gi], "", ""])
 
 
-def read_profile_csv(path):
-    from oracle import profiles  # CSV parsing only; no scheduling arithmetic
-    with open(path) as f:
-        return profiles.read_profile_csv(f.read())
+def load_profile(path=PROFILE_CSV, slo_mode="rule"):
+    """The profile as libgpulet parses and envelopes it (gl_profile_load, C4.1) and the
+    SLOs it derives (gl_workload_rates, C4.2): dict lat [m][b-1][gi] (µs), l2, mem
+    [m][si][gi], sm {p: SMs}, slo [m] (µs).  No scheduling arithmetic in Python."""
+    from paper_2109_01611_b200 import gpulet
+    lat, l2, mem, sm = gpulet.profile_load(path)
+    slo = gpulet.workload_rates(lat, "equal", 1.0, 1, slo_mode)[0]
+    return {"lat": lat.tolist(), "l2": l2.tolist(), "mem": mem.tolist(), "sm": dict(zip(GRID, sm.tolist())),
+            "slo": slo, "lat_np": lat}
 
 
-def envelope(lat):
-    """C4.1 min-envelope, applied by the harness before scheduling (as the
-    oracle does); realisable by padding the batch or using fewer SMs."""
-    out = [[0] * 6 for _ in range(32)]
-    for b in range(31, -1, -1):
-        for g in range(6):
-            v = lat[b][g]
-            if b + 1 < 32:
-                v = min(v, out[b + 1][g])
-            if g > 0:
-                v = min(v, out[b][g - 1])
-            out[b][g] = v
-    return out
-
-
-def slos_from(lat_env):
-    """SLO_m = 2 L*(32, 100 %)."""
-    return [2 * lat_env[m][31][5] for m in range(len(lat_env))]
-
-
-def scenario_rates(name, slo_us, x=1.0):
-    """Rates of a scenario, scaled by SLO_paper/SLO_B200 (C4.3) and multiplier x."""
-    base = {"equal": (50,) * 6, "mix6": (50,) * 6, "long-only": (0, 0, 100, 100, 100, 100),
-            "short-skew": (100, 100, 100, 50, 50, 50)}
-    app_ref = None
-    if name.startswith("game"):
-        r = (6, 0, 1, 0, 0, 0)
-        base_r = [v * 100 for v in r]
-        app_ref = "resnet50"           # app SLO = ResNet-50's (P:791-792)
-    elif name.startswith("traffic"):
-        base_r = [0, 100, 0, 100, 100, 0]
-        app_ref = "ssd_mobilenet_v1"   # app SLO = SSD's 136 ms (P:791-792)
-    else:
-        base_r = list(base[name])
-    if app_ref is not None:
-        # an application keeps its composition (P:787-790: 6 LeNet + 1 ResNet per
-        # game request): one B200 scale for all its models, the app-SLO model's
-        s = PAPER_SLO_MS[app_ref] * 1000.0 / slo_us[MODELS.index(app_ref)]
-        return [int(r * s * x) for r in base_r]
-    out = []
-    for m, r in enumerate(base_r):
-        ref = MODELS[m] if MODELS[m] in PAPER_SLO_MS else "resnet50"
-        s = PAPER_SLO_MS[ref] * 1000.0 / slo_us[MODELS.index(ref)]
-        out.append(int(r * s * x))
-    return out
+def scenario_rates(prof, scen, x=1.0, n_gpus=1, slo_mode="rule"):
+    """Scenario rates at multiplier x (gl_workload_rates: C4.3-C4.4, scaled natively)."""
+    from paper_2109_01611_b200 import gpulet
+    return gpulet.workload_rates(prof["lat_np"], scen, x, n_gpus, slo_mode)[1]
 
 
 def load_coeffs(path=COEFFS_JSON):

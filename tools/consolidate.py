@@ -53,17 +53,18 @@ def main():
     from tools import common
 
     ctx = gpulet.Context(1)
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
-    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
-    slo = common.slos_from(lat_env)
-    srv = bench.Server(ctx, 0, (lat_env, l2, mem, slo, common.load_coeffs()), False)
+    srv = bench.Server(ctx, 0, False)
+    lat_env, slo = srv.lat, srv.slo
     small, large = a.models.split(",")
     ms, ml = common.MODELS.index(small), common.MODELS.index(large)
     g100, g20, g80 = common.GRID.index(100), common.GRID.index(20), common.GRID.index(80)
     base = [0] * len(common.MODELS)
-    for m in (ms, ml):   # the paper's 100 req/s per model, scaled to B200 (C4.3)
-        ref = common.MODELS[m] if common.MODELS[m] in common.PAPER_SLO_MS else "resnet50"
-        base[m] = 100.0 * common.PAPER_SLO_MS[ref] * 1000.0 / slo[common.MODELS.index(ref)]
+    # the paper's 100 req/s per model, scaled to B200 (C4.3, gl_workload_rates' per-model
+    # scale: the "long-only" scenario is 100 req/s of ResNet/SSD/VGG/BERT, "short-skew" 100 of LeNet)
+    lo = srv.scenario_rates("long-only", 1.0)
+    sk = srv.scenario_rates("short-skew", 1.0)
+    for m in (ms, ml):
+        base[m] = float(lo[m] if lo[m] else sk[m])
     out = {"models": [small, large], "slo_us": [slo[ms], slo[ml]], "base_req_s": [base[ms], base[ml]],
            "secs": a.secs, "cite": "P:257-276", "curves": {"temporal": [], "spatial-20:80": []}}
     for x in [float(v) for v in a.xs.split(",")]:

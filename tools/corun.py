@@ -78,7 +78,8 @@ def main():
     xs = {m: common.device_input(m, 32) for m in models}
     ys = {(m, s): torch.empty(ctx.model_io(mids[m], 32)[1] // 4, device="cuda") for m in models for s in (0, 1)}
     torch.cuda.current_stream().synchronize()
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
+    prof = common.load_profile()
+    l2, mem = prof["l2"], prof["mem"]
     si = {b: common.STAT_B.index(min(sb for sb in common.STAT_B if sb >= b)) for b in batches}
     rows = []
     t0 = time.time()

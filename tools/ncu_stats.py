@@ -34,7 +34,6 @@ def order(sm_counts):
 def launch():
     import torch
     from paper_2109_01611_b200 import gpulet
-    lat, _l2, _mem = common.read_profile_csv(common.PROFILE_CSV)
     nsm = read_sm_counts()
     ctx = gpulet.Context(1)
     mids = {m: ctx.load_model(0, m, synthgen.weight_file(m)) for m in common.MODELS}

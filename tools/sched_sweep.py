@@ -6,14 +6,18 @@ model of the five takes a rate in {0, 200, 400, 600} req/s, all-zero excluded
 Schedulable.  Its ideal comparison (Fig. ideal_1023): gpulet+int
 schedules 18 fewer than the exhaustive ideal (1.8 % of 1,023) on 4 GPUs.
 
-Here the rates are scaled to B200 by SLO_paper / SLO_B200 per model (C4.3),
-the profile / SLOs / interference coefficients are the measured B200 ones
-(profiles/profile_b200.csv, coeffs_b200.json), and the native scheduler
-(libgpulet gl_schedule, CPU code) decides; a seeded sample of the decisions
-is replayed through the oracle (oracle/sched.py) and must be byte-identical.
+Here every decision is one gl_schedule_files call on the measured B200 files
+(profiles/profile_b200.csv, coeffs_b200.json): the profile envelope, the SLOs
+(rule or Table constants) and the B200 rate scaling of the paper's rates
+(C4.3) are native; a seeded sample of the decisions is replayed through the
+oracle (oracle/workload.py + oracle/sched.py) and must be byte-identical.
+Modes: SBP on whole GPUs and on 50:50 gpu-lets (Fig. success-case), gpulet,
+gpulet+int, and the exhaustive ideal (Fig. ideal_1023); then the maximum
+schedulable rate of the five scenarios per mode, normalised to SBP and to the
+ideal (Fig. ideal_macrobenchmark, P:933-940).
 
-    python tools/sched_sweep.py [--gpus 1,4] [--modes sbp,gpulet,gpulet+int,ideal]
-                                [--with-bert] [--json profiles/sched_sweep_b200.json]
+    python tools/sched_sweep.py [--gpus 1,4] [--modes sbp,sbp50,gpulet,gpulet+int,ideal]
+                                [--with-bert] [--slo-mode rule|table] [--json profiles/sched_sweep_b200.json]
 """
 import argparse
 import itertools
@@ -37,28 +41,30 @@ def scenarios(n_models):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", default="1,4")
-    ap.add_argument("--modes", default="sbp,gpulet,gpulet+int,ideal")
+    ap.add_argument("--modes", default="sbp,sbp50,gpulet,gpulet+int,ideal")
     ap.add_argument("--with-bert", action="store_true", help="6 models (4^6 - 1 = 4,095 scenarios)")
-    ap.add_argument("--oracle-sample", type=int, default=40, help="decisions replayed through oracle/sched.py")
+    ap.add_argument("--slo-mode", default="rule", choices=["rule", "table"])
+    ap.add_argument("--oracle-sample", type=int, default=40, help="decisions replayed through oracle/")
     ap.add_argument("--json", default="")
     a = ap.parse_args()
     from paper_2109_01611_b200 import gpulet
 
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
-    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
-    slo = common.slos_from(lat_env)
-    coeffs = common.load_coeffs()
+    prof, coeffs = common.PROFILE_CSV, common.COEFFS_JSON
+
+    def decide(workload):
+        """gl_schedule_files: the profile, SLOs and B200 rate scaling are all native (C4)."""
+        head, _dump, ok, text = gpulet.schedule_files(prof, coeffs, dict(workload, slo_mode=a.slo_mode))
+        return head, ok, text
+
     nm = 6 if a.with_bert else 5
     names = list(common.MODELS[:nm])
-    scale = []
-    for m in names:
-        ref = m if m in common.PAPER_SLO_MS else "resnet50"
-        scale.append(common.PAPER_SLO_MS[ref] * 1000.0 / slo[common.MODELS.index(ref)])
-    L, L2, ME, S = lat_env[:nm], l2[:nm], mem[:nm], slo[:nm]
     scen = scenarios(nm)
-    out = {"scenarios": len(scen), "levels_req_s_paper": LEVELS, "models": names,
-           "b200_rate_scale": [round(s, 3) for s in scale], "slo_us": S, "coeffs": list(coeffs),
-           "paper": {"ideal_minus_gpulet_int": 18, "of": 1023, "gpus": 4, "cite": "P:927"}, "results": {}}
+    head0, _, _ = decide({"rates": [0] * 6})
+    out = {"scenarios": len(scen), "levels_req_s_paper": LEVELS, "models": names, "slo_mode": a.slo_mode,
+           "slo_us": head0["slo_us"][:nm], "coeffs": common.load_coeffs(),
+           "paper": {"ideal_minus_gpulet_int": 18, "of": 1023, "gpus": 4, "cite": "P:927",
+                     "success_case": "SBP without vs with 50:50 partitioning, Fig. success-case P:262-270"},
+           "results": {}}
     decided = []
     for N in [int(v) for v in a.gpus.split(",")]:
         for mode in a.modes.split(","):
@@ -66,11 +72,11 @@ def main():
             ok = 0
             flags = []
             for r in scen:
-                rates = [int(v * s) for v, s in zip(r, scale)]
-                _dump, sch = gpulet.schedule(names, L, L2, ME, S, rates, N, mode, coeffs)
+                wl = {"base_rates": list(r) + [0] * (6 - nm), "num_gpus": N, "mode": mode}
+                _h, sch, _t = decide(wl)
                 ok += sch
                 flags.append(sch)
-                decided.append((N, mode, rates))
+                decided.append(wl)
             dt = time.perf_counter() - t0
             out["results"][f"{mode}@{N}"] = {"schedulable": ok, "of": len(scen),
                                              "native_ms_per_decision": round(1e3 * dt / len(scen), 4)}
@@ -86,51 +92,63 @@ def main():
             out["results"][f"gpulet_int_not_ideal@{N}"] = sum(
                 1 for x, y in zip(g["_flags"], i["_flags"]) if x and not y)
     # scheduler-level maximum rates (the paper's Fig. "maximum achievable
-    # throughput", before serving validation): per scenario, GPU
-    # count and mode, the largest rate multiplier the scheduler accepts
+    # throughput", and Fig. ideal_macrobenchmark: rates
+    # normalised to the ideal's), per scenario, GPU count and mode
     cap = {}
-    full_l2, full_mem = l2, mem
-    for scen in ("game", "traffic", "equal", "long-only", "short-skew"):
+    for sc in ("game", "traffic", "equal", "long-only", "short-skew"):
         for N in (1, 2, 4, 8):
-            for mode in ("sbp", "gpulet", "gpulet+int"):
+            for mode in ("sbp", "sbp50", "gpulet", "gpulet+int", "ideal"):
+                if mode == "ideal" and N > 4:
+                    continue
+
                 def ok(x):
-                    rates = common.scenario_rates(scen, slo, x)
-                    return gpulet.schedule(common.MODELS, lat_env, full_l2, full_mem, slo, [r * N for r in rates],
-                                           N, mode, coeffs)[1] and sum(rates) > 0
+                    return decide({"scenario": sc, "x": x, "num_gpus": N, "mode": mode})[1]
                 lo, hi = 0.0, 0.25
                 while ok(hi) and hi < 1e4:
                     lo, hi = hi, hi * 2
                 for _ in range(30):
                     mid = (lo + hi) / 2
                     lo, hi = (mid, hi) if ok(mid) else (lo, mid)
-                rates = common.scenario_rates(scen, slo, lo)
-                cap[f"{scen}@{N}/{mode}"] = {"x": round(lo, 4), "model_req_s": sum(rates) * N}
+                rates = decide({"scenario": sc, "x": lo, "num_gpus": N, "mode": mode})[0]["rates"]
+                cap[f"{sc}@{N}/{mode}"] = {"x": round(lo, 4), "model_req_s": sum(rates) if lo > 0 else 0}
         for N in (1, 2, 4, 8):
-            b = cap[f"{scen}@{N}/sbp"]["model_req_s"]
-            for mode in ("gpulet", "gpulet+int"):
-                g = cap[f"{scen}@{N}/{mode}"]["model_req_s"]
-                cap[f"{scen}@{N}/{mode}"]["vs_sbp"] = round(g / b, 3) if b else None
+            b = cap[f"{sc}@{N}/sbp"]["model_req_s"]
+            idl = cap.get(f"{sc}@{N}/ideal", {}).get("model_req_s")
+            for mode in ("sbp50", "gpulet", "gpulet+int"):
+                g = cap[f"{sc}@{N}/{mode}"]["model_req_s"]
+                cap[f"{sc}@{N}/{mode}"]["vs_sbp"] = round(g / b, 3) if b else None
+                if idl:
+                    cap[f"{sc}@{N}/{mode}"]["vs_ideal"] = round(g / idl, 3)
     out["max_schedulable_rate"] = cap
+    ratios = [v["vs_ideal"] for k, v in cap.items() if k.endswith("/gpulet+int") and v.get("vs_ideal") is not None
+              and "@4/" in k]
+    out["gpulet_int_vs_ideal_rate_at_4"] = {"mean": round(sum(ratios) / len(ratios), 4) if ratios else None,
+                                            "min": min(ratios) if ratios else None,
+                                            "paper": "92.3 % mean, traffic lowest at 87.7 % (P:939-940)"}
     out["paper_max_rate"] = {"cite": "P:833-852 (4 x 2080 Ti)", "gpulet_vs_sbp": "+106.0 %",
                              "gpulet_int_vs_sbp": "+102.6 %"}
     for k, v in cap.items():
-        if k.endswith("gpulet+int") or k.endswith("gpulet"):
-            print(f"{k:28s} {v}", flush=True)
-    # oracle replay of a seeded sample (byte-identical plan dumps)
-    from oracle import sched as osched
-    P = osched.Profile(names, L, L2, ME)
+        print(f"{k:28s} {v}", flush=True)
+    # oracle replay of a seeded sample (byte-identical outputs: header + plan dump)
+    from oracle import workload as owl
+    with open(prof) as f:
+        ptxt = f.read()
+    with open(coeffs) as f:
+        ctxt = f.read()
     rnd = random.Random(11)
     sample = rnd.sample(decided, min(a.oracle_sample, len(decided)))
-    same, t_or = 0, 0.0
-    for N, mode, rates in sample:
-        dump, sch = gpulet.schedule(names, L, L2, ME, S, rates, N, mode, coeffs)
+    same, t_or, t_nat = 0, 0.0, 0.0
+    for wl in sample:
         t0 = time.perf_counter()
-        ref = osched.ideal(P, S, rates, N, "gpulet+int", coeffs) if mode == "ideal" else \
-            osched.schedule(P, S, rates, N, mode, coeffs)
+        _h, sch, text = decide(wl)
+        t_nat += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref, rok = owl.schedule_files(ptxt, ctxt, json.dumps(dict(wl, slo_mode=a.slo_mode)))
         t_or += time.perf_counter() - t0
-        same += (ref.dump == dump and ref.ok == sch)
+        same += (ref == text and rok == sch)
     out["oracle_replay"] = {"sample": len(sample), "identical": same,
-                            "oracle_ms_per_decision": round(1e3 * t_or / max(1, len(sample)), 3)}
+                            "oracle_ms_per_decision": round(1e3 * t_or / max(1, len(sample)), 3),
+                            "native_ms_per_decision_incl_file_parse": round(1e3 * t_nat / max(1, len(sample)), 3)}
     print(f"oracle replay: {same}/{len(sample)} identical", flush=True)
     for v in out["results"].values():
         if isinstance(v, dict):
@@ -138,7 +156,7 @@ def main():
     if a.json:
         with open(a.json, "w") as f:
             json.dump(out, f, indent=1)
-    print(json.dumps({k: v for k, v in out.items() if k != "results"}))
+    print(json.dumps({k: v for k, v in out.items() if k not in ("results", "max_schedulable_rate")}))
     print(json.dumps(out["results"]))
 
 

@@ -22,10 +22,7 @@ def main():
     from paper_2109_01611_b200 import gpulet
     from tools import common
     ctx = gpulet.Context(1)
-    lat, l2, mem = common.read_profile_csv(common.PROFILE_CSV)
-    lat_env = [common.envelope(lat[m]) for m in range(len(common.MODELS))]
-    slo = common.slos_from(lat_env)
-    srv = bench.Server(ctx, 0, (lat_env, l2, mem, slo, common.load_coeffs()), False)
+    srv = bench.Server(ctx, 0, False)
     out = {"lib": os.environ.get("GL_LIB", "in-tree")}
     for m, b in (("lenet5", 24), ("resnet50", 15)):
         d = [sum(ctx.run_once(srv.mids[m], b, srv.x[m, 0], srv.y[m, 0], 0, True)) / 1e3 for _ in range(5)]
