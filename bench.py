@@ -152,31 +152,43 @@ def allmax(dist, vals):
 
 
 # ----------------------------------------------------------------------------- oracle arm
+GAME_MIX = (("lenet5", 6), ("resnet50", 1))   # one game app request = 6 LeNet-5 + 1 ResNet-50
+
+
+def _oracle_game_request(omodels, ws, seed):
+    """The oracle serving one game app request (7 model requests, batch 1 each)."""
+    for m, k in GAME_MIX:
+        for j in range(k):
+            omodels.forward(m, ws[m], synthgen.model_input(m, 1, batch_id=seed * 8 + j))
+    return sum(k for _m, k in GAME_MIX)
+
+
 def reference_arm(a, world, rank):
-    """The CPU oracle (fp64 numpy forward) as it stands, one request per step,
-    models cycled in canonical order (bounded sample of the same mixed workload)."""
+    """The CPU oracle (fp64 numpy forward) as it stands on the headline workload's
+    request mix: each step = one game app request (6 LeNet-5 + 1 ResNet-50, batch 1),
+    a bounded sample of the same workload; value = model req/s."""
     if rank != 0:
         return None
     from oracle import models as omodels
-    ws = {m: synthgen.weights(m) for m in synthgen.MODELS}
-    order = list(synthgen.MODELS)
-    times = []
+    ws = {m: synthgen.weights(m) for m, _k in GAME_MIX}
+    times, reqs = [], 0
     for s in range(a.warmup + a.steps):
-        m = order[s % len(order)]
-        x = synthgen.model_input(m, 1, batch_id=s)
         t0 = time.perf_counter()
-        omodels.forward(m, ws[m], x)
+        n = _oracle_game_request(omodels, ws, s)
         if s >= a.warmup:
             times.append(time.perf_counter() - t0)
+            reqs += n
     tot = sum(times)
-    val = a.steps / tot
+    val = reqs / tot
     cores = _blas_threads()
     return {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1000 * tot / a.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "oracle forward, 1 request per step cycling the six models"},
+            "data": "synthetic",
+            "config": {"workload": "cfg4 game request mix on the CPU oracle: one app request (6 LeNet-5 + 1 ResNet-50, "
+                                   "batch 1, fp64 numpy) per step"},
             "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": "1 request per step, models cycled in canonical order"},
+                             "sample": f"{a.steps} game app requests = {reqs} model requests"},
             "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -190,17 +202,34 @@ def _blas_threads():
 
 
 def cpu_baseline_sample():
-    """Oracle on the host cores: one request of each of the six models (batch 1)."""
+    """The oracle on the host cores: the game mix at batch 1 (the
+    headline's unit, model req/s), every model's batch-1 forward, and cfg1's
+    LeNet-5 b = 32 in seconds at 1 BLAS thread and at all threads (median of 5)."""
+    from threadpoolctl import threadpool_limits
     from oracle import models as omodels
-    t = 0.0
+    ws = {m: synthgen.weights(m) for m in synthgen.MODELS}
+    t0 = time.perf_counter()
+    reqs = sum(_oracle_game_request(omodels, ws, s) for s in range(3))
+    t_game = time.perf_counter() - t0
+    b1 = {}
     for m in synthgen.MODELS:
-        w = synthgen.weights(m)
         x = synthgen.model_input(m, 1)
         t0 = time.perf_counter()
-        omodels.forward(m, w, x)
-        t += time.perf_counter() - t0
-    return {"value": round(len(synthgen.MODELS) / t, 4), "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
-            "sample": "one batch-1 request of each of the six models (fp64 numpy forward)"}
+        omodels.forward(m, ws[m], x)
+        b1[m] = round(time.perf_counter() - t0, 4)
+    x32 = synthgen.model_input("lenet5", 32)
+    le = {}
+    for th in (1, None):
+        with threadpool_limits(limits=th):
+            ts = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                omodels.forward("lenet5", ws["lenet5"], x32)
+                ts.append(time.perf_counter() - t0)
+        le["1_thread" if th == 1 else "all_threads"] = round(statistics.median(ts), 5)
+    return {"value": round(reqs / t_game, 4), "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
+            "sample": f"3 game app requests (6 LeNet-5 + 1 ResNet-50 each, batch 1, fp64 numpy) = {reqs} model requests",
+            "model_b1_s": b1, "cfg1_lenet5_b32_s": le, "host_cpus": os.cpu_count()}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -248,7 +277,8 @@ class Server:
         lat, l2, mem, sm = gpulet.profile_load(self.profile_csv)
         self.lat, self.l2, self.mem = lat.tolist(), l2.tolist(), mem.tolist()
         self.sm_of = dict(zip(common.GRID, sm.tolist()))
-        self.slo = gpulet.workload_rates(lat, "equal", 1.0, 1, slo_mode)[0]
+        self.lat_np = lat
+        self.set_slo_mode(slo_mode)
         self.mids = {m: ctx.load_model(gpu, m, synthgen.weight_file(m)) for m in common.MODELS}
         self.x, self.y, self.xh, self.yh, self.req_bytes = {}, {}, {}, {}, {}
         self.x2, self.y2 = {}, {}
@@ -278,6 +308,12 @@ class Server:
         torch.cuda.current_stream().synchronize()
         self.made, self.lanes = [], []
         self.made_sizes, self.made_nsm, self.reorganised = None, [], False
+
+    def set_slo_mode(self, slo_mode):
+        """C4.2: "rule" (2 x L*(32, 100 %)) or "table" (Table tab:ml-models)."""
+        from paper_2109_01611_b200 import gpulet
+        self.slo_mode = slo_mode
+        self.slo = gpulet.workload_rates(self.lat_np, "equal", 1.0, 1, slo_mode)[0]
 
     def _schedule(self, workload):
         from paper_2109_01611_b200 import gpulet
@@ -342,10 +378,14 @@ class Server:
             for ln in g["lanes"]:
                 m = ln["model"]
                 mi = common.MODELS.index(m)
-                drop = (self.lat[mi][0][common.GRID.index(g["size"])] * ln["F"] + 999) // 1000   # Leff(1)
+                gi = common.GRID.index(g["size"])
+                # Leff(k) = ceil(L(k, p) F / 1000) for k = 1..32: the drop rule uses Leff(1), the
+                # deadline guard the batch the lane would send (include/gpulet.h "Dispatch rule")
+                leff = [(self.lat[mi][k - 1][gi] * ln["F"] + 999) // 1000 for k in range(1, 33)]
                 ib, ob = self.req_bytes[m]
                 self.lanes.append(dict(gpulet=gid, model_id=self.mids[m], model_slot=mi, batch=ln["batch"],
-                                       duty_us=g["D_us"], weight=ln["rate"], drop_us=drop, x=self.x[m, g["slot"]],
+                                       duty_us=g["D_us"], weight=ln["rate"], drop_us=leff[0], leff_us=leff,
+                                       x=self.x[m, g["slot"]],
                                        y=self.y[m, g["slot"]], x_host=self.xh.get(m), y_host=self.yh.get(m),
                                        x2=self.x2.get((m, g["slot"])), y2=self.y2.get((m, g["slot"])),
                                        in_req_bytes=ib, out_req_bytes=ob, host_slots=self.host_slots.get(m, self.HOST_SLOTS),
@@ -387,77 +427,146 @@ class Server:
                     lanes=st["lanes"])
 
 
-def run_mode(srv, dist, rank, world, scen, mode, a, timed=True, clocks=False):
-    """Rate search + timed windows for one (scenario, mode).  Returns a dict."""
+def timed_runs(srv, dist, world, my, a, seed0, clocks=None):
+    """a.repeats runs of exactly a.steps timed windows (a step = one window of Poisson
+    arrivals), each run bracketed by a barrier; per run: SLO-satisfying requests,
+    arrivals, violations summed over ranks and the serving time max over ranks."""
+    runs, wins_all = [], []
+    if clocks:
+        clocks.__enter__()
+    try:
+        for rep in range(a.repeats):
+            if dist:
+                dist.barrier()
+            wins = [srv.window(my, a.window, seed0 + 100 * rep + s) for s in range(a.steps)]
+            wins_all += wins
+            sat, arr, viol = allsum(dist, [sum(w["sat"] for w in wins), sum(w["arrivals"] for w in wins),
+                                           sum(w["viol"] for w in wins)])
+            # serving time of a window: its device span (first dequeue -> last completion,
+            # %globaltimer), at least the arrival window itself (sparse traffic must
+            # not read as a high rate)
+            dev_s, wall_s, serve_s = allmax(dist, [sum(w["dev_s"] for w in wins), sum(w["wall_s"] for w in wins),
+                                                   sum(max(w["dev_s"], a.window) for w in wins)])
+            runs.append(dict(value=sat / serve_s if serve_s else 0.0, sat=sat, arrivals=arr,
+                             viol_frac=viol / max(arr, 1), dev_s=dev_s, wall_s=wall_s, serve_s=serve_s,
+                             windows=len(wins), per_model={k: v for w in wins[-1:] for k, v in w["per"].items()}))
+    finally:
+        if clocks:
+            clocks.__exit__()
+    return runs, wins_all
+
+
+def run_mode(srv, dist, rank, world, scen, mode, a, clocks=False):
+    """Headline: rate search, then a.repeats timed runs of a.steps windows at the
+    found multiplier x.  The pass rule (<= 1 % late + dropped, R19) must hold
+    in every timed run, not only in the probes: otherwise x is lowered by 4 % and
+    the timed runs are repeated (at most a.retries times).  value = the median run."""
     from tools import common
     xs = srv.max_sched_x(scen, mode, world)
     if not srv.plan(scen, mode, world, xs)[2]:
-        # no multiplier gives every model of the scenario a positive, schedulable rate on `world` GPU(s)
         return {"value": None, "x_sched": xs, "x": 0.0, "probes": [], "rates": [0] * len(common.MODELS),
                 "note": f"not schedulable on {world} GPU(s) at any multiplier that keeps every model of the scenario"}
-    best, probes = search(srv, dist, rank, world, scen, mode, a, xs, e2e=False)
+    best, probes = search(srv, dist, rank, world, scen, mode, a, xs, e2e=False, reps=3, win=a.probe_window)
     if best is None:
-        return {"value": 0.0, "x_sched": xs, "x": 0.0, "probes": probes, "rates": [0] * len(common.MODELS)}
-    rates, dump, ok = srv.plan(scen, mode, world, best)
-    my = srv.setup(dump, rank)
-    res = {"x_sched": xs, "x": best, "probes": probes, "rates": rates, "plan": dump,
-           "lanes": [{k: ln[k] for k in ("model", "batch", "duty_us", "size", "sm", "weight", "gpulet")}
-                     for ln in srv.lanes]}
-    try:
-        for s in range(a.warmup):
-            srv.window(my, a.window, 2000 + s)
-        if dist:
-            dist.barrier()
-        clk = ClockSampler(srv.gpu) if clocks else None
-        if clk:
-            clk.__enter__()
-        wins = [srv.window(my, a.window, 3000 + s) for s in range(a.steps if timed else 1)]
-        if clk:
-            clk.__exit__()
-            res["clocks"] = clk.summary()
-        res["lane_util"] = lane_util(srv, wins)
-        sat, arr, viol = allsum(dist, [sum(w["sat"] for w in wins), sum(w["arrivals"] for w in wins),
-                                       sum(w["viol"] for w in wins)])
-        # serving time of a window: its device span (first dequeue -> last completion,
-        # %globaltimer), at least the arrival window itself (sparse traffic must
-        # not read as a high rate)
-        dev_s, wall_s, serve_s = allmax(dist, [sum(w["dev_s"] for w in wins), sum(w["wall_s"] for w in wins),
-                                               sum(max(w["dev_s"], a.window) for w in wins)])
-        res.update(value=sat / serve_s if serve_s else 0.0, sat=sat, arrivals=arr, viol_frac=viol / max(arr, 1),
-                   dev_s=dev_s, serve_s=serve_s, wall_s=wall_s, windows=len(wins),
-                   per_model={k: v for w in wins[-1:] for k, v in w["per"].items()})
-    finally:
-        srv.teardown()
-    if a.e2e and timed:
-        res["e2e"] = e2e_leg(srv, dist, rank, world, scen, mode, a, best)
+        return {"value": None, "x_sched": xs, "x": 0.0, "probes": probes, "rates": [0] * len(common.MODELS),
+                "note": "no probed multiplier met the <= 1 % violation rule"}
+    x, attempts = best, []
+    for attempt in range(a.retries + 1):
+        rates, dump, ok = srv.plan(scen, mode, world, x)
+        if not ok:
+            x *= 0.96
+            continue
+        my = srv.setup(dump, rank)
+        res = {"x_sched": xs, "x": x, "probes": probes, "rates": rates, "plan": dump,
+               "lanes": [{k: ln[k] for k in ("model", "batch", "duty_us", "size", "sm", "weight", "gpulet")}
+                         for ln in srv.lanes]}
+        try:
+            for s in range(a.warmup):
+                srv.window(my, a.window, 2000 + s)
+            clk = ClockSampler(srv.gpu) if clocks else None
+            runs, wins = timed_runs(srv, dist, world, my, a, 3000 + 1000 * attempt, clk)
+            if clk:
+                res["clocks"] = clk.summary()
+            res["lane_util"] = lane_util(srv, wins)
+        finally:
+            srv.teardown()
+        worst = max(r["viol_frac"] for r in runs)
+        attempts.append({"x": round(x, 4), "viol_frac": [round(r["viol_frac"], 4) for r in runs],
+                         "value": [round(r["value"], 1) for r in runs]})
+        if worst <= 0.01:
+            break
+        x *= 0.96
+    vals = sorted(r["value"] for r in runs)
+    med = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
+    res.update(value=med["value"], sat=med["sat"], arrivals=med["arrivals"], viol_frac=med["viol_frac"],
+               dev_s=med["dev_s"], serve_s=med["serve_s"], wall_s=med["wall_s"], windows=med["windows"],
+               per_model=med["per_model"], attempts=attempts, criterion_met=worst <= 0.01,
+               repeats=[{"value": round(r["value"], 2), "viol_frac": round(r["viol_frac"], 4),
+                         "arrivals": r["arrivals"]} for r in runs],
+               spread=round((vals[-1] - vals[0]) / max(vals[len(vals) // 2], 1e-9), 4))
+    if a.e2e:
+        res["e2e"] = e2e_leg(srv, dist, rank, world, scen, mode, a, res["x"])
     return res
 
 
-def search(srv, dist, rank, world, scen, mode, a, x0, e2e):
+def quick_mode(srv, dist, rank, world, scen, mode, a):
+    """One cell of the comparison matrix (same kernels, same frontend): the rate
+    search with single probe windows, then one verification window at the found x."""
+    from tools import common
+    xs = srv.max_sched_x(scen, mode, world)
+    if not srv.plan(scen, mode, world, xs)[2]:
+        return {"value": None, "x_sched": round(xs, 4), "note": "not schedulable (every model of the scenario "
+                                                               "needs a positive, schedulable rate)"}
+    best, probes = search(srv, dist, rank, world, scen, mode, a, xs, e2e=False, reps=1, win=a.matrix_window,
+                          max_probes=a.matrix_probes)
+    if best is None:
+        return {"value": 0.0, "x_sched": round(xs, 4), "probes": probes,
+                "note": "no probed multiplier met the <= 1 % violation rule"}
+    rates, dump, ok = srv.plan(scen, mode, world, best)
+    my = srv.setup(dump, rank)
+    try:
+        w = srv.window(my, 2 * a.matrix_window, 7000)
+    finally:
+        srv.teardown()
+    sat, arr, viol = allsum(dist, [w["sat"], w["arrivals"], w["viol"]])
+    serve, = allmax(dist, [max(w["dev_s"], 2 * a.matrix_window)])
+    return {"value": round(sat / serve, 2), "x": round(best, 4), "x_sched": round(xs, 4), "rates_req_s": rates,
+            "viol_frac": round(viol / max(arr, 1), 4),
+            "gpulets": sorted({(ln["size"], ln["sm"]) for ln in srv_lanes_of(dump, srv)})}
+
+
+def srv_lanes_of(dump, srv):
+    from tools import common
+    gls, _ = common.parse_plan(dump)
+    return [{"size": g["size"], "sm": g["sm"]} for g in gls if g["lanes"]]
+
+
+def search(srv, dist, rank, world, scen, mode, a, x0, e2e, reps=3, win=None, max_probes=None):
     """Bisect the rate multiplier down from x0 until violations (late + dropped,
     P:860) are <= 1 % of arrivals (R19).  Returns (best x or None, probes)."""
     lo, hi, best = 0.0, x0, None
     x = x0
     probes = []
-    for it in range(a.probes + 1):
+    win = win or a.probe_window
+    for it in range((max_probes if max_probes is not None else a.probes) + 1):
         rates, dump, ok = srv.plan(scen, mode, world, x)
         w = None
-        if ok and sum(rates) > 0:
+        if ok:
             # median violation rate of three runs (P:823: "iterate the experiment
             # three times ... and pick the median SLO violation rate")
             my = srv.setup(dump, rank)
             runs = []
-            for rep in range(3):
-                w = srv.window(my, a.probe_window, (5000 if e2e else 1000) + 10 * it + rep, e2e=e2e)
+            for rep in range(reps):
+                w = srv.window(my, win, (5000 if e2e else 1000) + 10 * it + rep, e2e=e2e)
                 arr_r, viol_r = allsum(dist, [w["arrivals"], w["viol"]])
                 runs.append((viol_r / arr_r if arr_r else 1.0, arr_r, viol_r))
             srv.teardown()
-            frac, arr, viol = sorted(runs)[1]
+            frac, arr, viol = sorted(runs)[len(runs) // 2]
         else:
             arr, viol, frac = 0, 1, 1.0
         probes.append({"x": round(x, 4), "viol_frac": round(frac, 4),
                        "viol_by_model": {k: v["viol"] for k, v in (w["per"] if w else {}).items() if v["viol"]}})
-        log(f"[{scen}/{mode}{'/e2e' if e2e else ''}] probe x={x:.4f} viol={frac:.4f}")
+        log(f"[{scen}/{mode}/{srv.slo_mode}{'/e2e' if e2e else ''}] probe x={x:.4f} viol={frac:.4f}")
         if arr and frac <= 0.01:
             lo, best = x, x
             if it == 0:
@@ -476,7 +585,7 @@ def e2e_leg(srv, dist, rank, world, scen, mode, a, x_dev):
     latency (gl_serve end-to-end mode); its own rate search from the
     device-resident maximum down; value = SLO-satisfying requests / host wall
     time of the timed windows."""
-    best, probes = search(srv, dist, rank, world, scen, mode, a, x_dev, e2e=True)
+    best, probes = search(srv, dist, rank, world, scen, mode, a, x_dev, e2e=True, reps=3, win=a.probe_window)
     if best is None:
         return {"value": 0.0, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0, "probes": probes}
     rates, dump, ok = srv.plan(scen, mode, world, best)
@@ -498,6 +607,16 @@ def e2e_leg(srv, dist, rank, world, scen, mode, a, x_dev):
             "slo_satisfied_frac": round(esat / max(earr, 1), 4), "probes": probes,
             "per_model": {k: v for w in ew[-1:] for k, v in w["per"].items()},
             "timing": "host wall clock of the windows; H2D/D2H of every batch inside each request's latency"}
+
+
+def _bw_of(sm_pct):
+    """K12 HBM roof of a gpu-let size (profiles/extras_b200.json, tools/measure_extras.py),
+    else None (the whole-GPU copy peak is used and said so)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "extras_b200.json")) as f:
+            return json.load(f)["bw_probe"][str(sm_pct)]["gbs"]
+    except Exception:
+        return None
 
 
 def lane_util(srv, wins):
@@ -522,6 +641,8 @@ def lane_util(srv, wins):
         # at the 1965 MHz boost clock), not the tensor pipe's
         alu = m == "lenet5"
         peak_t = ln["sm"] * 128 * 2 * 1.965e9 / 1e12 if alu else ln["sm"] / 148.0 * sus
+        bw = _bw_of(ln["size"])
+        hbm_l = bw if bw else hbm
         ach_t = fl / t / 1e12 if t else 0.0
         ach_b = by / t / 1e9 if t else 0.0
         out.append({"model": m, "gpulet_pct": ln["size"], "sm": ln["sm"], "planned_batch": ln["batch"],
@@ -530,8 +651,10 @@ def lane_util(srv, wins):
                     "mean_batch": round(r / b, 2) if b else 0.0, "mean_batch_us": round(t / b * 1e6, 1) if b else 0.0,
                     "tflops": round(ach_t, 2), "tensor_frac": round(ach_t / peak_t, 4) if peak_t else 0.0,
                     "tensor_peak_tflops": round(peak_t, 1), "gbs": round(ach_b, 1),
-                    "hbm_frac": round(ach_b / hbm, 4), "hbm_peak_gbs": hbm,
-                    "peak_source": f"{src}: SM-share of the sustained bf16 peak (kernel inside a long run); HBM copy"})
+                    "hbm_frac": round(ach_b / hbm_l, 4), "hbm_peak_gbs": hbm_l,
+                    "peak_source": f"{src}: SM-share of the sustained bf16 peak (kernel inside a long run); HBM: "
+                                   + (f"K12 copy probe on the gpu-let's {ln['sm']} SMs" if bw else
+                                      "whole-GPU copy peak (no K12 probe file)")})
     return out
 
 
@@ -600,6 +723,10 @@ def roofline(ctx, srv, lanes):
             "peak_source": f"{src} (MEASURED_PEAKS.json, burst: kernel timed alone)"}
 
 
+MATRIX_SCENARIOS = ("game", "traffic", "equal", "long-only", "short-skew", "mix6")
+MATRIX_MODES = ("gpulet", "gpulet+int", "sbp")
+
+
 def our_arm(a, world, rank, local, dist):
     import torch
     from paper_2109_01611_b200 import gpulet
@@ -607,48 +734,61 @@ def our_arm(a, world, rank, local, dist):
 
     torch.cuda.set_device(local)
     ctx = gpulet.Context(local + 1)
-    srv = Server(ctx, local, a.e2e)
-    slo = srv.slo
-    head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, timed=True, clocks=True)
-    extra = {}
+    srv = Server(ctx, local, a.e2e, slo_mode=a.slo_mode)
+    head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, clocks=True)
+    matrix = {}
     if not a.headline_only:
-        other = "gpulet+int" if a.mode == "gpulet" else "gpulet"
-        for key, scen, mode in (("baseline_sbp", a.scenario, "sbp"), (other.replace("+", "_"), a.scenario, other),
-                                ("traffic", "traffic", a.mode), ("traffic_baseline_sbp", "traffic", "sbp"),
-                                ("long_only", "long-only", a.mode), ("long_only_baseline_sbp", "long-only", "sbp"),
-                                ("mix6", "mix6", a.mode), ("mix6_baseline_sbp", "mix6", "sbp")):
-            r = run_mode(srv, dist, rank, world, scen, mode, a, timed=False)
-            extra[key] = {"value": round(r["value"], 2), "scenario": scen, "mode": mode,
-                          "rate_multiplier": round(r["x"], 4), "x_sched": round(r["x_sched"], 4),
-                          "rates_req_s": r["rates"], "viol_frac": round(r.get("viol_frac", 1.0), 4),
-                          "lanes": r.get("lanes", []), "note": r.get("note")}
+        # the same kernels and frontend under every scheduler (gpu-lets with and
+        # without the interference model vs whole-GPU temporal sharing),
+        # every scenario, both SLO readings (C4.2: rule / Table constants)
+        for slo_mode in ("rule", "table"):
+            srv.set_slo_mode(slo_mode)
+            for scen in MATRIX_SCENARIOS:
+                for mode in MATRIX_MODES:
+                    if (slo_mode, scen, mode) == (a.slo_mode, a.scenario, a.mode):
+                        continue
+                    r = quick_mode(srv, dist, rank, world, scen, mode, a)
+                    matrix[f"{slo_mode}/{scen}/{mode}"] = r
+                    log(f"matrix {slo_mode}/{scen}/{mode}: {r.get('value')}")
+        srv.set_slo_mode(a.slo_mode)
     roof = roofline_serving(head.get("lane_util")) if rank == 0 else None
-    roof1 = roofline(ctx, srv, head.get("lanes", [])) if rank == 0 else None
+    roof1 = roofline(ctx, srv, head.get("lanes", [])) if rank == 0 and head.get("lanes") else None
     if rank != 0:
         ctx.close()
         return None
     rates = head["rates"]
+    slo = srv.slo
     app = rates[2] if a.scenario == "game" else None
+    sched_ok = {}
+    for k, v in matrix.items():
+        sm, sc, mo = k.split("/")
+        if v.get("value"):
+            sched_ok.setdefault(f"{sm}/{mo}", []).append(sc)
     line = {
-        "metric": METRIC, "value": round(head["value"], 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "metric": METRIC, "value": round(head["value"], 2) if head.get("value") is not None else None,
+        "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(1000 * head.get("serve_s", 0.0) / max(head.get("windows", 1), 1), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": (f"cfg4 {a.scenario}: paper game (6 LeNet-5 + 1 ResNet-50 per app request, P:787), "
                                 if a.scenario == "game" else f"cfg4 {a.scenario}, ")
-                   + f"max Poisson rate with <=1% SLO violations, mode {a.mode}, gpu-lets on {world} GPU(s)",
+                   + f"max Poisson rate with <=1% SLO violations in every timed run, mode {a.mode}, "
+                   + f"SLOs {a.slo_mode}, gpu-lets on {world} GPU(s)",
                    "rate_multiplier": round(head["x"], 4), "x_sched_max": round(head["x_sched"], 4),
-                   "rates_req_s": rates, "app_req_s": app, "slo_us": slo, "lanes": head.get("lanes", []),
-                   "window_s": a.window, "arrivals": head.get("arrivals"),
-                   "slo_satisfied_frac": round(1 - head.get("viol_frac", 1.0), 4), "probes": head["probes"],
-                   "per_model": head.get("per_model"),
+                   "rates_req_s": rates, "app_req_s": app, "slo_us": slo, "slo_mode": a.slo_mode,
+                   "lanes": head.get("lanes", []), "window_s": a.window, "arrivals": head.get("arrivals"),
+                   "slo_satisfied_frac": round(1 - head.get("viol_frac", 1.0), 4),
+                   "criterion_met": head.get("criterion_met"), "repeats": head.get("repeats"),
+                   "spread": head.get("spread"), "attempts": head.get("attempts"), "probes": head["probes"],
+                   "per_model": head.get("per_model"), "note": head.get("note"),
                    "l2_flush": "none: inputs resident; six models' weights (~0.58 GB) exceed L2 between batches",
                    "parallelism": f"dp{world} (gpu-lets placed on {world} GPU(s) by the scheduler)"},
         "gpu_launches": len({ln["gpulet"] for ln in head.get("lanes", [])}),
         "gpu_launches_note": "persistent executors serving the timed windows (launched at gpu-let creation)",
         "roofline": roof, "roofline_oneshot_148sm": roof1, "gpulets": head.get("lane_util"),
         "clocks": head.get("clocks"), "e2e": head.get("e2e"),
+        "matrix": matrix,
+        "matrix_schedulable": {k: sorted(v) for k, v in sched_ok.items()},
     }
-    line.update(extra)
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample()
     ctx.close()
@@ -661,11 +801,16 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="gpulet", choices=["gpulet", "gpulet+int", "sbp"])
+    ap.add_argument("--mode", default="gpulet", choices=["gpulet", "gpulet+int", "sbp", "sbp50"])
     ap.add_argument("--scenario", default="game")
     ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
-    ap.add_argument("--probe-window", type=float, default=0.3, help="seconds per probe run (3 runs per probe)")
+    ap.add_argument("--repeats", type=int, default=3, help="timed runs of --steps windows (value = the median)")
+    ap.add_argument("--retries", type=int, default=4, help="x lowered by 4 %% while a timed run violates > 1 %%")
+    ap.add_argument("--probe-window", type=float, default=0.5, help="seconds per probe run (3 runs per probe)")
     ap.add_argument("--probes", type=int, default=6)
+    ap.add_argument("--slo-mode", default="rule", choices=["rule", "table"])
+    ap.add_argument("--matrix-window", type=float, default=0.25, help="seconds per matrix probe (1 run)")
+    ap.add_argument("--matrix-probes", type=int, default=5)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--headline-only", action="store_true")

@@ -130,6 +130,25 @@ gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completio
 gl_status gl_profile(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t batch, int32_t warmup, int32_t reps,
                      const void* in_dev, void* out_dev, double* median_us);
 
+/* K12 HBM probe (the per-gpu-let HBM roof BW(n) is measured, not
+ * assumed to be n/148 of the GPU's): a 16-B grid-stride copy of `bytes` (>= 1 MiB)
+ * device buffer to another, 4 CTAs x 512 threads per SM, launched on the green
+ * context of a slot-0 gpu-let of sm_pct (100 = the whole GPU); best of `reps` runs
+ * after one warm-up, host-timed around a stream synchronize (use >= 256 MiB so the
+ * few-µs launch/sync overhead is < 1 %).  Out: *gbs = read + write bytes / s / 1e9;
+ * *sm_count (optional) = SMs it ran on.  The GPU must have no live gpu-let
+ * (GL_E_STATE).  Errors: GL_E_ARG, GL_E_GRID, GL_E_STATE, GL_E_CUDA. */
+gl_status gl_bw_probe(gl_ctx* ctx, int gpu, int sm_pct, int64_t bytes, int32_t reps, double* gbs, int32_t* sm_count);
+
+/* Executor floor: `warmup` + `reps` descriptors with an empty
+ * program (no layer step) through gpulet_id's ring, one in flight, as gl_profile
+ * measures a batch.  Out: *host_us = median submit -> completion visible to the
+ * host (µs); *device_us (optional) = median start -> end stamps (the start barrier
+ * and the completion write).  Needs a model loaded on the gpu-let's GPU (its
+ * program pointer is carried but not run).  Errors: GL_E_ARG, GL_E_MODEL,
+ * GL_E_QUEUE_FULL, GL_E_TIMEOUT. */
+gl_status gl_floor(gl_ctx* ctx, int32_t gpulet_id, int32_t warmup, int32_t reps, double* host_us, double* device_us);
+
 /* One-shot executor launch (blocking) of one batch on n_sm CTAs (whole GPU, no
  * green context): for ncu capture and per-step tracing.  trace_ns (host, cap
  * entries, optional) receives %globaltimer at program start and after each step

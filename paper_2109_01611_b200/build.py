@@ -23,6 +23,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 SOURCES = [
     ("executor.cu", []),
     ("detect.cu", []),
+    ("probe.cu", []),
     ("runtime.cpp", []),
     ("models.cpp", []),
     ("frontend.cpp", []),

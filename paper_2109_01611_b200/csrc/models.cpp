@@ -41,6 +41,7 @@ static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 struct WRef {
   void* ptr = nullptr;
   int rows = 0, K_real = 0, K_pad = 0;
+  int K_alg = 0;  // the method's reduction length (kh * kw * real input channels): FLOP / weight accounting
 };
 
 struct Err {
@@ -65,6 +66,7 @@ static WRef conv_weight(DevWeights& dw, const ParamMap& P, const std::string& na
   r.rows = co;
   r.K_real = kh * kw * cin_pad;
   r.K_pad = rup(r.K_real, 64);
+  r.K_alg = kh * kw * ci;
   auto f = dw.ptr.find(key);
   if (f != dw.ptr.end()) {
     r.ptr = f->second;
@@ -98,6 +100,7 @@ static WRef conv_weight_s2d(DevWeights& dw, const ParamMap& P, const std::string
   r.rows = co;
   r.K_real = Kp * Kp * C4;
   r.K_pad = rup(r.K_real, 64);
+  r.K_alg = K * K * ci;
   const std::string key = name + "#s2d" + std::to_string(cin_pad);
   auto f = dw.ptr.find(key);
   if (f != dw.ptr.end()) {
@@ -136,6 +139,7 @@ static WRef conv_weight_kwpack(DevWeights& dw, const ParamMap& P, const std::str
   r.rows = co;
   r.K_real = K * cpk;
   r.K_pad = rup(r.K_real, 64);
+  r.K_alg = K * K * ci;
   const std::string key = name + "#kwp" + std::to_string(cpk);
   auto f = dw.ptr.find(key);
   if (f != dw.ptr.end()) {
@@ -165,6 +169,7 @@ static WRef fc_weight(DevWeights& dw, const ParamMap& P, const std::string& name
   r.rows = p.shape[0];
   r.K_real = p.shape[1];
   r.K_pad = rup(r.K_real, 64);
+  r.K_alg = r.K_real;
   const std::string key = name + "#fc";
   auto f = dw.ptr.find(key);
   if (f != dw.ptr.end()) {
@@ -368,8 +373,9 @@ class Builder {
     op.pf_addr = (uint64_t)(uintptr_t)w.ptr;
     op.pf_bytes = (uint64_t)w.rows * w.K_pad * 2;
     finish_gemm(op);
-    prog.flops += 2.0 * M * g.N * (double)w.K_real;
-    prog.weight_bytes += (double)w.rows * w.K_real * 2;
+    // the method's FLOPs / weight bytes (real K: no padded channels, no zero taps of the re-layouts)
+    prog.flops += 2.0 * M * g.N * (double)w.K_alg;
+    prog.weight_bytes += (double)w.rows * w.K_alg * 2;
   }
 
   // Swap-AB linear for small batches: weights are the M operand (TMA), the
@@ -402,8 +408,8 @@ class Builder {
     op.pf_addr = (uint64_t)(uintptr_t)w.ptr;
     op.pf_bytes = (uint64_t)w.rows * w.K_pad * 2;
     finish_gemm(op);
-    prog.flops += 2.0 * nrows * g.M * (double)w.K_real;
-    prog.weight_bytes += (double)w.rows * w.K_real * 2;
+    prog.flops += 2.0 * nrows * g.M * (double)w.K_alg;
+    prog.weight_bytes += (double)w.rows * w.K_alg * 2;
   }
 
   // UMMA N tile: the widest balanced tile (<= 256 columns) that still gives

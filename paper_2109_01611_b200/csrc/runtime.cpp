@@ -29,6 +29,7 @@
 #include "runtime.h"
 
 extern "C" cudaKernel_t gl_executor_handle();
+extern "C" cudaKernel_t gl_probe_handle();
 extern "C" const void* gl_executor_fn();
 
 namespace gl {
@@ -844,8 +845,17 @@ gl_status gl_gpulet_smids(gl_ctx* ctx, int32_t id, int32_t* smids, int32_t cap, 
   return GL_OK;
 }
 
+static gl_status submit_impl(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_dev, void* out_dev,
+                             int32_t batch, float slo_ms, uint64_t* ticket, bool empty);
+
 gl_status gl_submit_batch(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_dev, void* out_dev, int32_t batch,
                           float slo_ms, uint64_t* ticket) {
+  return submit_impl(ctx, gid, mid, in_dev, out_dev, batch, slo_ms, ticket, false);
+}
+
+// empty: a descriptor whose program has no step (the executor floor, gl_floor)
+static gl_status submit_impl(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_dev, void* out_dev,
+                             int32_t batch, float slo_ms, uint64_t* ticket, bool empty) {
   if (!ctx || gid < 0 || gid >= (int)ctx->gpulets.size() || !in_dev || !out_dev)
     return fail(GL_E_ARG, "gl_submit_batch: bad arguments");
   if (batch < 1 || batch > 32) return fail(GL_E_CAPACITY, "gl_submit_batch: batch outside [1,32]");
@@ -873,7 +883,7 @@ gl_status gl_submit_batch(gl_ctx* ctx, int32_t gid, int32_t mid, const void* in_
   w.prog = prog;
   w.in = in_dev;
   w.out = out_dev;
-  w.n_ops = n_ops;
+  w.n_ops = empty ? 0 : n_ops;
   w.model = mid;
   w.batch = batch;
   w.slo_us = (int32_t)(slo_ms * 1000.0f);
@@ -996,6 +1006,51 @@ gl_status gl_profile(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32
   return GL_OK;
 }
 
+gl_status gl_floor(gl_ctx* ctx, int32_t gid, int32_t warmup, int32_t reps, double* host_us, double* device_us) {
+  // the executor's fixed service cost (SURVEY §8(d) cfg1 "executor floor"): a
+  // descriptor with an empty program through the same ring, dequeue, start
+  // barrier and completion path as gl_profile
+  if (!ctx || !host_us || reps < 1 || warmup < 0 || gid < 0 || gid >= (int)ctx->gpulets.size() ||
+      !ctx->gpulets[gid] || !ctx->gpulets[gid]->alive)
+    return fail(GL_E_ARG, "gl_floor: bad arguments");
+  Gpulet& g = *ctx->gpulets[gid];
+  int mid = -1;
+  for (int i = 0; i < (int)ctx->models.size() && mid < 0; ++i)
+    if (ctx->models[i] && ctx->models[i]->gpu == g.gpu) mid = i;
+  if (mid < 0) return fail(GL_E_MODEL, "gl_floor: no model loaded on the gpu-let's GPU");
+  std::vector<double> lat, dev;
+  for (int i = 0; i < warmup + reps; ++i) {
+    uint64_t t;
+    const gl_status s = submit_impl(ctx, gid, mid, g.ws, g.ws, 1, 0.f, &t, true);
+    if (s) return s;
+    const uint64_t t_sub = now_ns();
+    const auto t0 = std::chrono::steady_clock::now();
+    bool done = false;
+    while (!done) {
+      gl_completion c[64];
+      const int n = collect(ctx, c, 64);
+      for (int k = 0; k < n; ++k) {
+        if (c[k].ticket == t) {
+          done = true;
+          if (i >= warmup) {
+            lat.push_back((now_ns() - t_sub) / 1000.0);
+            dev.push_back((c[k].t_end_ns - c[k].t_start_ns) / 1000.0);
+          }
+        } else {
+          ctx->stash.push_back(c[k]);
+        }
+      }
+      if (!done && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        return fail(GL_E_TIMEOUT, "gl_floor: timeout");
+    }
+  }
+  std::sort(lat.begin(), lat.end());
+  std::sort(dev.begin(), dev.end());
+  *host_us = lat[lat.size() / 2];
+  if (device_us) *device_us = dev[dev.size() / 2];
+  return GL_OK;
+}
+
 gl_status gl_test_gemm(gl_ctx* ctx, int gpu, const void* A, const uint16_t* W, const uint16_t* bias, void* out,
                        int32_t M, int32_t N, int32_t K, int32_t act, int32_t swap_ab, int32_t splitk, int32_t out_fp32,
                        int32_t a_in_ws) {
@@ -1030,6 +1085,69 @@ gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* 
   if (tl_per_cta) *tl_per_cta = g_test_tl_cap;
   if (timeline)
     for (int i = 0; i < cap && i < (int)g_test_tl.size(); ++i) timeline[i] = g_test_tl[i];
+  return GL_OK;
+}
+
+// K12 HBM probe on the SMs of a gpu-let size (include/gpulet.h gl_bw_probe).
+gl_status gl_bw_probe(gl_ctx* ctx, int gpu, int sm_pct, int64_t bytes, int32_t reps, double* gbs, int32_t* sm_count) {
+  if (!ctx || gpu < 0 || gpu >= (int)ctx->gpus.size() || !gbs || bytes < (1 << 20) || reps < 1)
+    return fail(GL_E_ARG, "gl_bw_probe: bad arguments");
+  if (sm_pct != 100 && grid_index(sm_pct) < 0) return fail(GL_E_GRID, "gl_bw_probe: sm_pct off the grid");
+  GpuState& G = ctx->gpus[gpu];
+  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_bw_probe: the GPU has live gpu-lets");
+  CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  if (!G.green_ready) {
+    gl_status rc = prepare_green(ctx, G);
+    if (rc) return rc;
+  }
+  CUstream st = G.full_stream;
+  int nsm = G.nsm;
+  if (sm_pct != 100) {
+    const int gi = grid_index(sm_pct);
+    gl_status rc = ensure_green(ctx, G, 0, gi);
+    if (rc) return rc;
+    st = G.gstream[0][gi];
+    nsm = G.gnsm[0][gi];
+  }
+  Driver& D = driver();
+  CUkernel k = (CUkernel)gl_probe_handle();
+  if (!k) return fail(GL_E_CUDA, "cudaGetKernel(bw_copy) failed");
+  const int64_t n16 = bytes / 16;
+  char *src = nullptr, *dst = nullptr;
+  CK(cudaMalloc(&src, (size_t)n16 * 16), "cudaMalloc(probe src)");
+  CK(cudaMalloc(&dst, (size_t)n16 * 16), "cudaMalloc(probe dst)");
+  CK(cudaMemset(src, 1, (size_t)n16 * 16), "memset");
+  CK(cudaDeviceSynchronize(), "sync");
+  CUlaunchConfig cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = nsm * 4;   // 4 CTAs of 512 threads per SM: 64 warps, the SM's full occupancy
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = 512;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.hStream = st;
+  int64_t n = n16;
+  void* args[] = {&src, &dst, &n};
+  double best = 0.0;
+  gl_status rc = GL_OK;
+  for (int it = 0; it < reps + 1 && !rc; ++it) {   // the first run warms up
+    const auto t0 = std::chrono::steady_clock::now();
+    CUresult r = D.launchKernelEx(&cfg, (CUfunction)k, args, nullptr);
+    if (r != CUDA_SUCCESS) {
+      rc = cu_check(ctx, r, "cuLaunchKernelEx(bw_copy)");
+      break;
+    }
+    if (cudaStreamSynchronize((cudaStream_t)st) != cudaSuccess) {
+      rc = fail(GL_E_CUDA, "gl_bw_probe: sync");
+      break;
+    }
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (it > 0) best = std::max(best, 2.0 * (double)n16 * 16 / s / 1e9);
+  }
+  cudaFree(src);
+  cudaFree(dst);
+  if (rc) return rc;
+  *gbs = best;
+  if (sm_count) *sm_count = nsm;
   return GL_OK;
 }
 

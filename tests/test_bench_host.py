@@ -10,8 +10,14 @@ import bench
 class FakeServer:
     """Violations jump above 1 % once x exceeds `cap`; records the probes."""
 
+    slo_mode = "rule"
+
     def __init__(self, cap):
         self.cap, self.lanes, self.calls = cap, [], []
+        self.gpu = 0
+
+    def max_sched_x(self, scen, mode, world):
+        return 4.0
 
     def plan(self, scen, mode, world, x):
         return [100, 0, 10, 0, 0, 0], "dump", True
@@ -26,8 +32,10 @@ class FakeServer:
         x = self._x
         self.calls.append(x)
         arr = 10000
-        viol = 5 if x <= self.cap else 500
-        return {"arrivals": arr, "viol": viol, "per": {}}
+        cap = getattr(self, "cap_timed", self.cap) if secs == getattr(self, "timed_secs", None) else self.cap
+        viol = 5 if x <= cap else 500
+        return {"arrivals": arr, "viol": viol, "per": {}, "sat": arr - viol, "dev_s": secs, "wall_s": secs,
+                "lanes": []}
 
 
 def test_search_bisects_to_the_cap():
@@ -69,3 +77,22 @@ def test_poisson_trace_rates_and_order():
     n0, n2 = int((m == 0).sum()), int((m == 2).sum())
     assert abs(n0 - 4000) < 5 * np.sqrt(4000) and abs(n2 - 1000) < 5 * np.sqrt(1000)
     assert int((m == 1).sum()) == 0
+
+
+def test_timed_runs_enforce_the_rule():
+    """The probes pass at x but the timed windows (a tighter cap) violate: run_mode must
+    lower x until every timed run meets <= 1 %, value = the median run."""
+    a = types.SimpleNamespace(probes=12, probe_window=0.01, window=0.02, steps=2, warmup=0, repeats=3, retries=6,
+                              e2e=False)
+    srv = FakeServer(cap=1.37)
+    srv.cap_timed, srv.timed_secs = 1.2, 0.02     # the timed windows see a lower capacity than the probes
+    orig = srv.plan
+
+    def plan(scen, mode, world, x):
+        srv._x = x
+        return orig(scen, mode, world, x)
+    srv.plan = plan
+    r = bench.run_mode(srv, None, 0, 1, "game", "gpulet", a)
+    assert r["criterion_met"] and r["x"] <= 1.2
+    assert all(v["viol_frac"] <= 0.01 for v in r["repeats"]) and len(r["repeats"]) == 3
+    assert len(r["attempts"]) >= 2 and max(r["attempts"][0]["viol_frac"]) > 0.01

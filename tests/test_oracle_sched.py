@@ -262,17 +262,50 @@ def test_elastic_implies_brute_force():
     assert gaps <= 25
 
 
+def _worked_profile(names):
+    fns = {"W2": W2, "WB": WB}
+    return prof_from([fns[n] for n in names]), None
+
+
+def test_sbp_and_ideal_worked_examples():
+    """Hand-derived SBP / SBP-on-50:50 / ideal plans (tests/golden/sched_sbp_ideal_worked.json,
+    each with its derivation): the oracle reproduces every dump byte for byte."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sched_sbp_ideal_worked.json")) as f:
+        gold = json.load(f)
+    for case in gold["cases"]:
+        P, _ = _worked_profile(case["profile"])
+        P.names = ["A", "B"][:len(case["profile"])]
+        if case["mode"] == "ideal":
+            plan = sched.ideal(P, case["slo"], case["rates"], case["gpus"], "gpulet+int", (0, 0, 0, 0, 0))
+        else:
+            plan = sched.schedule(P, case["slo"], case["rates"], case["gpus"], case["mode"])
+        assert plan.dump == "\n".join(case["dump"]) + "\n", case["name"]
+
+
 def test_ideal_dominates_on_tiny():
+    """Any instance Alg. 1 schedules with its split at a layout of the ideal's grid is
+    also schedulable by the ideal (it tries that layout); on random tiny instances the
+    ideal's verdict is at least the elastic one whenever the elastic plan's layout is
+    one of {100}, {20,80}, {40,60}, {50,50}."""
     rnd = random.Random(13)
-    for _ in range(15):
+    checked = 0
+    for _ in range(40):
         M, N = rnd.randint(1, 3), rnd.randint(1, 2)
         P, slo = _random_instance(rnd, M)
         S = Scheduler(P, slo, None, "gpulet")
         rates = [rnd.randint(1, 2 * max(1, S.cap(m, 100))) for m in range(M)]
-        if sched.schedule(P, slo, rates, N, "gpulet").ok:
-            # ideal explores the fixed layouts; elastic split sizes are a subset
-            # for single-split layouts only, so only check that ideal runs.
-            sched.ideal(P, slo, rates, N, "gpulet")
+        plan = sched.schedule(P, slo, rates, N, "gpulet")
+        if not plan.ok:
+            continue
+        sizes = {}
+        for g in plan.gpulets:
+            sizes.setdefault(g.gpu, []).append(g.size)
+        if all(tuple(sorted(v)) in {(100,), (20, 80), (40, 60), (50, 50)} for v in sizes.values()):
+            assert sched.ideal(P, slo, rates, N, "gpulet+int", (0, 0, 0, 0, 0)).ok
+            checked += 1
+    assert checked >= 5
 
 
 def test_layout_count():

@@ -89,3 +89,19 @@ def test_fit_interference_matches_oracle():
     np.testing.assert_allclose(gpulet.fit_interference(X, y), interf.fit(X, y), rtol=1e-9, atol=1e-12)
     with pytest.raises(gpulet.GpuletError):
         gpulet.fit_interference(np.tile(X[:1], (50, 1)), np.ones(50))
+
+
+def test_native_reproduces_worked_sbp_ideal_examples():
+    """The hand-derived plans of tests/golden/sched_sbp_ideal_worked.json, through gl_schedule."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sched_sbp_ideal_worked.json")) as f:
+        gold = json.load(f)
+    fns = {"W2": W2, "WB": WB}
+    for case in gold["cases"]:
+        P = prof_from([fns[n] for n in case["profile"]])
+        names = ["A", "B"][:len(case["profile"])]
+        dump, ok = gpulet.schedule(names, P.lat, None, None, case["slo"], case["rates"], case["gpus"], case["mode"],
+                                   (0, 0, 0, 0, 0))
+        assert dump == "\n".join(case["dump"]) + "\n", case["name"]
+        assert ok == ('"Schedulable"' in case["dump"][-1])
