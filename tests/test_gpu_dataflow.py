@@ -18,7 +18,7 @@ from oracle import models as om
 from paper_2109_01611_b200 import gpulet
 from tools import common
 from tests.gpu_util import rel_err, REL_TOL
-gpulet.set_tuning(6, 2)   # dataflow joins + plan log
+gpulet.Context.set_tuning(6, 2)   # dataflow joins + plan log
 ctx = gpulet.Context(1)
 for m, b in (("resnet50", 3), ("vgg16", 2)):
     mid = ctx.load_model(0, m, synthgen.weight_file(m))
