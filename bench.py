@@ -345,7 +345,7 @@ class Server:
                 break
         return lo
 
-    def setup(self, dump, rank, reuse=False):
+    def setup(self, dump, rank, reuse=False, unconfined=False):
         """Create this GPU's gpu-lets of the plan and build its lanes; returns
         the per-model arrival rates this rank must serve.  reuse: when the plan
         keeps this GPU's gpu-let sizes, keep the live gpu-lets and only re-plan
@@ -362,7 +362,7 @@ class Server:
         else:
             self.teardown()
             self.reorganised = True
-            made = self.ctx.create_gpulets(self.gpu, sizes) if used else []
+            made = self.ctx.create_gpulets(self.gpu, sizes, unconfined) if used else []
             self.made = [gid for gid, _n in made]
             self.made_sizes, self.made_nsm = sizes, [n for _g, n in made]
             for p, (_gid, n) in zip(sizes, made):

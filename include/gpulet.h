@@ -75,7 +75,9 @@ gl_status gl_load_model(gl_ctx* ctx, int gpu, int kind, const char* weight_file,
 /* Bytes of the model's input and output buffers at `batch`.  Input layouts:
  * LeNet NHWC bf16 [b,28,28,1]; GoogLeNet/ResNet-50/VGG-16 NHWC bf16 [b,224,224,8]
  * (channels 3..7 zero); SSD NHWC bf16 [b,300,300,8]; BERT int32 ids [b,128].
- * Outputs fp32: [b,classes]; SSD loc [b,3000,4] followed by conf [b,3000,21]. */
+ * Outputs fp32: [b,classes]; SSD loc [b,3000,4] followed by conf [b,3000,21]; BERT
+ * logits [b,2] followed, at byte offset roundup(8b, 16), by the pooled [CLS] vector
+ * (tanh pooler output, P:741 BERT-base) bf16 [b,768]. */
 gl_status gl_model_io(gl_ctx* ctx, int32_t model_id, int32_t batch, int64_t* in_bytes, int64_t* out_bytes);
 /* Algorithmic FLOPs and weight bytes of one batch (for roofline accounting). */
 gl_status gl_model_cost(gl_ctx* ctx, int32_t model_id, int32_t batch, double* flops, double* weight_bytes);
@@ -98,6 +100,16 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int sm_pct, int32_t* gpulet_id,
  * the way to (re)partition a GPU).  The GPU must have no live gpu-let (GL_E_STATE).
  * Out: ids[n], sm_counts[n] (optional). */
 gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids, int32_t* sm_counts);
+/* The unpartitioned-concurrency baseline (Fig.
+ * slo-violation "MPS(default)": concurrent kernels with no static SM partition): the same
+ * executors as gl_create_gpulets, on the primary context (one non-blocking stream per
+ * slot), no green context and no SM confinement -- executor i runs 2 * round(p_i * SMs /
+ * 200) CTAs that the hardware block scheduler places on whatever SMs are free (one
+ * executor CTA fills an SM, so the CTA counts, not SM sets, are what is fixed), with the
+ * programs tiled for that CTA count.  pcts in {20,40,50,60,80}, n in {1,2}, sum <= 100;
+ * gl_gpulet_smids reports where the CTAs landed.  Errors: as gl_create_gpulets. */
+gl_status gl_create_gpulets_unconfined(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids,
+                                       int32_t* sm_counts);
 /* Drain and stop a gpu-let's executor; its slot becomes free. */
 gl_status gl_destroy_gpulet(gl_ctx* ctx, int32_t gpulet_id);
 /* %smid of every executor CTA (confinement audit); *n = number written. */

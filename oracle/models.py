@@ -172,7 +172,7 @@ def bert_base(P, ids):
         x = R(nn.layernorm(y, P[pre + ".ln2.g"], P[pre + ".ln2.b"]))
     cls = x.reshape(b, S, BERT_H)[:, 0]
     pooled = R(np.tanh(P.fc(cls, "pool")))
-    return {"logits": nn.rf32(P.fc(pooled, "cls"))}
+    return {"logits": nn.rf32(P.fc(pooled, "cls")), "pooled": pooled}
 
 
 FORWARD = {"lenet5": lenet5, "googlenet": googlenet, "resnet50": resnet50,

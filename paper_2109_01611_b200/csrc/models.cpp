@@ -1074,11 +1074,21 @@ static void build_bert(Builder& B, size_t& in_b, size_t& out_b) {
   B.step();
   B.flush_finals();
   B.fc_swap(pooled.ref, b, H, H, "cls", ACT_NONE, out_ref(0), 1);
-  B.release(pooled);
   B.step();
   B.flush_finals();
+  // the pooled [CLS] vector (bf16 [b,768]) follows the logits at the next 16-B
+  // boundary, so parity can check the 768-d representation and not only 2 logits
+  const uint64_t pool_off = ((uint64_t)b * 2 * 4 + 15) / 16 * 16;
+  {
+    OpDesc& op = B.add(OP_COPY);
+    op.m.x = pooled.ref, op.m.y = out_ref(pool_off);
+    op.m.rows = b * H * 2 / 16;
+    op.n_units = 1;
+    B.step();
+  }
+  B.release(pooled);
   in_b = (size_t)b * S * 4;
-  out_b = (size_t)b * 2 * 4;
+  out_b = pool_off + (size_t)b * H * 2;
 }
 
 // ------------------------------------------------------------------ barrier-free GEMM step joins

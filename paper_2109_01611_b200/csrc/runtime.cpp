@@ -198,6 +198,7 @@ struct Gpulet {
   uint64_t comp_seen = 0;  // completions consumed by the host
   std::vector<int> groups;
   bool uses_rem = false;
+  bool unconfined = false;  // primary context, no green context (F4 "MPS(default)" analogue)
 };
 
 // Upload a program bound to workspace `ws` (tensor maps of workspace operands).
@@ -243,6 +244,7 @@ struct GpuState {
   CUstream gstream[2][5] = {};
   int gnsm[2][5] = {};
   CUstream full_stream = nullptr;  // 100 %: a non-blocking stream of the primary context
+  CUstream ustream[2] = {};        // unconfined executors: one non-blocking primary stream per slot
   int dev = 0;
   int nsm = 0;
   bool split = false;
@@ -548,6 +550,8 @@ gl_status gl_shutdown(gl_ctx* ctx) {
     if (G.green_ready) {
       drop_green(G);
       if (G.full_stream) cudaStreamDestroy((cudaStream_t)G.full_stream);
+      for (auto& us : G.ustream)
+        if (us) cudaStreamDestroy((cudaStream_t)us), us = nullptr;
       G.green_ready = false;
     }
     for (auto& R : G.slot_res) {
@@ -690,7 +694,13 @@ static void bind_sized(gl_ctx* ctx, GpuState& G, int gpu, int slot, int nsm) {
   }
 }
 
+static gl_status create_gpulet(gl_ctx* ctx, int gpu, int pct, bool unconfined, int32_t* gpulet_id, int32_t* sm_count);
+
 gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, int32_t* sm_count) {
+  return create_gpulet(ctx, gpu, pct, false, gpulet_id, sm_count);
+}
+
+static gl_status create_gpulet(gl_ctx* ctx, int gpu, int pct, bool unconfined, int32_t* gpulet_id, int32_t* sm_count) {
   if (!ctx || !gpulet_id || gpu < 0 || gpu >= (int)ctx->gpus.size()) return fail(GL_E_ARG, "gl_create_gpulet: bad arguments");
   if (sm_for_pct(pct) < 0) return fail(GL_E_GRID, "gl_create_gpulet: sm_pct not in {20,40,50,60,80,100}");
   if (ctx->poisoned) return fail(GL_E_CUDA, "context poisoned by an earlier CUDA error");
@@ -722,6 +732,18 @@ gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, in
     g->stream = G.full_stream;
     g->own_primary_stream = true;
     g->nsm = G.nsm;
+  } else if (unconfined) {
+    // the same executor on the primary context: sm_for_pct CTAs that the
+    // hardware block scheduler places on any free SMs (no SM confinement)
+    if (!G.ustream[slot]) {
+      cudaStream_t s;
+      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "unconfined stream");
+      G.ustream[slot] = (CUstream)s;
+    }
+    g->stream = G.ustream[slot];
+    g->own_primary_stream = true;
+    g->unconfined = true;
+    g->nsm = sm_for_pct(pct, G.nsm);
   } else {
     const int gi = grid_index(pct);
     gl_status rc = ensure_green(ctx, G, slot, gi);
@@ -1310,6 +1332,39 @@ extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const in
   for (int i = 0; i < n; ++i) {
     int32_t sm = 0;
     gl_status rc = gl_create_gpulet(ctx, gpu, pcts[i], &ids[i], &sm);
+    if (rc) return rc;
+    if (sm_counts) sm_counts[i] = sm;
+  }
+  return GL_OK;
+}
+
+extern "C" gl_status gl_create_gpulets_unconfined(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids,
+                                                  int32_t* sm_counts) {
+  if (!ctx || !pcts || !ids || n < 1 || n > 2 || gpu < 0 || gpu >= (int)ctx->gpus.size())
+    return fail(GL_E_ARG, "gl_create_gpulets_unconfined: bad arguments");
+  GpuState& G = ctx->gpus[gpu];
+  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_create_gpulets_unconfined: GPU has live gpu-lets");
+  int sum = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sm_for_pct(pcts[i]) < 0 || pcts[i] == 100)
+      return fail(GL_E_GRID, "gl_create_gpulets_unconfined: sm_pct not in {20,40,50,60,80}");
+    sum += pcts[i];
+  }
+  if (sum > 100) return fail(GL_E_PARTITION, "gl_create_gpulets_unconfined: sizes sum to more than 100");
+  CK(cudaSetDevice(G.dev), "cudaSetDevice");
+  if (!G.green_ready) {
+    gl_status rc = prepare_green(ctx, G);
+    if (rc) return rc;
+  }
+  {
+    gl_status rc = ensure_slot_res(ctx, G, gpu);
+    if (rc) return rc;
+  }
+  for (int i = 0; i < n; ++i) bind_sized(ctx, G, gpu, i, sm_for_pct(pcts[i], G.nsm));
+  CK(cudaDeviceSynchronize(), "sized programs");
+  for (int i = 0; i < n; ++i) {
+    int32_t sm = 0;
+    gl_status rc = create_gpulet(ctx, gpu, pcts[i], true, &ids[i], &sm);
     if (rc) return rc;
     if (sm_counts) sm_counts[i] = sm;
   }

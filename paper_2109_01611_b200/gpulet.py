@@ -20,7 +20,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3, "sbp50": 4}
 
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
-           "gl_create_gpulet", "gl_create_gpulets", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
+           "gl_create_gpulet", "gl_create_gpulets", "gl_create_gpulets_unconfined", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
            "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_schedule", "gl_profile_load",
            "gl_workload_rates", "gl_schedule_files", "gl_bw_probe", "gl_floor", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
            "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
@@ -76,6 +76,8 @@ def lib():
             "gl_model_cost": [P, I32, I32, ctypes.POINTER(D), ctypes.POINTER(D)],
             "gl_create_gpulet": [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I32), ctypes.POINTER(I32)],
             "gl_create_gpulets": [P, ctypes.c_int, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)],
+            "gl_create_gpulets_unconfined": [P, ctypes.c_int, I32, ctypes.POINTER(I32), ctypes.POINTER(I32),
+                                             ctypes.POINTER(I32)],
             "gl_destroy_gpulet": [P, I32],
             "gl_gpulet_smids": [P, I32, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)],
             "gl_submit_batch": [P, I32, I32, P, P, I32, ctypes.c_float, ctypes.POINTER(U64)],
@@ -212,13 +214,15 @@ class Context:
         _check(lib().gl_create_gpulet(self.h, gpu, sm_pct, ctypes.byref(gid), ctypes.byref(n)))
         return gid.value, n.value
 
-    def create_gpulets(self, gpu, pcts):
-        """Partition a GPU into len(pcts) gpu-lets at once; returns [(id, sm_count)]."""
+    def create_gpulets(self, gpu, pcts, unconfined=False):
+        """Partition a GPU into len(pcts) gpu-lets at once; returns [(id, sm_count)].
+        unconfined: the F4 "MPS(default)" analogue (gl_create_gpulets_unconfined)."""
         n = len(pcts)
         p = (ctypes.c_int32 * n)(*pcts)
         ids = (ctypes.c_int32 * n)()
         sms = (ctypes.c_int32 * n)()
-        _check(lib().gl_create_gpulets(self.h, gpu, n, p, ids, sms))
+        fn = lib().gl_create_gpulets_unconfined if unconfined else lib().gl_create_gpulets
+        _check(fn(self.h, gpu, n, p, ids, sms))
         return [(ids[i], sms[i]) for i in range(n)]
 
     def destroy_gpulet(self, gid):

@@ -37,3 +37,20 @@ def top1_agreement(got, ref, tau):
     keep = gap > tau
     judged = float((a[keep] == b[keep]).mean()) if keep.any() else 1.0
     return strict, judged, float(1 - keep.mean())
+
+
+def split_outputs(model, y, b):
+    """The GPU output buffer of one batch (fp32 view, gl_model_io layout) as the
+    oracle's output dict: logits [b,classes]; SSD loc/conf; BERT logits and the
+    bf16 pooled [CLS] vector at byte offset roundup(8b, 16)."""
+    y = np.asarray(y)
+    if model == "ssd_mobilenet_v1":
+        yf = y.astype(np.float64)
+        return {"loc": yf[: b * 3000 * 4].reshape(b, 3000, 4),
+                "conf": yf[b * 3000 * 4: b * 3000 * 25].reshape(b, 3000, 21)}
+    if model == "bert_base":
+        y32 = np.ascontiguousarray(y, np.float32)
+        off = (b * 8 + 15) // 16 * 16
+        pooled = bits_to_f64(y32.view(np.uint16)[off // 2: off // 2 + b * 768]).reshape(b, 768)
+        return {"logits": y32[: 2 * b].astype(np.float64).reshape(b, 2), "pooled": pooled}
+    return {"logits": np.asarray(y, np.float64).reshape(b, -1)}

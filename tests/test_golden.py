@@ -124,3 +124,20 @@ def test_survey_W2_plans():
                 ln = g["lanes"][0]
                 assert (g["size"], ln["rate"], ln["batch"], ln["exec_us"]) == \
                     (c[k]["size"], c[k]["rate"], c[k]["batch"], c[k]["exec_us"])
+
+
+def test_top1_golden_files_match_oracle():
+    """tests/golden/top1_*.npz (scripts/make_top1_golden.py) exist for every model and
+    their first LeNet-5 batch equals a fresh oracle forward (the files are oracle output)."""
+    import numpy as np
+    import synthgen
+    from oracle import models as om
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    for m in synthgen.MODELS:
+        g = np.load(os.path.join(gdir, f"top1_{m}.npz"))
+        n = 1024 if m == "lenet5" else 256
+        assert len(g["batch_ids"]) * int(g["batch"]) == n
+    g = np.load(os.path.join(gdir, "top1_lenet5.npz"))
+    b = int(g["batch"])
+    ref = om.forward("lenet5", synthgen.weights("lenet5"), synthgen.model_input("lenet5", b, int(g["batch_ids"][0])))
+    assert np.array_equal(g["logits"][:b], ref["logits"].astype(np.float32))

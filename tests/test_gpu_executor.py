@@ -94,3 +94,27 @@ def test_corun_overlap(c):
     finally:
         c.destroy_gpulet(a)
         c.destroy_gpulet(b)
+
+
+def test_unconfined_pair_serves_and_places_one_cta_per_sm(c):
+    """F4 "MPS(default)" analogue (gl_create_gpulets_unconfined): two executors on the
+    primary context, CTA counts of the 20:80 split, placed by the hardware; each CTA
+    holds a whole SM, so the two CTA sets land on distinct SMs; both serve batches
+    that match the oracle."""
+    import torch
+    from oracle import models as omodels
+    (a, na), (b, nb) = c.create_gpulets(0, [20, 80], unconfined=True)
+    try:
+        assert (na, nb) == (30, 118)
+        sa, sb = c.gpulet_smids(a), c.gpulet_smids(b)
+        assert len(set(sa)) == na and len(set(sb)) == nb and not set(sa) & set(sb)
+        x = synthgen.model_input("lenet5", 8)
+        for gid in (a, b):
+            y = torch.empty(c.model_io(c.mid, 8)[1] // 4, device="cuda")
+            c.wait(c.submit_batch(gid, c.mid, to_dev_bf16(x), y, 8, 10.0))
+            ref = omodels.forward("lenet5", synthgen.weights("lenet5"), x)["logits"]
+            got = y.cpu().numpy().astype(np.float64).reshape(ref.shape)
+            assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
+    finally:
+        c.destroy_gpulet(a)
+        c.destroy_gpulet(b)

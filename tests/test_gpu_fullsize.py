@@ -9,7 +9,7 @@ import pytest
 
 import synthgen
 from oracle import models as omodels
-from tests.gpu_util import REL_TOL, rel_err
+from tests.gpu_util import REL_TOL, rel_err, split_outputs
 
 pytestmark = pytest.mark.gpu
 
@@ -32,19 +32,15 @@ def _run(c, gid, m, b, batch_id):
     xd = common.device_input(m, b, batch_id)
     y = torch.empty(c.model_io(c.mids[m], b)[1] // 4, device="cuda")
     c.wait(c.submit_batch(gid, c.mids[m], xd, y, b, 100.0))
-    return y.cpu().numpy().astype(np.float64)
+    return y.cpu().numpy()
 
 
 def _check(m, got, b, idx, batch_id):
     x = synthgen.model_input(m, b, batch_id)[list(idx)]
     ref = omodels.forward(m, synthgen.weights(m), x)
-    if m == "ssd_mobilenet_v1":
-        loc = got[: b * 3000 * 4].reshape(b, 3000, 4)[list(idx)]
-        conf = got[b * 3000 * 4:].reshape(b, 3000, 21)[list(idx)]
-        assert rel_err(loc, ref["loc"]) <= REL_TOL and rel_err(conf, ref["conf"]) <= REL_TOL
-    else:
-        g = got.reshape(b, -1)[list(idx)]
-        assert rel_err(g, ref["logits"].reshape(len(idx), -1)) <= REL_TOL, m
+    out = split_outputs(m, got, b)
+    for k in ref:
+        assert rel_err(out[k][list(idx)], ref[k].reshape(out[k][list(idx)].shape)) <= REL_TOL, (m, k)
 
 
 @pytest.mark.parametrize("m", ["googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"])

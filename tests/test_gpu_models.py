@@ -7,7 +7,7 @@ import pytest
 
 import synthgen
 from oracle import models as omodels
-from tests.gpu_util import REL_TOL, TOP1_TOL, rel_err, to_dev_bf16, top1_agreement
+from tests.gpu_util import REL_TOL, TOP1_TOL, rel_err, split_outputs, to_dev_bf16, top1_agreement
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,7 @@ def run_model(c, gid, mid, model, batch, batch_id=0):
     y = torch.empty(outb // 4, dtype=torch.float32, device="cuda")
     t = c.submit_batch(gid, mid, xd, y, batch, 100.0)
     comp = c.wait(t)
-    return x, y.cpu().numpy().astype(np.float64), comp
+    return x, y.cpu().numpy(), comp
 
 
 @pytest.mark.parametrize("model", synthgen.MODELS)
@@ -50,21 +50,22 @@ def test_model_parity(served, model):
     x, got, comp = run_model(c, gid, mids[model], model, b)
     assert comp.t_end_ns > comp.t_start_ns
     ref = omodels.forward(model, synthgen.weights(model), x)
+    out = split_outputs(model, got, b)
     if model == "ssd_mobilenet_v1":
-        loc, conf = got[: b * 3000 * 4].reshape(b, 3000, 4), got[b * 3000 * 4:].reshape(b, 3000, 21)
-        assert rel_err(loc, ref["loc"]) <= REL_TOL
-        assert rel_err(conf, ref["conf"]) <= REL_TOL
-        err = np.abs(conf - ref["conf"]).max()
-        strict, judged, amb = top1_agreement(conf, ref["conf"], 4 * err)
+        assert rel_err(out["loc"], ref["loc"]) <= REL_TOL
+        assert rel_err(out["conf"], ref["conf"]) <= REL_TOL
+        err = np.abs(out["conf"] - ref["conf"]).max()
+        strict, judged, amb = top1_agreement(out["conf"], ref["conf"], 4 * err)
         assert judged >= TOP1_TOL, (strict, judged, amb)
     else:
-        ref_l = ref["logits"]
-        got_l = got.reshape(ref_l.shape)
+        ref_l, got_l = ref["logits"], out["logits"].reshape(ref["logits"].shape)
         e = rel_err(got_l, ref_l)
         assert e <= REL_TOL, e
         err = np.abs(got_l - ref_l).max()
         strict, judged, amb = top1_agreement(got_l, ref_l, 4 * err)
         assert judged >= TOP1_TOL, (strict, judged, amb)
+        if model == "bert_base":   # the 768-d pooled [CLS] representation, element by element
+            assert rel_err(out["pooled"], ref["pooled"]) <= REL_TOL
 
 
 def test_batch_sizes_ragged(served):
@@ -73,4 +74,4 @@ def test_batch_sizes_ragged(served):
     for b in (1, 5):
         x, got, _ = run_model(c, gid, mids["resnet50"], "resnet50", b, batch_id=3)
         ref = omodels.forward("resnet50", synthgen.weights("resnet50"), x)["logits"]
-        assert rel_err(got.reshape(ref.shape), ref) <= REL_TOL
+        assert rel_err(split_outputs("resnet50", got, b)["logits"], ref) <= REL_TOL

@@ -8,10 +8,13 @@ Schemes, on the same kernels and the same Poisson traces:
              is its largest SLO-feasible batch at 100 %, the shared duty cycle
              is the longest of the two lanes' execution times;
   spatial    two gpu-lets, 20 % for LeNet and 80 % for VGG-16 (the paper's
-             "MPS(20:80)"): each lane on its own gpu-let with its own duty cycle.
-The paper's third scheme, unpartitioned concurrent kernels ("MPS(default)"),
-has no analogue here: an executor holds a whole SM (1 CTA/SM, ~225 KB of
-shared memory), so two executors cannot share SMs.
+             "MPS(20:80)"): each lane on its own gpu-let with its own duty cycle;
+  unconfined the paper's third scheme, concurrent kernels without a static SM
+             partition ("MPS(default)"; two persistent executors
+             without green contexts, gl_create_gpulets_unconfined): the same two
+             lanes on two executors of the primary context whose CTAs the
+             hardware places; one executor CTA fills an SM, so each still runs a
+             fixed CTA count (20:80, and 50:50 -- no size policy at all).
 
 For rate multipliers x (the models' B200-scaled paper rates times x), the
 violation fraction (late + dropped) of each model is measured.
@@ -26,6 +29,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
+
+
+SCHEMES = ("temporal", "spatial-20:80", "unconfined-20:80", "unconfined-50:50")
 
 
 def lane(model, rate, batch, exec_us):
@@ -66,10 +72,10 @@ def main():
     for m in (ms, ml):
         base[m] = float(lo[m] if lo[m] else sk[m])
     out = {"models": [small, large], "slo_us": [slo[ms], slo[ml]], "base_req_s": [base[ms], base[ml]],
-           "secs": a.secs, "cite": "P:257-276", "curves": {"temporal": [], "spatial-20:80": []}}
+           "secs": a.secs, "cite": "P:257-276", "curves": {k: [] for k in SCHEMES}}
     for x in [float(v) for v in a.xs.split(",")]:
         rates = [int(r * x) for r in base]
-        for scheme in ("temporal", "spatial-20:80"):
+        for scheme in SCHEMES:
             if scheme == "temporal":
                 bs, bl = b_sat(lat_env, ms, g100, slo[ms]), b_sat(lat_env, ml, g100, slo[ml])
                 es, el = lat_env[ms][bs - 1][g100], lat_env[ml][bl - 1][g100]
@@ -77,14 +83,17 @@ def main():
                 gls = [{"gpu": 0, "slot": 0, "size": 100, "sm": 148, "D_us": int(d),
                         "lanes": [lane(small, rates[ms], bs, es), lane(large, rates[ml], bl, el)]}]
             else:
-                bs, bl = b_sat(lat_env, ms, g20, slo[ms]), b_sat(lat_env, ml, g80, slo[ml])
-                es, el = lat_env[ms][bs - 1][g20], lat_env[ml][bl - 1][g80]
-                gls = [{"gpu": 0, "slot": 0, "size": 20, "sm": 0, "D_us": int(es),
+                ps, pl = (50, 50) if scheme.endswith("50:50") else (20, 80)
+                gs, gl_ = common.GRID.index(ps), common.GRID.index(pl)
+                bs, bl = b_sat(lat_env, ms, gs, slo[ms]), b_sat(lat_env, ml, gl_, slo[ml])
+                es, el = lat_env[ms][bs - 1][gs], lat_env[ml][bl - 1][gl_]
+                gls = [{"gpu": 0, "slot": 0, "size": ps, "sm": 0, "D_us": int(es),
                         "lanes": [lane(small, rates[ms], bs, es)]},
-                       {"gpu": 0, "slot": 1, "size": 80, "sm": 0, "D_us": int(el),
+                       {"gpu": 0, "slot": 1, "size": pl, "sm": 0, "D_us": int(el),
                         "lanes": [lane(large, rates[ml], bl, el)]}]
             dump = "\n".join(json.dumps(g) for g in gls) + "\n" + json.dumps({"verdict": "Forced"})
-            my = srv.setup(dump, 0)
+            my = srv.setup(dump, 0, unconfined=scheme.startswith("unconfined"))
+            smids = [sorted(ctx.gpulet_smids(gid)) for gid in srv.made] if scheme.startswith("unconfined") else None
             w = srv.window(my, a.secs, 900 + int(100 * x))
             srv.teardown()
             per = w["per"]
@@ -92,6 +101,8 @@ def main():
                    "viol_frac": {m: round(per[m]["viol"] / max(per[m]["arrivals"], 1), 4) for m in (small, large)
                                  if m in per},
                    "p99_us": {m: per[m]["p99_us"] for m in (small, large) if m in per}}
+            if smids:
+                row["smids"] = smids
             out["curves"][scheme].append(row)
             print(scheme, json.dumps(row), flush=True)
     if a.json:
