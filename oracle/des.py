@@ -50,7 +50,7 @@ class Lane:
         self.cur = 0         # smooth weighted round-robin credit
 
 
-def simulate_trace(plan_gpulets, prof, slo, trace):
+def simulate_trace(plan_gpulets, prof, slo, trace, spawn=None, handoff_us=0):
     """The frontend + FIFO gpu-lets on a merged arrival trace, event by event.
 
     plan_gpulets: [(size, D_us, [(m, rate, batch, F), ...]), ...] (plan order);
@@ -74,6 +74,18 @@ def simulate_trace(plan_gpulets, prof, slo, trace):
         checked in order;
       * a gpu-let runs its batches in dispatch order; a batch of k starts at
         max(t, when the gpu-let is free) and takes Leff(k) = ceil(L(k,p) F / 1000).
+
+    Two-stage applications (F3, `traffic` P:788-790; DESIGN R28) when `spawn`
+    is given ({m: [m2, ...]}): every request of model m, when its batch
+    completes at `end`, creates one request of each m2 in order (indices
+    len(trace), len(trace) + 1, ... in creation order) that reaches the
+    frontend at end + handoff_us (the detector -> recogniser hand-off) and
+    keeps its root's arrival time, so its latency, deadline-guard and drop
+    tests measure from the application request's arrival against slo[m2] (the
+    application's budget from its arrival).  Arrivals -- trace and spawned --
+    are routed in (time, index) order.  Then returns (lat, log, parent, model)
+    over all requests: parent[i] the request that spawned i (-1 for the
+    trace), model[i] its model.
     """
     lanes, by_model = [], {}
     for gi, (size, D, ls) in enumerate(plan_gpulets):
@@ -82,8 +94,12 @@ def simulate_trace(plan_gpulets, prof, slo, trace):
             lanes.append(ln)
             by_model.setdefault(m, []).append(ln)
     free = [0] * len(plan_gpulets)
+    arr = [t for t, _m in trace]          # arrival of the request's root (deadlines, drops, latency)
+    model = [m for _t, m in trace]
+    parent = [-1] * len(trace)
     lat = [-1] * len(trace)
     log = []
+    pending = []                          # spawned requests not yet routed: heap of (ready time, index)
 
     def leff(ln, k):
         return (prof.L(ln.m, k, ln.size) * ln.F + 999) // 1000
@@ -93,13 +109,26 @@ def simulate_trace(plan_gpulets, prof, slo, trace):
             return False
         k = min(len(ln.q), ln.b)
         return (len(ln.q) >= ln.b or t - ln.window >= ln.D
-                or t - trace[ln.q[0]][0] + leff(ln, k) >= slo[ln.m])
+                or t - arr[ln.q[0]] + leff(ln, k) >= slo[ln.m])
 
     def first_ready_time(ln):
         if not ln.q:
             return None
         k = min(len(ln.q), ln.b)
-        return min(ln.window + ln.D, trace[ln.q[0]][0] + slo[ln.m] - leff(ln, k))
+        return min(ln.window + ln.D, arr[ln.q[0]] + slo[ln.m] - leff(ln, k))
+
+    def route(r):
+        cand = by_model.get(model[r], [])
+        if cand:
+            total = sum(ln.rate for ln in cand)
+            for ln in cand:
+                ln.cur += ln.rate
+            best = cand[0]
+            for ln in cand[1:]:
+                if ln.cur > best.cur:
+                    best = ln
+            best.cur -= total
+            best.q.append(r)
 
     nxt = 0
     while True:
@@ -107,26 +136,25 @@ def simulate_trace(plan_gpulets, prof, slo, trace):
         times = [x for x in times if x is not None]
         if nxt < len(trace):
             times.append(trace[nxt][0])
+        if pending:
+            times.append(pending[0][0])
         if not times:
             break
         t = min(times)
-        while nxt < len(trace) and trace[nxt][0] <= t:
-            m = trace[nxt][1]
-            cand = by_model.get(m, [])
-            if cand:
-                total = sum(ln.rate for ln in cand)
-                for ln in cand:
-                    ln.cur += ln.rate
-                best = cand[0]
-                for ln in cand[1:]:
-                    if ln.cur > best.cur:
-                        best = ln
-                best.cur -= total
-                best.q.append(nxt)
-            nxt += 1
+        while True:   # route every arrival up to t in (time, index) order
+            a = (trace[nxt][0], nxt) if nxt < len(trace) and trace[nxt][0] <= t else None
+            s_ = pending[0] if pending and pending[0][0] <= t else None
+            if a is None and s_ is None:
+                break
+            if s_ is None or (a is not None and a < s_):
+                route(nxt)
+                nxt += 1
+            else:
+                heapq.heappop(pending)
+                route(s_[1])
         for li, ln in enumerate(lanes):
             while ready(ln, t):
-                ln.q = [r for r in ln.q if (t - trace[r][0]) + leff(ln, 1) <= slo[ln.m]]
+                ln.q = [r for r in ln.q if (t - arr[r]) + leff(ln, 1) <= slo[ln.m]]
                 ln.window = t
                 if not ln.q:
                     break
@@ -136,8 +164,32 @@ def simulate_trace(plan_gpulets, prof, slo, trace):
                 free[ln.gl] = end
                 log.append((li, t, k, batch[0]))
                 for r in batch:
-                    lat[r] = end - trace[r][0]
-    return lat, log
+                    lat[r] = end - arr[r]
+                    for m2 in (spawn or {}).get(model[r], ()):
+                        arr.append(arr[r])
+                        model.append(m2)
+                        parent.append(r)
+                        lat.append(-1)
+                        heapq.heappush(pending, (end + handoff_us, len(arr) - 1))
+    if spawn is None:
+        return lat, log
+    return lat, log, parent, model
+
+
+def app_latencies(lat, parent, n_root):
+    """Latency of each application request (F3): the largest latency over the
+    request and its descendants (all measured from the root's arrival); -1 if
+    any of them was dropped."""
+    out = list(lat[:n_root])
+    for i in range(n_root, len(lat)):
+        r = parent[i]
+        while r >= n_root:
+            r = parent[r]
+        if lat[i] < 0 or out[r] < 0:
+            out[r] = -1
+        else:
+            out[r] = max(out[r], lat[i])
+    return out
 
 
 def simulate(plan_gpulets, prof, slo, arrivals, names=None):

@@ -85,6 +85,58 @@ def test_model_without_lane_dropped():
     assert lat == [-1, 5] and log == [(0, 3, 1, 1)]
 
 
+class PerModel:
+    """Profile with L(k, p) = lat[m] for every k and p (hand-traced chain pins)."""
+
+    def __init__(self, lat):
+        self.lat = lat
+
+    def L(self, m, k, p):
+        return self.lat[m]
+
+
+CHAIN_PLAN = [(100, 10**6, [(0, 1, 1, 1000)]), (50, 1000, [(1, 1, 2, 1000)]), (50, 10**6, [(2, 1, 1, 1000)])]
+
+
+def test_chain_hand_traced():
+    """F3 two-stage chain (DESIGN R28): detector m0 (L 100, b 1) spawns one m1 (L 50,
+    b 2, D 1000) and one m2 (L 30, b 1) request per completed request, 7 µs later,
+    each keeping its root's arrival.  t=0: m0 batch -> end 100, spawns 2,3 at 107;
+    t=10: m0 batch starts when the gpu-let frees at 100 -> end 200, spawns 4,5 at 207;
+    t=107: 3 dispatches alone (b 1) -> 137; 2 waits (b 2, window 0 + D 1000, deadline
+    0 + 5000 - 50); t=207: 4 completes m1's batch [2, 4] -> 257, 5 -> 237."""
+    lat, log, parent, model = des.simulate_trace(CHAIN_PLAN, PerModel([100, 50, 30]), [1000, 5000, 5000],
+                                                 [(0, 0), (10, 0)], spawn={0: [1, 2]}, handoff_us=7)
+    assert lat == [100, 190, 257, 137, 247, 227]
+    assert parent == [-1, -1, 0, 0, 1, 1] and model == [0, 0, 1, 2, 1, 2]
+    assert log == [(0, 0, 1, 0), (0, 10, 1, 1), (2, 107, 1, 3), (1, 207, 2, 2), (2, 207, 1, 5)]
+    assert des.app_latencies(lat, parent, 2) == [257, 247]
+
+
+def test_chain_drops_propagate():
+    """A hopeless second-stage request is dropped ((107 - 0) + 30 > 120) and fails its
+    application; a dropped first-stage request spawns nothing."""
+    lat, log, parent, model = des.simulate_trace(CHAIN_PLAN, PerModel([100, 50, 30]), [1000, 5000, 120],
+                                                 [(0, 0), (10, 0)], spawn={0: [1, 2]}, handoff_us=7)
+    assert lat[3] == -1 and des.app_latencies(lat, parent, 2)[0] == -1
+    lat, log, parent, model = des.simulate_trace(CHAIN_PLAN, PerModel([100, 50, 30]), [150, 5000, 5000],
+                                                 [(0, 0), (10, 0)], spawn={0: [1, 2]}, handoff_us=7)
+    # request 1 would end at 200 > 10 + 150: dropped at its dispatch (t = 10: 0 + 100 > 150? no -> sent);
+    # it is late (190 > 150) but still spawns; only a drop stops the chain
+    assert lat[:2] == [100, 190] and len(lat) == 6
+    lat, log, parent, model = des.simulate_trace(CHAIN_PLAN, PerModel([100, 50, 30]), [90, 5000, 5000],
+                                                 [(0, 0), (10, 0)], spawn={0: [1, 2]}, handoff_us=7)
+    assert lat == [-1, -1] and parent == [-1, -1] and des.app_latencies(lat, parent, 2) == [-1, -1]
+
+
+def test_chain_empty_spawn_is_plain():
+    plan = [(100, 1000, [(0, 1, 4, 1000)])]
+    tr = [(0, 0), (5, 0), (3000, 0)]
+    lat0, log0 = des.simulate_trace(plan, Flat([100] * 32), [10_000], tr)
+    lat1, log1, parent, model = des.simulate_trace(plan, Flat([100] * 32), [10_000], tr, spawn={})
+    assert (lat0, log0) == (lat1, log1) and parent == [-1] * 3 and model == [0, 0, 0]
+
+
 # ---- native gl_serve_sim == oracle DES ------------------------------------------------------------
 def _lanes_from_plan(dump, prof_lat):
     plan, lanes = [], []
