@@ -255,6 +255,38 @@ gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n
                    const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
                    uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes, gl_lane_stats* lane_stats);
 
+/* Two-stage applications (`traffic` P:788-790: SSD-MobileNet detects,
+ * GoogLeNet and VGG-16 recognise; DESIGN R28).  A request of model i, when its batch
+ * completes at t, creates spawn[i * n_models + j] requests of each model j (j ascending;
+ * indices n_req, n_req + 1, ... in creation order) that reach the frontend at
+ * t + handoff_us (the detector -> recogniser hand-off: box decode, NMS and crops, see
+ * gl_ssd_detect / gl_crop_resize) and keep the arrival time of the trace request they
+ * descend from: their latency, deadline guard and drop test are measured from it
+ * against slo_us[j] (the application's budget from its arrival), so the stage split of
+ * an application SLO is expressed by the SLOs of its first-stage models.  Trace and
+ * spawned arrivals are routed in (time, index) order.  A dropped request spawns nothing;
+ * a late one still does.  lat_us / parent / req_model hold cap_req entries (trace +
+ * spawned); GL_E_CAPACITY if a run would create more. */
+typedef struct {
+  const int32_t* spawn;      /* [n_models][n_models] requests created per completion */
+  int32_t handoff_us;        /* >= 0 */
+  int32_t pad_;
+  int64_t cap_req;           /* >= n_req: capacity of lat_us, parent, req_model */
+  int32_t* parent;           /* out (optional): spawning request, -1 for trace requests */
+  int32_t* req_model;        /* out (optional): model slot of every request */
+  int64_t n_total;           /* out: requests of the run (trace + spawned) */
+} gl_chain;
+/* gl_serve with application chains (plain or end-to-end lanes as gl_serve; a spawned
+ * request of model j takes the next host slot of model j in end-to-end mode). */
+gl_status gl_serve_chain(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                         const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, gl_chain* chain,
+                         int64_t* lat_us, uint64_t* dev_ns, gl_lane_stats* lane_stats);
+/* gl_serve_sim with application chains: a completion is the end of its batch on the
+ * virtual FIFO gpu-let (oracle: oracle/des.py simulate_trace(spawn=...)). */
+gl_status gl_serve_sim_chain(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                             const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, gl_chain* chain,
+                             int64_t* lat_us, int64_t* batch_log, int64_t cap, int64_t* n_log);
+
 /* ---- scheduler (Alg. 1) --------------------------------- */
 typedef struct {
   int32_t n_models;          /* <= 8, canonical order */

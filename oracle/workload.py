@@ -149,6 +149,50 @@ def slos(lat_env, slo_mode):
     raise WorkloadError("arg", "slo_mode")
 
 
+PAPER_APP_SLO_MS = {"game": 95, "traffic": 136}
+
+
+def traffic_stage_slos(lat_env, slo_mode="rule", handoff_us=0):
+    """F3 `traffic` as a two-stage chain (DESIGN R28).  The application SLO is "the
+    longest model inference latency" of the app doubled: 2 max over
+    {SSD, GoogLeNet, VGG-16} of L*(32, 100 %) in rule mode, 136 ms in table mode.
+    The detector stage gets the share of it that its solo latency has of the two
+    stages' (the slower recogniser counts: they run in parallel):
+    s1 = floor(s_app L_ssd / (L_ssd + max(L_goo, L_vgg))), all at (32, 100 %).
+    Returns (s_app, s1); the recognisers' budget from their spawn is
+    s_app - s1 - handoff_us."""
+    g = GRID.index(100)
+    L = {m: lat_env[NAMES.index(m)][BMAX - 1][g] for m in ("ssd_mobilenet_v1", "googlenet", "vgg16")}
+    if slo_mode == "rule":
+        s_app = 2 * max(L.values())
+    elif slo_mode == "table":
+        s_app = PAPER_APP_SLO_MS["traffic"] * 1000
+    else:
+        raise WorkloadError("arg", "slo_mode")
+    l2 = max(L["googlenet"], L["vgg16"])
+    s1 = (s_app * L["ssd_mobilenet_v1"]) // (L["ssd_mobilenet_v1"] + l2)
+    if s_app - s1 - handoff_us <= 0:
+        raise WorkloadError("arg", "handoff_us")
+    return s_app, s1
+
+
+def chain_workload(lat_env, slo_mode, x=1.0, num_gpus=1, handoff_us=0):
+    """Scenario "traffic-chain": per-model SLOs of the plan (SSD s1; GoogLeNet and VGG-16
+    s_app - s1 - handoff_us, their budget from the spawn) and rates: traffic's 100 req/s
+    per model scaled by the application's SLO, floor((100 * 136 ms * x) /
+    s_app) * num_gpus (C4.3 with the app SLO as the reference, R23/R28)."""
+    if not (x >= 0.0 and math.isfinite(x)):
+        raise WorkloadError("arg", "x")
+    s_app, s1 = traffic_stage_slos(lat_env, slo_mode, handoff_us)
+    slo = slos(lat_env, slo_mode)
+    rates = [0] * len(NAMES)
+    for m in ("ssd_mobilenet_v1", "googlenet", "vgg16"):
+        i = NAMES.index(m)
+        slo[i] = s1 if m == "ssd_mobilenet_v1" else s_app - s1 - handoff_us
+        rates[i] = math.floor(float(100 * PAPER_APP_SLO_MS["traffic"] * 1000) * x / float(s_app)) * num_gpus
+    return slo, rates, s_app
+
+
 def scenario_rates(scenario, slo_us, x=1.0, num_gpus=1):
     """Returns (rates, base).  rate_m = floor(((base_m * paper_us_ref) * x) / slo_us_ref) * num_gpus."""
     if scenario not in SCENARIOS:
@@ -189,7 +233,13 @@ def schedule_files(profile_text, coeffs_text, workload_text):
     if len(given) != 1:
         raise WorkloadError("arg", "exactly one of scenario, base_rates, rates, models")
     truncated = None
-    if "scenario" in W or "base_rates" in W:
+    app_slo = None
+    if W.get("scenario") == "traffic-chain":
+        slo, rates, app_slo = chain_workload(prof["lat"], slo_mode, float(W.get("x", 1.0)), N,
+                                             int(W.get("handoff_us", 0)))
+        base = [0, 100, 0, 100, 100, 0]
+        truncated = next((m for m in range(len(NAMES)) if base[m] > 0 and rates[m] == 0), None)
+    elif "scenario" in W or "base_rates" in W:
         if "scenario" in W:
             rates, base = scenario_rates(W["scenario"], slo, float(W.get("x", 1.0)), N)
         else:
@@ -208,8 +258,10 @@ def schedule_files(profile_text, coeffs_text, workload_text):
     coeffs = None
     if coeffs_text is not None:
         coeffs = tuple(float(c) for c in json.loads(coeffs_text)["coeffs"])
-    head = json.dumps({"slo_us": slo, "rates": rates, "num_gpus": N, "mode": mode, "slo_mode": slo_mode},
-                      separators=(",", ":")) + "\n"
+    hd = {"slo_us": slo, "rates": rates, "num_gpus": N, "mode": mode, "slo_mode": slo_mode}
+    if app_slo is not None:
+        hd["app_slo_us"] = app_slo
+    head = json.dumps(hd, separators=(",", ":")) + "\n"
     if truncated is not None:
         return head + json.dumps({"verdict": "NotSchedulable", "failed_model": NAMES[truncated],
                                   "reason": "rate_truncated"}, separators=(",", ":")) + "\n", False

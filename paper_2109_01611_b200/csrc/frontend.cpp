@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <deque>
+#include <queue>
 #include <unordered_map>
 #include <vector>
 
@@ -205,14 +206,93 @@ struct Cleanup {
     }
   }
 };
+// ---- two-stage application chains (F3, DESIGN R28) -------------------------------------------
+// Requests of the trace keep indices 0..n_req-1; a completed request of model m
+// creates spawn[m][m2] requests of each m2 (m2 ascending), indices in creation
+// order, that reach the frontend handoff_us later and keep their root's arrival
+// (deadlines, drops and latency measure from it).  Arrivals -- trace and spawned --
+// are routed in (time, index) order.
+struct Requests {
+  std::vector<int64_t> arr;     // root arrival of every request
+  std::vector<int32_t> model;
+  std::vector<int32_t> parent;
+  std::priority_queue<std::pair<int64_t, int64_t>, std::vector<std::pair<int64_t, int64_t>>,
+                      std::greater<std::pair<int64_t, int64_t>>> pending;   // (ready time, index)
+  const int32_t* spawn = nullptr;
+  int32_t n_models = 0, handoff = 0;
+  int64_t cap = 0;
+  bool init(const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const gl_chain* ch, int32_t nm) {
+    n_models = nm;
+    cap = ch ? ch->cap_req : n_req;
+    if (cap < n_req) return false;
+    arr.reserve(cap), model.reserve(cap), parent.reserve(cap);   // data() stays valid: never grows past cap
+    arr.assign(arr_us, arr_us + n_req);
+    model.assign(arr_model, arr_model + n_req);
+    parent.assign(n_req, -1);
+    if (ch) spawn = ch->spawn, handoff = ch->handoff_us;
+    return true;
+  }
+  // spawn the children of request r completed at t; calls made(j) for each; false: capacity
+  template <class F>
+  bool complete(int64_t r, int64_t t, F&& made) {
+    if (!spawn) return true;
+    for (int32_t m2 = 0; m2 < n_models; ++m2)
+      for (int32_t c = 0; c < spawn[(int64_t)model[r] * n_models + m2]; ++c) {
+        const int64_t j = (int64_t)arr.size();
+        if (j >= cap) return false;
+        arr.push_back(arr[r]);
+        model.push_back(m2);
+        parent.push_back((int32_t)r);
+        pending.push({t + handoff, j});
+        made(j);
+      }
+    return true;
+  }
+  // route every arrival up to t in (time, index) order
+  template <class F>
+  void arrivals(int64_t t, int64_t n_req, int64_t& next, F&& route) {
+    for (;;) {
+      const bool a = next < n_req && arr[next] <= t;
+      const bool p = !pending.empty() && pending.top().first <= t;
+      if (!a && !p) return;
+      if (!p || (a && std::make_pair(arr[next], next) < pending.top())) {
+        route(next++);
+      } else {
+        const int64_t j = pending.top().second;
+        pending.pop();
+        route(j);
+      }
+    }
+  }
+  int64_t next_time(int64_t n_req, int64_t next) const {
+    int64_t t = next < n_req ? arr[next] : INT64_MAX;
+    if (!pending.empty()) t = std::min(t, pending.top().first);
+    return t;
+  }
+  void out(const gl_chain* ch_const) const {
+    gl_chain* ch = const_cast<gl_chain*>(ch_const);
+    if (!ch) return;
+    ch->n_total = (int64_t)arr.size();
+    for (size_t i = 0; i < arr.size(); ++i) {
+      if (ch->parent) ch->parent[i] = parent[i];
+      if (ch->req_model) ch->req_model[i] = model[i];
+    }
+  }
+};
 }  // namespace
 
-extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
-                              const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
-                              int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes,
-                              gl_lane_stats* lane_stats) {
-  if (!ctx || !lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || !slo_us || !lat_us)
+
+static gl_status serve_impl(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
+                            const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
+                            gl_chain* chain, int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes,
+                            int64_t* d2h_bytes, gl_lane_stats* lane_stats) {
+  if (!ctx || !lanes || n_lanes < 1 || n_models < 1 || n_req < 0 || (!arr_us && n_req) || (!arr_model && n_req) ||
+      !slo_us || !lat_us || (chain && chain->handoff_us < 0) || (chain && !chain->spawn))
     return GL_E_ARG;
+  for (int64_t r = 1; r < n_req; ++r)
+    if (arr_us[r] < arr_us[r - 1]) return gl::set_error(GL_E_ARG, "gl_serve: arrivals must be sorted");
+  Requests R;
+  if (!R.init(arr_us, arr_model, n_req, chain, n_models)) return gl::set_error(GL_E_ARG, "gl_serve: cap_req < n_req");
   std::vector<LaneState> L(n_lanes);
   Cleanup cleanup{L};
   RtGuard rt;
@@ -230,11 +310,11 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
         if (cudaEventCreateWithFlags(&L[i].buf[b].ev, cudaEventDisableTiming) != cudaSuccess) return GL_E_CUDA;
     }
   }
-  Policy<LaneState> pol(L, n_models, arr_us, arr_model, slo_us);
-  for (int64_t r = 0; r < n_req; ++r) lat_us[r] = -2;
+  Policy<LaneState> pol(L, n_models, R.arr.data(), R.model.data(), slo_us);
+  for (int64_t r = 0; r < R.cap; ++r) lat_us[r] = -2;
   if (lane_stats)
     for (int i = 0; i < n_lanes; ++i) lane_stats[i] = gl_lane_stats{0, 0, 0, 0};
-  std::vector<int64_t> seq_of(n_req, 0);   // model-local arrival index of each request (host slot rule)
+  std::vector<int64_t> seq_of(R.cap, 0);   // model-local arrival index of each request (host slot rule)
   std::vector<int64_t> model_seq(n_models, 0);
   int64_t h2d = 0, d2h = 0;
   uint64_t t_first = ~0ull, t_last = 0;
@@ -244,32 +324,36 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
     return (int64_t)std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0)
         .count();
   };
-  auto complete = [&](Batch& b, int64_t t, int64_t& outstanding) {
-    for (int64_t r : b.reqs) {
-      lat_us[r] = t - arr_us[r];
-      --outstanding;
-    }
+  int64_t next = 0, outstanding = 0;
+  bool over_cap = false;
+  // a request done at t: its latency, then its spawned successors (outstanding until served or dropped)
+  auto finish = [&](int64_t r, int64_t t) {
+    lat_us[r] = t - R.arr[r];
+    --outstanding;
+    over_cap |= !R.complete(r, t, [&](int64_t) { ++outstanding; });
+  };
+  auto complete = [&](Batch& b, int64_t t) {
+    for (int64_t r : b.reqs) finish(r, t);
     b.reqs.clear();
     b.slots.clear();
     b.stage = FREE;
   };
-  int64_t next = 0, outstanding = 0;
   gl_completion comp[128];
   const int64_t deadline = (n_req ? arr_us[n_req - 1] : 0) + 30'000'000;
   while (next < n_req || outstanding > 0) {
     int64_t now = now_us();
     if (now > deadline) return GL_E_TIMEOUT;
-    // 1. arrivals -> lanes (smooth weighted round-robin per model)
-    while (next < n_req && arr_us[next] <= now) {
-      const int m = arr_model[next];
-      seq_of[next] = model_seq[m]++;
-      if (pol.route(next) < 0) {
-        lat_us[next] = -1;
-      } else {
-        ++outstanding;
+    if (over_cap) return gl::set_error(GL_E_CAPACITY, "gl_serve: spawned requests exceed cap_req");
+    // 1. arrivals (trace and spawned) -> lanes (smooth weighted round-robin per model)
+    R.arrivals(now, n_req, next, [&](int64_t r) {
+      const int m = R.model[r];
+      seq_of[r] = model_seq[m]++;
+      if (r < n_req) ++outstanding;   // spawned requests were counted when created
+      if (pol.route(r) < 0) {
+        lat_us[r] = -1;
+        --outstanding;
       }
-      ++next;
-    }
+    });
     // 2. duty-cycle dispatch
     for (int li = 0; li < n_lanes; ++li) {
       LaneState& ln = L[li];
@@ -337,7 +421,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
         if (q == cudaErrorNotReady) continue;
         if (q != cudaSuccess) return GL_E_CUDA;
         if (bt.stage == D2H) {
-          complete(bt, now_us(), outstanding);
+          complete(bt, now_us());
           continue;
         }
         uint64_t ticket = 0;
@@ -371,10 +455,7 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       if (b < 0) {   // plain mode, or a zero-copy batch (outputs already in the host ring)
         if (b == kZeroCopyBuf) d2h += (int64_t)it->second.reqs.size() * ln.cfg.out_req_bytes;
         const int64_t t = now_us();
-        for (int64_t r : it->second.reqs) {
-          lat_us[r] = t - arr_us[r];
-          --outstanding;
-        }
+        for (int64_t r : it->second.reqs) finish(r, t);
         inflight.erase(it);
         continue;
       }
@@ -386,20 +467,39 @@ extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes
       bt.stage = D2H;
     }
   }
+  if (over_cap) return gl::set_error(GL_E_CAPACITY, "gl_serve: spawned requests exceed cap_req");
   if (dev_ns) {
     dev_ns[0] = t_first == ~0ull ? 0 : t_first;
     dev_ns[1] = t_last;
   }
   if (h2d_bytes) *h2d_bytes = h2d;
   if (d2h_bytes) *d2h_bytes = d2h;
+  R.out(chain);
   return GL_OK;
 }
 
-extern "C" gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
-                                  const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
-                                  int64_t* batch_log, int64_t cap, int64_t* n_log) {
+extern "C" gl_status gl_serve(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
+                              const int64_t* arr_us, const int32_t* arr_model, int64_t n_req, const int32_t* slo_us,
+                              int64_t* lat_us, uint64_t* dev_ns, int64_t* h2d_bytes, int64_t* d2h_bytes,
+                              gl_lane_stats* lane_stats) {
+  return serve_impl(ctx, lanes, n_lanes, n_models, arr_us, arr_model, n_req, slo_us, nullptr, lat_us, dev_ns,
+                    h2d_bytes, d2h_bytes, lane_stats);
+}
+
+extern "C" gl_status gl_serve_chain(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
+                                    const int64_t* arr_us, const int32_t* arr_model, int64_t n_req,
+                                    const int32_t* slo_us, gl_chain* chain, int64_t* lat_us, uint64_t* dev_ns,
+                                    gl_lane_stats* lane_stats) {
+  if (!chain) return gl::set_error(GL_E_ARG, "gl_serve_chain: chain is NULL");
+  return serve_impl(ctx, lanes, n_lanes, n_models, arr_us, arr_model, n_req, slo_us, chain, lat_us, dev_ns, nullptr,
+                    nullptr, lane_stats);
+}
+
+static gl_status serve_sim_impl(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                                const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, gl_chain* chain,
+                                int64_t* lat_us, int64_t* batch_log, int64_t cap, int64_t* n_log) {
   if (!lanes || n_lanes < 1 || n_models < 1 || (!arr_us && n_req) || (!arr_model && n_req) || !slo_us ||
-      (!lat_us && n_req) || n_req < 0 || (!batch_log && cap > 0))
+      (!lat_us && n_req) || n_req < 0 || (!batch_log && cap > 0) || (chain && (chain->handoff_us < 0 || !chain->spawn)))
     return gl::set_error(GL_E_ARG, "gl_serve_sim: bad arguments");
   std::vector<PLane> L(n_lanes);
   std::unordered_map<int32_t, int64_t> free_at;   // gpu-let id -> time its FIFO drains
@@ -412,14 +512,16 @@ extern "C" gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t
   }
   for (int64_t r = 1; r < n_req; ++r)
     if (arr_us[r] < arr_us[r - 1]) return gl::set_error(GL_E_ARG, "gl_serve_sim: arrivals must be sorted");
-  Policy<PLane> pol(L, n_models, arr_us, arr_model, slo_us);
+  Requests R;
+  if (!R.init(arr_us, arr_model, n_req, chain, n_models)) return gl::set_error(GL_E_ARG, "gl_serve_sim: cap_req < n_req");
+  Policy<PLane> pol(L, n_models, R.arr.data(), R.model.data(), slo_us);
   int64_t logged = 0, next = 0;
-  for (int64_t r = 0; r < n_req; ++r) lat_us[r] = -1;
+  for (int64_t r = 0; r < R.cap; ++r) lat_us[r] = -1;
   for (;;) {
-    int64_t t = next < n_req ? arr_us[next] : INT64_MAX;
+    int64_t t = R.next_time(n_req, next);
     for (int li = 0; li < n_lanes; ++li) t = std::min(t, pol.deadline(li));
     if (t == INT64_MAX) break;
-    while (next < n_req && arr_us[next] <= t) pol.route(next++);   // no lane: stays -1 (dropped)
+    R.arrivals(t, n_req, next, [&](int64_t r) { pol.route(r); });   // no lane: stays -1 (dropped)
     for (int li = 0; li < n_lanes; ++li) {
       PLane& ln = L[li];
       while (pol.ready(li, t)) {
@@ -437,12 +539,32 @@ extern "C" gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t
         }
         ++logged;
         for (int i = 0; i < k; ++i) {
-          lat_us[ln.q.front()] = end - arr_us[ln.q.front()];
+          const int64_t r = ln.q.front();
+          lat_us[r] = end - R.arr[r];
           ln.q.pop_front();
+          if (!R.complete(r, end, [](int64_t) {}))
+            return gl::set_error(GL_E_CAPACITY, "gl_serve_sim: spawned requests exceed cap_req");
         }
       }
     }
   }
   if (n_log) *n_log = logged;
+  R.out(chain);
   return GL_OK;
+}
+
+extern "C" gl_status gl_serve_sim(const gl_lane* lanes, int32_t n_lanes, int32_t n_models, const int64_t* arr_us,
+                                  const int32_t* arr_model, int64_t n_req, const int32_t* slo_us, int64_t* lat_us,
+                                  int64_t* batch_log, int64_t cap, int64_t* n_log) {
+  return serve_sim_impl(lanes, n_lanes, n_models, arr_us, arr_model, n_req, slo_us, nullptr, lat_us, batch_log, cap,
+                        n_log);
+}
+
+extern "C" gl_status gl_serve_sim_chain(const gl_lane* lanes, int32_t n_lanes, int32_t n_models,
+                                        const int64_t* arr_us, const int32_t* arr_model, int64_t n_req,
+                                        const int32_t* slo_us, gl_chain* chain, int64_t* lat_us, int64_t* batch_log,
+                                        int64_t cap, int64_t* n_log) {
+  if (!chain) return gl::set_error(GL_E_ARG, "gl_serve_sim_chain: chain is NULL");
+  return serve_sim_impl(lanes, n_lanes, n_models, arr_us, arr_model, n_req, slo_us, chain, lat_us, batch_log, cap,
+                        n_log);
 }

@@ -486,6 +486,31 @@ gl_status rates_of(const int32_t* slo, const std::string& scen, double x, int nu
   return scale_rates(slo, base, app, x, num_gpus, rates);
 }
 
+// F3 `traffic` as a two-stage chain (DESIGN R28): application SLO = 2 x the longest
+// member's L*(32, 100 %) (136 ms in table mode); the detector's budget is
+// its share of the two stages' solo latencies, s1 = floor(s_app L_ssd / (L_ssd +
+// max(L_goo, L_vgg))); the recognisers get s_app - s1 - handoff from their spawn;
+// rates floor((100 * 136 ms * x) / s_app) * num_gpus for SSD, GoogLeNet, VGG-16.
+constexpr int kSsd = 3, kGoo = 1, kVgg = 4;
+constexpr int64_t kPaperTrafficSloMs = 136;
+gl_status chain_workload(const int32_t* lat, int slo_mode, double x, int num_gpus, int64_t handoff, int32_t* slo,
+                         int64_t* rates, int64_t* s_app_out) {
+  if (!(x >= 0.0) || !std::isfinite(x)) return err(GL_E_ARG, "x must be finite and >= 0");
+  auto L = [&](int m) { return (int64_t)lat[((size_t)m * kB + (kB - 1)) * kP + (kP - 1)]; };
+  const int64_t l1 = L(kSsd), l2 = std::max(L(kGoo), L(kVgg));
+  const int64_t s_app = slo_mode == 0 ? 2 * std::max(l1, l2) : kPaperTrafficSloMs * 1000;
+  const int64_t s1 = (s_app * l1) / (l1 + l2);
+  if (handoff < 0 || s_app - s1 - handoff <= 0) return err(GL_E_ARG, "traffic-chain: handoff_us");
+  slos(lat, slo_mode, slo);
+  for (int m = 0; m < kM; ++m) rates[m] = 0;
+  for (int m : {kGoo, kSsd, kVgg}) {
+    slo[m] = (int32_t)(m == kSsd ? s1 : s_app - s1 - handoff);
+    rates[m] = (int64_t)std::floor((double)(100 * kPaperTrafficSloMs * 1000) * x / (double)s_app) * num_gpus;
+  }
+  *s_app_out = s_app;
+  return GL_OK;
+}
+
 std::string ints_json(const int64_t* v, int n) {
   std::string s = "[";
   for (int i = 0; i < n; ++i) s += (i ? "," : "") + std::to_string(v[i]);
@@ -514,7 +539,10 @@ extern "C" gl_status gl_workload_rates(const int32_t* lat_us, int32_t slo_mode, 
   int32_t slo[kM];
   slos(lat_us, slo_mode, slo);
   int64_t r[kM];
-  gl_status rc = rates_of(slo, scenario, x, num_gpus, r, nullptr);
+  int64_t s_app = 0;
+  gl_status rc = std::string(scenario) == "traffic-chain"
+                     ? chain_workload(lat_us, slo_mode, x, num_gpus, 0, slo, r, &s_app)
+                     : rates_of(slo, scenario, x, num_gpus, r, nullptr);
   if (rc) return rc;
   for (int m = 0; m < kM; ++m) {
     if (r[m] > INT32_MAX) return err(GL_E_ARG, "gl_workload_rates: rate overflows int32");
@@ -569,7 +597,19 @@ extern "C" gl_status gl_schedule_files(const char* profile_csv, const char* coef
   const JVal* brts = W.get("base_rates");
   if ((scen != nullptr) + (rts != nullptr) + (mods != nullptr) + (brts != nullptr) != 1)
     return err(GL_E_ARG, "workload: give exactly one of scenario, base_rates, rates, models");
-  if (scen || brts) {
+  int64_t app_slo = -1;
+  if (scen && scen->kind == JVal::STR && scen->s == "traffic-chain") {
+    double x = 1.0;
+    if (const JVal* v = W.get("x"))
+      if (!jnum_double(v, x)) return err(GL_E_ARG, "workload: x");
+    int64_t handoff = 0;
+    if (const JVal* v = W.get("handoff_us"))
+      if (!jnum_int(v, handoff)) return err(GL_E_ARG, "workload: handoff_us");
+    rc = chain_workload(T.lat.data(), slo_mode == "rule" ? 0 : 1, x, (int)num_gpus, handoff, slo, rates, &app_slo);
+    if (rc) return rc;
+    for (int m : {kGoo, kSsd, kVgg})   // canonical order: the first model whose rate truncated
+      if (rates[m] == 0 && truncated < 0) truncated = m;
+  } else if (scen || brts) {
     if (scen && scen->kind != JVal::STR) return err(GL_E_ARG, "workload: scenario");
     double x = 1.0;
     if (const JVal* v = W.get("x"))
@@ -626,7 +666,8 @@ extern "C" gl_status gl_schedule_files(const char* profile_csv, const char* coef
   for (int m = 0; m < kM; ++m) slo64[m] = slo[m];
   std::string head = "{\"slo_us\":" + ints_json(slo64, kM) + ",\"rates\":" + ints_json(rates, kM) +
                      ",\"num_gpus\":" + std::to_string(num_gpus) + ",\"mode\":\"" + mode + "\",\"slo_mode\":\"" +
-                     slo_mode + "\"}\n";
+                     slo_mode + "\"" + (app_slo >= 0 ? ",\"app_slo_us\":" + std::to_string(app_slo) : std::string()) +
+                     "}\n";
   std::string out;
   int32_t ok = 0;
   if (truncated >= 0) {

@@ -56,6 +56,13 @@ class Lane(ctypes.Structure):
                 ("leff_us", ctypes.POINTER(ctypes.c_int32))]
 
 
+class Chain(ctypes.Structure):
+    """gl_chain (include/gpulet.h): two-stage application chains (F3)."""
+    _fields_ = [("spawn", ctypes.POINTER(ctypes.c_int32)), ("handoff_us", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("cap_req", ctypes.c_int64), ("parent", ctypes.POINTER(ctypes.c_int32)),
+                ("req_model", ctypes.POINTER(ctypes.c_int32)), ("n_total", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -92,6 +99,12 @@ def lib():
                          ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int64)],
             "gl_serve_sim": [ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
                              ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64), I64, ctypes.POINTER(I64)],
+            "gl_serve_chain": [P, ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
+                               ctypes.POINTER(I32), ctypes.POINTER(Chain), ctypes.POINTER(I64), ctypes.POINTER(U64),
+                               ctypes.POINTER(ctypes.c_int64)],
+            "gl_serve_sim_chain": [ctypes.POINTER(Lane), I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I32), I64,
+                                   ctypes.POINTER(I32), ctypes.POINTER(Chain), ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                   I64, ctypes.POINTER(I64)],
             "gl_schedule": [ctypes.POINTER(SchedInput), ctypes.c_char_p, ctypes.c_size_t,
                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_profile_load": [ctypes.c_char_p, I32, ctypes.POINTER(I32), ctypes.POINTER(D), ctypes.POINTER(D),
@@ -173,6 +186,42 @@ def serve_sim(lanes, n_models, arr_us, arr_model, slo_us, cap=1 << 20):
                               log.ctypes.data_as(P64), cap, ctypes.byref(n)))
     assert n.value <= cap
     return lat, [tuple(int(v) for v in row) for row in log[:n.value]]
+
+
+def _chain(n_models, spawn, handoff_us, n_req):
+    """spawn: {model slot: [spawned model slots]} -> (gl_chain, buffers kept alive, cap)."""
+    import numpy as np
+    sp = np.zeros((n_models, n_models), np.int32)
+    for m, kids in spawn.items():
+        for k in kids:
+            sp[m, k] += 1
+    fan = max(1, int(sp.sum(1).max()) + 1)
+    cap = n_req * fan          # a chain of depth 1 (trace -> spawned); deeper chains: pass a larger cap
+    par = np.zeros(cap, np.int32)
+    mdl = np.zeros(cap, np.int32)
+    P32 = ctypes.POINTER(ctypes.c_int32)
+    c = Chain(sp.ctypes.data_as(P32), int(handoff_us), 0, cap, par.ctypes.data_as(P32), mdl.ctypes.data_as(P32), 0)
+    return c, (sp, par, mdl), cap
+
+
+def serve_sim_chain(lanes, n_models, arr_us, arr_model, slo_us, spawn, handoff_us, cap=1 << 20):
+    """gl_serve_sim_chain -> (lat_us, batch log, parent, model) over trace + spawned requests."""
+    import numpy as np
+    L, keep = _lanes(lanes)
+    a = np.ascontiguousarray(arr_us, dtype=np.int64)
+    m = np.ascontiguousarray(arr_model, dtype=np.int32)
+    s = np.ascontiguousarray(slo_us, dtype=np.int32)
+    ch, bufs, creq = _chain(n_models, spawn, handoff_us, len(a))
+    lat = np.zeros(creq, np.int64)
+    log = np.zeros((cap, 4), np.int64)
+    n = ctypes.c_int64()
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    _check(lib().gl_serve_sim_chain(L, len(lanes), n_models, a.ctypes.data_as(P64),
+                                    m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
+                                    s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(ch),
+                                    lat.ctypes.data_as(P64), log.ctypes.data_as(P64), cap, ctypes.byref(n)))
+    t = ch.n_total
+    return lat[:t], [tuple(int(v) for v in row) for row in log[:n.value]], bufs[1][:t].copy(), bufs[2][:t].copy()
 
 
 class Context:
@@ -318,6 +367,32 @@ class Context:
             return out, {"dev_ns": (dev[0], dev[1]), "h2d_bytes": hb.value, "d2h_bytes": db.value,
                          "lanes": lanes_st}
         return out
+
+    def serve_chain(self, lanes, n_models, arr_us, arr_model, slo_us, spawn, handoff_us, stats=False):
+        """gl_serve_chain (device-resident lanes): returns (lat_us, parent, model) over the
+        trace + spawned requests, and with stats {"dev_ns", "lanes"}."""
+        import numpy as np
+        L, keep = _lanes(lanes)
+        for i, d in enumerate(lanes):
+            L[i].in_dev, L[i].out_dev = _ptr(d["x"]), _ptr(d["y"])
+        a = np.ascontiguousarray(arr_us, dtype=np.int64)
+        m = np.ascontiguousarray(arr_model, dtype=np.int32)
+        s = np.ascontiguousarray(slo_us, dtype=np.int32)
+        ch, bufs, creq = _chain(n_models, spawn, handoff_us, len(a))
+        out = np.zeros(creq, dtype=np.int64)
+        dev = (ctypes.c_uint64 * 2)()
+        ls = (ctypes.c_int64 * (4 * len(lanes)))()
+        _check(lib().gl_serve_chain(self.h, L, len(lanes), n_models, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                    m.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(a),
+                                    s.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(ch),
+                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), dev, ls))
+        t = ch.n_total
+        res = (out[:t], bufs[1][:t].copy(), bufs[2][:t].copy())
+        if stats:
+            lanes_st = [{"batches": ls[4 * i], "requests": ls[4 * i + 1], "busy_ns": ls[4 * i + 2] & (2**64 - 1)}
+                        for i in range(len(lanes))]
+            return res + ({"dev_ns": (dev[0], dev[1]), "lanes": lanes_st},)
+        return res
 
     def floor(self, gid, warmup=10, reps=200):
         """gl_floor -> (median host round trip µs, median device start -> end µs) of an empty program."""

@@ -211,3 +211,53 @@ def test_serve_sim_edge_cases():
         gpulet.serve_sim([dict(lanes[0], leff_us=None)], 2, [0], [0], [50, 50])
     with pytest.raises(gpulet.GpuletError):
         gpulet.serve_sim(lanes, 2, [5, 0], [0, 0], [50, 50])
+
+
+# ---- application chains (F3, DESIGN R28): native gl_serve_sim_chain == oracle DES ----------
+@native_lib
+def test_serve_sim_chain_hand_traced():
+    lanes = []
+    for gi, (size, D, ls) in enumerate(CHAIN_PLAN):
+        for (m, rate, b, F) in ls:
+            lanes.append(dict(gpulet=gi, model_slot=m, batch=b, duty_us=D, weight=rate, drop_us=[100, 50, 30][m],
+                              leff_us=[[100, 50, 30][m]] * 32))
+    lat, log, parent, model = gpulet.serve_sim_chain(lanes, 3, [0, 10], [0, 0], [1000, 5000, 5000], {0: [1, 2]}, 7)
+    assert lat.tolist() == [100, 190, 257, 137, 247, 227]
+    assert parent.tolist() == [-1, -1, 0, 0, 1, 1] and model.tolist() == [0, 0, 1, 2, 1, 2]
+    assert log == [(0, 0, 1, 0), (0, 10, 1, 1), (2, 107, 1, 3), (1, 207, 2, 2), (2, 207, 1, 5)]
+    lat, log, parent, model = gpulet.serve_sim_chain(lanes, 3, [0, 10], [0, 0], [90, 5000, 5000], {0: [1, 2]}, 7)
+    assert lat.tolist() == [-1, -1] and parent.tolist() == [-1, -1]
+
+
+@native_lib
+@pytest.mark.parametrize("load", [0.7, 1.4])
+@pytest.mark.parametrize("handoff", [0, 130])
+def test_serve_sim_chain_equals_des_traffic(load, handoff):
+    """`traffic` as a two-stage chain on the measured profile: the stage-split SLOs and
+    rates of scenario "traffic-chain" (R28) planned by gl_schedule_files, Poisson SSD
+    app arrivals; every SSD completion spawns one GoogLeNet and one VGG-16 request."""
+    prof = W.parse_profile(open(PROFILE).read())
+    lat_env = prof["lat"]
+    ssd, goo, vgg = W.NAMES.index("ssd_mobilenet_v1"), W.NAMES.index("googlenet"), W.NAMES.index("vgg16")
+    x = 1.0
+    for _ in range(12):
+        head, dump, ok, _ = gpulet.schedule_files(PROFILE, COEFFS, {"scenario": "traffic-chain", "x": x,
+                                                                    "handoff_us": handoff, "mode": "gpulet", "num_gpus": 2})
+        if ok:
+            break
+        x /= 2
+    assert ok
+    s_app = head["app_slo_us"]
+    assert head["slo_us"][ssd] + head["slo_us"][goo] + handoff == s_app
+    plan, lanes = _lanes_from_plan(dump, lat_env)
+    slo = list(head["slo_us"])
+    slo[goo] = slo[vgg] = s_app                    # from the application's arrival
+    t, m = _poisson([0, 0, 0, head["rates"][ssd] * load, 0, 0], 0.3, seed=7 + handoff)
+    lat_n, log_n, par_n, mdl_n = gpulet.serve_sim_chain(lanes, 6, t, m, slo, {ssd: [goo, vgg]}, handoff)
+    lat_o, log_o, par_o, mdl_o = des.simulate_trace(plan, osched.Profile(W.NAMES, lat_env), slo,
+                                                    list(zip(t.tolist(), m.tolist())), spawn={ssd: [goo, vgg]},
+                                                    handoff_us=handoff)
+    assert log_n == log_o and lat_n.tolist() == lat_o
+    assert par_n.tolist() == par_o and mdl_n.tolist() == mdl_o
+    assert len(lat_o) == len(t) + 2 * sum(1 for x in lat_o[:len(t)] if x >= 0)
+    assert len(log_o) > 10

@@ -54,3 +54,29 @@ def test_serve_e2e_zero_copy_and_copy_paths():
             ctx.destroy_gpulet(gid)
     finally:
         ctx.close()
+
+
+def test_serve_chain_spawns_after_completion():
+    """gl_serve_chain on a live gpu-let (F3, DESIGN R28): every completed first-stage
+    request spawns two second-stage requests that arrive handoff_us after its
+    completion; latencies are measured from the application's arrival."""
+    import torch
+    from paper_2109_01611_b200 import gpulet
+    ctx = gpulet.Context(1)
+    try:
+        mid = ctx.load_model(0, "lenet5", synthgen.weight_file("lenet5"))
+        (gid, _n), = ctx.create_gpulets(0, [100])
+        x = torch.zeros(ctx.model_io(mid, 32)[0] // 2, dtype=torch.bfloat16, device="cuda")
+        lanes = [dict(gpulet=gid, model_id=mid, model_slot=s, batch=b, duty_us=200, weight=1, drop_us=0, x=x,
+                      y=torch.empty(ctx.model_io(mid, 32)[1] // 4, device="cuda")) for s, b in ((0, 4), (1, 8))]
+        t = (np.arange(20) * 1000).astype(np.int64)
+        m = np.zeros(20, np.int32)
+        lat, parent, model = ctx.serve_chain(lanes, 2, t, m, [10**7, 10**7], {0: [1, 1]}, 300)
+        assert len(lat) == 60 and (lat >= 0).all()
+        assert parent[:20].tolist() == [-1] * 20 and model[20:].tolist() == [1] * 40
+        assert all(parent[i] == (i - 20) // 2 for i in range(20, 60))    # children of completion order
+        for i in range(20, 60):
+            assert lat[i] >= lat[parent[i]] + 300
+        ctx.destroy_gpulet(gid)
+    finally:
+        ctx.close()

@@ -103,3 +103,25 @@ def test_truncation_reported():
     head, verdict = [json.loads(ln) for ln in out.splitlines()]
     assert head["rates"][2] == 0 and not ok and verdict["reason"] == "rate_truncated"
     assert math.floor(600 * 95000 * 0.0008 / 8400) == head["rates"][0] > 0
+
+
+def test_traffic_stage_slos_hand_computed():
+    """R28 on a hand-made table (L at b = 32, 100 %): SSD 1000, GoogLeNet 500, VGG 3000 µs.
+    Rule: s_app = 2 * 3000 (the longest member doubled); s1 = 6000 * 1000 /
+    (1000 + 3000) = 1500; the recognisers get 6000 - 1500 - handoff.  Table: 136 ms
+    (P:791), s1 = 136000 / 4 = 34000.  Rates: floor(100 * 136000 * x / s_app)."""
+    from oracle import workload as W
+    lat = [[[1] * 6 for _ in range(32)] for _ in W.NAMES]
+    for m, v in (("ssd_mobilenet_v1", 1000), ("googlenet", 500), ("vgg16", 3000)):
+        lat[W.NAMES.index(m)][31][5] = v
+    assert W.traffic_stage_slos(lat, "rule") == (6000, 1500)
+    assert W.traffic_stage_slos(lat, "table") == (136000, 34000)
+    slo, rates, s_app = W.chain_workload(lat, "rule", x=0.5, num_gpus=2, handoff_us=100)
+    i = W.NAMES.index
+    assert s_app == 6000 and slo[i("ssd_mobilenet_v1")] == 1500
+    assert slo[i("googlenet")] == slo[i("vgg16")] == 4400
+    assert rates[i("ssd_mobilenet_v1")] == rates[i("vgg16")] == (100 * 136000 // 2 // 6000) * 2 == 2266
+    assert rates[i("lenet5")] == rates[i("resnet50")] == rates[i("bert_base")] == 0
+    import pytest
+    with pytest.raises(W.WorkloadError):
+        W.traffic_stage_slos(lat, "rule", handoff_us=4500)

@@ -175,3 +175,22 @@ def test_workload_json_errors():
         assert code in (-9, -1), bad
     with pytest.raises(gpulet.GpuletError):
         gpulet.schedule_files(PROFILE, None, {"scenario": "game", "mode": "gpulet+int"})   # needs coefficients
+
+
+@pytest.mark.parametrize("slo_mode", ["rule", "table"])
+@pytest.mark.parametrize("mode", ["gpulet", "gpulet+int", "sbp"])
+def test_traffic_chain_identical(mode, slo_mode):
+    """Scenario "traffic-chain" (F3, DESIGN R28): stage-split SLOs (header app_slo_us),
+    app-SLO-scaled rates and the plan, byte-identical, with and without a hand-off
+    reservation; gl_workload_rates agrees with the oracle (hand-off 0)."""
+    for n in (1, 2, 4):
+        for x in (0.01, 0.2, 0.9, 2.5):
+            for h in (0, 130):
+                wl = {"scenario": "traffic-chain", "x": x, "num_gpus": n, "mode": mode, "slo_mode": slo_mode,
+                      "handoff_us": h}
+                assert _native(PROFILE, COEFFS, wl) == _oracle(PROFILE, COEFFS, wl), wl
+    lat, *_ = gpulet.profile_load(PROFILE)
+    ref_lat = W.parse_profile(_read(PROFILE))["lat"]
+    slo, rates = gpulet.workload_rates(lat, "traffic-chain", 0.7, 2, slo_mode)
+    ref_slo, ref_rates, _s_app = W.chain_workload(ref_lat, slo_mode, 0.7, 2)
+    assert slo == ref_slo and rates == ref_rates
