@@ -21,7 +21,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3, "sbp50": 4}
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_create_gpulets_unconfined", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
-           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_schedule", "gl_profile_load",
+           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_serve_chain", "gl_serve_sim_chain", "gl_schedule", "gl_profile_load",
            "gl_workload_rates", "gl_schedule_files", "gl_bw_probe", "gl_floor", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
            "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
 
