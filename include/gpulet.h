@@ -182,7 +182,9 @@ typedef struct {
   int32_t duty_us;      /* duty cycle D of the gpu-let (dispatch when the window is this old) */
   int32_t weight;       /* routing weight = assigned rate (smooth weighted round-robin) */
   int32_t drop_us;      /* Leff(1): a request with (now - arrival) + drop_us > SLO is dropped */
-  int32_t pad_;
+  int32_t margin_us;    /* >= 0: the deadline guard fires this much earlier (a reserve for the host /
+                           PCIe jitter between the profile's median latency and a real completion;
+                           DESIGN R29); 0 = the rule as written */
   const void* in_dev;   /* device input holding `batch` requests (first k used for a k-batch) */
   void* out_dev;        /* device output */
   const void* in_host;  /* NULL, or pinned host inputs (end-to-end mode): the k requests of a batch are
@@ -222,7 +224,7 @@ typedef struct {
 /* Dispatch rule (SURVEY §8(c) C2.11 + DESIGN R26), shared by gl_serve and gl_serve_sim:
  * at time t a lane with a non-empty FIFO dispatches when (a) it holds >= batch requests,
  * (b) t - window_open >= duty_us, or (c) t - arrival(oldest) + Leff(min(queued, batch))
- * >= SLO.  Dispatching first drops every queued request with (t - arrival) + Leff(1) > SLO
+ * + margin_us >= SLO.  Dispatching first drops every queued request with (t - arrival) + Leff(1) > SLO
  * (a drop is a violation), reopens the window at t and sends the
  * min(queued, batch) oldest requests.  Arrivals are routed (smooth weighted round-robin
  * over the model's lanes, weights = assigned rates, first maximum wins) before the lanes

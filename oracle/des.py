@@ -43,8 +43,9 @@ def arrivals_poisson(rate, duration_us, seed):
 
 
 class Lane:
-    def __init__(self, gl, m, rate, batch, F, D, size):
+    def __init__(self, gl, m, rate, batch, F, D, size, margin=0):
         self.gl, self.m, self.rate, self.b, self.F, self.D, self.size = gl, m, rate, batch, F, D, size
+        self.margin = margin  # DESIGN R29: the deadline guard fires `margin` µs earlier (0: the rule as written)
         self.q = []          # request indices, oldest first
         self.window = 0      # the duty-cycle window opened at the previous dispatch
         self.cur = 0         # smooth weighted round-robin credit
@@ -64,7 +65,8 @@ def simulate_trace(plan_gpulets, prof, slo, trace, spawn=None, handoff_us=0):
         wins); the chosen lane then loses the model's total rate;
       * at time t a lane with queued requests dispatches if it holds >= b
         requests, or t - window >= D, or t - arrival(oldest) + Leff(min(q, b))
-        >= SLO (the batch it would send could otherwise not finish in time);
+        + margin >= SLO (the batch it would send could otherwise not finish in
+        time; margin = the lane's jitter reserve, DESIGN R29, 0 by default);
       * a dispatch drops every queued request with (t - arrival) + Leff(1) >
         SLO, reopens the window at t, and sends the min(q, b) oldest
         requests; the lane is checked again at the same t;
@@ -89,10 +91,10 @@ def simulate_trace(plan_gpulets, prof, slo, trace, spawn=None, handoff_us=0):
     """
     lanes, by_model = [], {}
     for gi, (size, D, ls) in enumerate(plan_gpulets):
-        for (m, rate, b, F) in ls:
-            ln = Lane(gi, m, rate, b, F, D, size)
+        for lt in ls:   # (m, rate, b, F) or (m, rate, b, F, margin_us)
+            ln = Lane(gi, *lt[:4], D, size, *lt[4:5])
             lanes.append(ln)
-            by_model.setdefault(m, []).append(ln)
+            by_model.setdefault(ln.m, []).append(ln)
     free = [0] * len(plan_gpulets)
     arr = [t for t, _m in trace]          # arrival of the request's root (deadlines, drops, latency)
     model = [m for _t, m in trace]
@@ -109,13 +111,13 @@ def simulate_trace(plan_gpulets, prof, slo, trace, spawn=None, handoff_us=0):
             return False
         k = min(len(ln.q), ln.b)
         return (len(ln.q) >= ln.b or t - ln.window >= ln.D
-                or t - arr[ln.q[0]] + leff(ln, k) >= slo[ln.m])
+                or t - arr[ln.q[0]] + leff(ln, k) + ln.margin >= slo[ln.m])
 
     def first_ready_time(ln):
         if not ln.q:
             return None
         k = min(len(ln.q), ln.b)
-        return min(ln.window + ln.D, arr[ln.q[0]] + slo[ln.m] - leff(ln, k))
+        return min(ln.window + ln.D, arr[ln.q[0]] + slo[ln.m] - leff(ln, k) - ln.margin)
 
     def route(r):
         cand = by_model.get(model[r], [])

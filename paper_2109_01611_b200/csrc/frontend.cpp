@@ -108,13 +108,14 @@ struct Policy {
     if (ln.q.empty()) return false;
     if ((int)ln.q.size() >= ln.cfg.batch) return true;                    // batch formed
     if (now - ln.window_us >= ln.cfg.duty_us) return true;                // duty cycle passed
-    return now - arr[ln.q.front()] + ln.leff(ln.next_k()) >= slo_of(ln);  // deadline guard (R26)
+    return now - arr[ln.q.front()] + ln.leff(ln.next_k()) + ln.cfg.margin_us >= slo_of(ln);  // guard (R26, R29)
   }
   // earliest time > now at which ready() turns true with no new arrival (INT64_MAX: never)
   int64_t deadline(int li) const {
     const LaneT& ln = L[li];
     if (ln.q.empty()) return INT64_MAX;
-    return std::min<int64_t>(ln.window_us + ln.cfg.duty_us, arr[ln.q.front()] + slo_of(ln) - ln.leff(ln.next_k()));
+    return std::min<int64_t>(ln.window_us + ln.cfg.duty_us,
+                             arr[ln.q.front()] + slo_of(ln) - ln.leff(ln.next_k()) - ln.cfg.margin_us);
   }
   // the dispatch itself: drop hopeless requests (-> dropped), reopen the window;
   // returns the batch size k (the caller takes the k oldest from q; 0 = emptied)
@@ -298,7 +299,8 @@ static gl_status serve_impl(gl_ctx* ctx, const gl_lane* lanes, int32_t n_lanes, 
   RtGuard rt;
   for (int i = 0; i < n_lanes; ++i) {
     L[i].cfg = lanes[i];
-    if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models || lanes[i].batch < 1 || lanes[i].batch > 32)
+    if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models || lanes[i].batch < 1 || lanes[i].batch > 32 ||
+        lanes[i].margin_us < 0)
       return GL_E_ARG;
     if (lanes[i].in_host) {
       if (!lanes[i].out_host || lanes[i].in_req_bytes <= 0 || lanes[i].out_req_bytes <= 0 || lanes[i].host_slots < 1)
@@ -506,7 +508,7 @@ static gl_status serve_sim_impl(const gl_lane* lanes, int32_t n_lanes, int32_t n
   for (int i = 0; i < n_lanes; ++i) {
     L[i].cfg = lanes[i];
     if (lanes[i].model_slot < 0 || lanes[i].model_slot >= n_models || !lanes[i].leff_us || lanes[i].batch < 1 ||
-        lanes[i].batch > 32 || lanes[i].duty_us < 0)
+        lanes[i].batch > 32 || lanes[i].duty_us < 0 || lanes[i].margin_us < 0)
       return gl::set_error(GL_E_ARG, "gl_serve_sim: bad lane");
     free_at[lanes[i].gpulet] = 0;
   }

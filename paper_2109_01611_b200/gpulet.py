@@ -49,7 +49,7 @@ class SchedInput(ctypes.Structure):
 class Lane(ctypes.Structure):
     _fields_ = [("gpulet", ctypes.c_int32), ("model_id", ctypes.c_int32), ("model_slot", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("duty_us", ctypes.c_int32), ("weight", ctypes.c_int32),
-                ("drop_us", ctypes.c_int32), ("pad_", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
+                ("drop_us", ctypes.c_int32), ("margin_us", ctypes.c_int32), ("in_dev", ctypes.c_void_p),
                 ("out_dev", ctypes.c_void_p), ("in_host", ctypes.c_void_p), ("out_host", ctypes.c_void_p),
                 ("in_req_bytes", ctypes.c_int64), ("out_req_bytes", ctypes.c_int64), ("host_slots", ctypes.c_int32),
                 ("pad2_", ctypes.c_int32), ("in_dev2", ctypes.c_void_p), ("out_dev2", ctypes.c_void_p),
@@ -161,6 +161,7 @@ def _lanes(lanes):
     for i, d in enumerate(lanes):
         L[i].gpulet, L[i].model_id, L[i].model_slot = d["gpulet"], d.get("model_id", 0), d["model_slot"]
         L[i].batch, L[i].duty_us, L[i].weight, L[i].drop_us = d["batch"], d["duty_us"], d["weight"], d["drop_us"]
+        L[i].margin_us = d.get("margin_us", 0)
         if d.get("leff_us") is not None:
             a = np.ascontiguousarray(d["leff_us"], dtype=np.int32)
             assert a.size == 32

@@ -9,3 +9,5 @@ for f in 0 2 1 4 8; do
   timeout 120 python tools/oneshot.py --model resnet50 --batch 32 --flags $f --json gpurun_out/trace_${TAG}_resnet50_b32_f$f.json > gpurun_out/oneshot_${TAG}_f$f.log 2>&1
 done
 timeout 900 python tools/consolidate.py --secs 1.0 --json gpurun_out/consolidate_$TAG.json > gpurun_out/consolidate_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/consolidate_$TAG.log
+timeout 300 python -m pytest tests/test_gpu_serve.py -m gpu -q > gpurun_out/gputests_serve_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/gputests_serve_$TAG.log
+timeout 1200 python tools/traffic_serve.py --json gpurun_out/traffic_serve_$TAG.json > gpurun_out/traffic_serve_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/traffic_serve_$TAG.log

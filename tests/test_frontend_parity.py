@@ -137,6 +137,16 @@ def test_chain_empty_spawn_is_plain():
     assert (lat0, log0) == (lat1, log1) and parent == [-1] * 3 and model == [0, 0, 0]
 
 
+def test_guard_margin():
+    """R29: a lone request (b = 4, long duty cycle, L = 100, SLO 500) is sent by the
+    deadline guard at t = 500 - 100 = 400 (ends at the SLO); with a 50 µs margin at
+    t = 350 (ends 50 µs inside it)."""
+    lat, log = des.simulate_trace([(100, 10**6, [(0, 1, 4, 1000)])], Flat([100] * 32), [500], [(0, 0)])
+    assert lat == [500] and log == [(0, 400, 1, 0)]
+    lat, log = des.simulate_trace([(100, 10**6, [(0, 1, 4, 1000, 50)])], Flat([100] * 32), [500], [(0, 0)])
+    assert lat == [450] and log == [(0, 350, 1, 0)]
+
+
 # ---- native gl_serve_sim == oracle DES ------------------------------------------------------------
 def _lanes_from_plan(dump, prof_lat):
     plan, lanes = [], []
@@ -188,6 +198,11 @@ def test_serve_sim_equals_des(scen, mode, x, n, load):
         x /= 2
     assert ok
     plan, lanes = _lanes_from_plan(dump, prof["lat"])
+    if load > 1:   # overload case: every lane with a jitter reserve (R29), same on both sides
+        mg = [(3 * i + 1) % 7 for i in range(len(lanes))]     # lane i of the plan order, both sides
+        it = iter(mg)
+        plan = [(sz, D, [lt + (next(it),) for lt in ls]) for sz, D, ls in plan]
+        lanes = [dict(ln, margin_us=g) for ln, g in zip(lanes, mg)]
     rates = [r * load for r in head["rates"]]
     t, m = _poisson(rates, 0.2, seed=int(100 * x) + int(10 * load))
     lat_n, log_n = gpulet.serve_sim(lanes, 6, t, m, head["slo_us"])

@@ -43,16 +43,19 @@ def main():
         print(f"floor {p}% ({n} SMs): host {h:.2f} us, device {d:.2f} us", flush=True)
         ctx.destroy_gpulet(gid)
     (gid, n), = ctx.create_gpulets(0, [100])
+    print("cfg1: gpu-let created", flush=True)
     x = common.device_input("lenet5", 32)
     y = torch.empty(ctx.model_io(mid, 32)[1] // 4, device="cuda")
     torch.cuda.synchronize()
     tickets = [ctx.submit_batch(gid, mid, x, y, 32, 5.0) for _ in range(10)]
     for t in tickets:
         ctx.wait(t)
+    print("cfg1: warm-up done", flush=True)
     dev = []
     for _ in range(1000):
         c = ctx.wait(ctx.submit_batch(gid, mid, x, y, 32, 5.0))
         dev.append((c.t_end_ns - c.t_start_ns) / 1e3)
+    print("cfg1: 1000 batches done", flush=True)
     host = ctx.profile(gid, mid, 32, x, y, 10, 200)
     dev = np.asarray(dev)
     out["cfg1_lenet5_b32"] = {"sm": n, "device_us_median": round(float(np.median(dev)), 2),
