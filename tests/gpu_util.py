@@ -54,3 +54,15 @@ def split_outputs(model, y, b):
         pooled = bits_to_f64(y32.view(np.uint16)[off // 2: off // 2 + b * 768]).reshape(b, 768)
         return {"logits": y32[: 2 * b].astype(np.float64).reshape(b, 2), "pooled": pooled}
     return {"logits": np.asarray(y, np.float64).reshape(b, -1)}
+
+
+def bert_logit_bound(pooled_ref):
+    """Per-element tolerance of BERT's 2 logits (DESIGN R30): REL_TOL times the
+    magnitude of the terms the logit sums, sum_k |pooled_k W_ck| (+ |b_c|).  The
+    logits (|l| ~ 0.2) are a near-cancelling sum of terms ~30x larger, so a
+    relative bound on the logits themselves measures the cancellation, not the
+    kernels; the pooled vector they come from is checked at REL_TOL as is."""
+    import synthgen
+    w = synthgen.weights("bert_base")
+    W, b = bits_to_f64(w["cls.w"]), bits_to_f64(w["cls.b"])
+    return REL_TOL * (np.abs(np.asarray(pooled_ref, np.float64)) @ np.abs(W).T + np.abs(b))

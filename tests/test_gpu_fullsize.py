@@ -9,7 +9,7 @@ import pytest
 
 import synthgen
 from oracle import models as omodels
-from tests.gpu_util import REL_TOL, rel_err, split_outputs
+from tests.gpu_util import REL_TOL, bert_logit_bound, rel_err, split_outputs
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,11 @@ def _check(m, got, b, idx, batch_id):
     ref = omodels.forward(m, synthgen.weights(m), x)
     out = split_outputs(m, got, b)
     for k in ref:
-        assert rel_err(out[k][list(idx)], ref[k].reshape(out[k][list(idx)].shape)) <= REL_TOL, (m, k)
+        mine = out[k][list(idx)]
+        if m == "bert_base" and k == "logits":   # R30
+            assert (np.abs(mine - ref[k].reshape(mine.shape)) <= bert_logit_bound(ref["pooled"])).all()
+        else:
+            assert rel_err(mine, ref[k].reshape(mine.shape)) <= REL_TOL, (m, k)
 
 
 @pytest.mark.parametrize("m", ["googlenet", "resnet50", "ssd_mobilenet_v1", "vgg16", "bert_base"])

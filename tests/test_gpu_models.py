@@ -7,7 +7,8 @@ import pytest
 
 import synthgen
 from oracle import models as omodels
-from tests.gpu_util import REL_TOL, TOP1_TOL, rel_err, split_outputs, to_dev_bf16, top1_agreement
+from tests.gpu_util import (REL_TOL, TOP1_TOL, bert_logit_bound, rel_err, split_outputs, to_dev_bf16,
+                            top1_agreement)
 
 pytestmark = pytest.mark.gpu
 
@@ -59,8 +60,11 @@ def test_model_parity(served, model):
         assert judged >= TOP1_TOL, (strict, judged, amb)
     else:
         ref_l, got_l = ref["logits"], out["logits"].reshape(ref["logits"].shape)
-        e = rel_err(got_l, ref_l)
-        assert e <= REL_TOL, e
+        if model == "bert_base":   # R30
+            assert (np.abs(got_l - ref_l) <= bert_logit_bound(ref["pooled"])).all()
+        else:
+            e = rel_err(got_l, ref_l)
+            assert e <= REL_TOL, e
         err = np.abs(got_l - ref_l).max()
         strict, judged, amb = top1_agreement(got_l, ref_l, 4 * err)
         assert judged >= TOP1_TOL, (strict, judged, amb)
