@@ -65,10 +65,13 @@ def test_serve_chain_spawns_after_completion():
     ctx = gpulet.Context(1)
     try:
         mid = ctx.load_model(0, "lenet5", synthgen.weight_file("lenet5"))
-        (gid, _n), = ctx.create_gpulets(0, [100])
+        # device buffers first: a whole-GPU executor leaves no SM for torch's fill kernels
         x = torch.zeros(ctx.model_io(mid, 32)[0] // 2, dtype=torch.bfloat16, device="cuda")
+        ys = [torch.empty(ctx.model_io(mid, 32)[1] // 4, device="cuda") for _ in range(2)]
+        torch.cuda.synchronize()
+        (gid, _n), = ctx.create_gpulets(0, [100])
         lanes = [dict(gpulet=gid, model_id=mid, model_slot=s, batch=b, duty_us=200, weight=1, drop_us=0, x=x,
-                      y=torch.empty(ctx.model_io(mid, 32)[1] // 4, device="cuda")) for s, b in ((0, 4), (1, 8))]
+                      y=y) for (s, b), y in zip(((0, 4), (1, 8)), ys)]
         t = (np.arange(20) * 1000).astype(np.int64)
         m = np.zeros(20, np.int32)
         lat, parent, model = ctx.serve_chain(lanes, 2, t, m, [10**7, 10**7], {0: [1, 1]}, 300)

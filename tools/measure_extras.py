@@ -42,11 +42,12 @@ def main():
         out["floor"][str(p)] = {"sm": n, "host_round_trip_us": round(h, 2), "device_us": round(d, 2)}
         print(f"floor {p}% ({n} SMs): host {h:.2f} us, device {d:.2f} us", flush=True)
         ctx.destroy_gpulet(gid)
-    (gid, n), = ctx.create_gpulets(0, [100])
-    print("cfg1: gpu-let created", flush=True)
+    # device buffers before the executor: a whole-GPU executor leaves no SM for torch's kernels
     x = common.device_input("lenet5", 32)
     y = torch.empty(ctx.model_io(mid, 32)[1] // 4, device="cuda")
     torch.cuda.synchronize()
+    (gid, n), = ctx.create_gpulets(0, [100])
+    print("cfg1: gpu-let created", flush=True)
     tickets = [ctx.submit_batch(gid, mid, x, y, 32, 5.0) for _ in range(10)]
     for t in tickets:
         ctx.wait(t)
