@@ -518,7 +518,10 @@ def run_mode(srv, dist, rank, world, scen, mode, a, clocks=False):
             srv.teardown()
         worst = max(r["viol_frac"] for r in runs)
         attempts.append({"x": round(x, 4), "viol_frac": [round(r["viol_frac"], 4) for r in runs],
-                         "value": [round(r["value"], 1) for r in runs]})
+                         "value": [round(r["value"], 1) for r in runs],
+                         # violations of every window, run by run: bursts (one window) vs a load-driven rise
+                         "viol_per_window": [[w["viol"] for w in wins[k * a.steps:(k + 1) * a.steps]]
+                                             for k in range(len(runs))]})
         if worst <= 0.01:
             break
         x *= 0.96
@@ -831,7 +834,7 @@ def main():
     ap.add_argument("--scenario", default="game")
     ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
     ap.add_argument("--repeats", type=int, default=3, help="timed runs of --steps windows (value = the median)")
-    ap.add_argument("--retries", type=int, default=4, help="x lowered by 4 %% while a timed run violates > 1 %%")
+    ap.add_argument("--retries", type=int, default=8, help="x lowered by 4 %% while a timed run violates > 1 %%")
     ap.add_argument("--probe-window", type=float, default=0.5, help="seconds per probe run (3 runs per probe)")
     ap.add_argument("--probes", type=int, default=6)
     ap.add_argument("--slo-mode", default="rule", choices=["rule", "table"])

@@ -152,6 +152,14 @@ gl_status gl_profile(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t b
  * (GL_E_STATE).  Errors: GL_E_ARG, GL_E_GRID, GL_E_STATE, GL_E_CUDA. */
 gl_status gl_bw_probe(gl_ctx* ctx, int gpu, int sm_pct, int64_t bytes, int32_t reps, double* gbs, int32_t* sm_count);
 
+/* Work-ring placement check (north_star "work queues in device memory"): the host
+ * round trip of publishing one 64-B work descriptor into device memory -- an async
+ * 64-B H2D copy on a non-blocking stream plus its completion -- median and p99 over
+ * `reps` (>= 10) after 10 warm-up copies.  The executor's host ring (pinned, mapped)
+ * needs only a host store; compare with gl_floor's whole round trip (descriptor ->
+ * executor -> completion seen by the host).  Errors: GL_E_ARG, GL_E_CUDA. */
+gl_status gl_publish_probe(gl_ctx* ctx, int gpu, int32_t reps, double* memcpy_us, double* memcpy_p99_us);
+
 /* Executor floor: `warmup` + `reps` descriptors with an empty
  * program (no layer step) through gpulet_id's ring, one in flight, as gl_profile
  * measures a batch.  Out: *host_us = median submit -> completion visible to the

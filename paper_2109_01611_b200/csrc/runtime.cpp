@@ -1110,6 +1110,39 @@ gl_status gl_test_stats(uint64_t* ns, uint64_t* timeline, int32_t cap, int32_t* 
   return GL_OK;
 }
 
+// Cost of publishing one 64-B work descriptor into DEVICE memory, the alternative to
+// the host-mapped ring (include/gpulet.h gl_publish_probe).
+gl_status gl_publish_probe(gl_ctx* ctx, int gpu, int32_t reps, double* memcpy_us, double* memcpy_p99_us) {
+  if (!ctx || gpu < 0 || gpu >= (int)ctx->gpus.size() || !memcpy_us || reps < 10)
+    return fail(GL_E_ARG, "gl_publish_probe: bad arguments");
+  CK(cudaSetDevice(ctx->gpus[gpu].dev), "cudaSetDevice");
+  WorkDesc* h = nullptr;
+  WorkDesc* d = nullptr;
+  cudaStream_t st = nullptr;
+  CK(cudaHostAlloc(&h, sizeof(WorkDesc), cudaHostAllocDefault), "cudaHostAlloc(probe)");
+  CK(cudaMalloc(&d, sizeof(WorkDesc)), "cudaMalloc(probe)");
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  std::memset((void*)h, 0, sizeof(WorkDesc));
+  std::vector<double> t;
+  gl_status rc = GL_OK;
+  for (int i = 0; i < reps + 10 && rc == GL_OK; ++i) {
+    h->ticket = (uint64_t)i;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (cudaMemcpyAsync(d, h, sizeof(WorkDesc), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      rc = fail(GL_E_CUDA, "gl_publish_probe: copy");
+    if (i >= 10) t.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+  cudaStreamDestroy(st);
+  cudaFree(d);
+  cudaFreeHost(h);
+  if (rc) return rc;
+  std::sort(t.begin(), t.end());
+  *memcpy_us = t[t.size() / 2];
+  if (memcpy_p99_us) *memcpy_p99_us = t[(t.size() * 99) / 100];
+  return GL_OK;
+}
+
 // K12 HBM probe on the SMs of a gpu-let size (include/gpulet.h gl_bw_probe).
 gl_status gl_bw_probe(gl_ctx* ctx, int gpu, int sm_pct, int64_t bytes, int32_t reps, double* gbs, int32_t* sm_count) {
   if (!ctx || gpu < 0 || gpu >= (int)ctx->gpus.size() || !gbs || bytes < (1 << 20) || reps < 1)

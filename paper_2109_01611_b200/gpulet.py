@@ -22,7 +22,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3, "sbp50": 4}
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_create_gpulets_unconfined", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
            "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_serve_chain", "gl_serve_sim_chain", "gl_schedule", "gl_profile_load",
-           "gl_workload_rates", "gl_schedule_files", "gl_bw_probe", "gl_floor", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
+           "gl_workload_rates", "gl_schedule_files", "gl_bw_probe", "gl_publish_probe", "gl_floor", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
            "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
 
 
@@ -114,6 +114,7 @@ def lib():
             "gl_schedule_files": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t,
                                   ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I32)],
             "gl_fit_interference": [ctypes.POINTER(D), ctypes.POINTER(D), I32, ctypes.POINTER(D)],
+            "gl_publish_probe": [P, ctypes.c_int, I32, ctypes.POINTER(D), ctypes.POINTER(D)],
             "gl_floor": [P, I32, I32, I32, ctypes.POINTER(D), ctypes.POINTER(D)],
             "gl_bw_probe": [P, ctypes.c_int, ctypes.c_int, I64, I32, ctypes.POINTER(D), ctypes.POINTER(I32)],
             "gl_test_gemm": [P, ctypes.c_int, P, P, P, P, I32, I32, I32, I32, I32, I32, I32, I32],
@@ -400,6 +401,12 @@ class Context:
         h, d = ctypes.c_double(), ctypes.c_double()
         _check(lib().gl_floor(self.h, gid, warmup, reps, ctypes.byref(h), ctypes.byref(d)))
         return h.value, d.value
+
+    def publish_probe(self, gpu=0, reps=1000):
+        """gl_publish_probe -> (median, p99) µs of a 64-B descriptor H2D copy + completion."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(lib().gl_publish_probe(self.h, gpu, reps, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def bw_probe(self, gpu, sm_pct, nbytes=1 << 30, reps=10):
         """gl_bw_probe -> (GB/s read + write, SMs)."""

@@ -36,6 +36,11 @@ def main():
         gbs, n = ctx.bw_probe(0, p, a.bytes, 10)
         out["bw_probe"][str(p)] = {"sm": n, "gbs": round(gbs, 1)}
         print(f"BW({n} SMs, {p}%) = {gbs:.1f} GB/s", flush=True)
+    med, p99 = ctx.publish_probe(0, 1000)
+    out["publish_probe"] = {"h2d_64B_copy_us_median": round(med, 2), "p99": round(p99, 2),
+                            "note": "host round trip of publishing one work descriptor into device memory; "
+                                    "compare with the floor's whole host round trip through the mapped ring"}
+    print(f"publish 64 B descriptor by H2D copy: median {med:.2f} us, p99 {p99:.2f} us", flush=True)
     for p in common.GRID:
         (gid, n), = ctx.create_gpulets(0, [p])
         h, d = ctx.floor(gid, 20, 500)
