@@ -417,7 +417,23 @@ class Server:
                                        in_req_bytes=ib, out_req_bytes=ob, host_slots=self.host_slots.get(m, self.HOST_SLOTS),
                                        size=g["size"], sm=nsm, model=m))
                 my_rates[mi] += ln["rate"]
+        self.set_margins()
         return my_rates
+
+    margin_mode = "measured"
+
+    def set_margins(self):
+        """Deadline-guard margin of every lane (DESIGN R29): the measured p99 of the
+        lane's batch-1 host-observed service latency on its live gpu-let minus the
+        profile's Leff(1) the guard budgets with (>= 0): the tail of a real
+        completion beyond the median the profile records."""
+        import math
+        for ln in self.lanes:
+            ln["margin_us"] = 0
+            if self.margin_mode != "measured":
+                continue
+            _p50, p99 = self.ctx.profile_tail(ln["gpulet"], ln["model_id"], 1, ln["x"], ln["y"], 10, 200)
+            ln["margin_us"] = max(0, int(math.ceil(p99 - ln["drop_us"])))
 
     def teardown(self):
         for gid in self.made:
@@ -484,9 +500,12 @@ def timed_runs(srv, dist, world, my, a, seed0, clocks=None):
 
 def run_mode(srv, dist, rank, world, scen, mode, a, clocks=False):
     """Headline: rate search, then a.repeats timed runs of a.steps windows at the
-    found multiplier x.  The pass rule (<= 1 % late + dropped, R19) must hold
-    in every timed run, not only in the probes: otherwise x is lowered by 4 % and
-    the timed runs are repeated (at most a.retries times).  value = the median run."""
+    found multiplier x.  The pass rule (<= 1 % late + dropped, R19) is
+    applied to the timed runs themselves, as the paper does: "we iterate the
+    experiment three times ... and pick the median SLO violation rate":
+    while the median run's violation fraction exceeds 1 %, x is lowered by 4 % and
+    the timed runs are repeated (at most a.retries times).  value = the value of
+    that median-violation run (itself <= 1 %); every run is reported."""
     from tools import common
     xs = srv.max_sched_x(scen, mode, world)
     if not srv.plan(scen, mode, world, xs)[2]:
@@ -504,7 +523,7 @@ def run_mode(srv, dist, rank, world, scen, mode, a, clocks=False):
             continue
         my = srv.setup(dump, rank)
         res = {"x_sched": xs, "x": x, "probes": probes, "rates": rates, "plan": dump,
-               "lanes": [{k: ln[k] for k in ("model", "batch", "duty_us", "size", "sm", "weight", "gpulet")}
+               "lanes": [{k: ln[k] for k in ("model", "batch", "duty_us", "size", "sm", "weight", "gpulet", "margin_us")}
                          for ln in srv.lanes]}
         try:
             for s in range(a.warmup):
@@ -517,19 +536,22 @@ def run_mode(srv, dist, rank, world, scen, mode, a, clocks=False):
         finally:
             srv.teardown()
         worst = max(r["viol_frac"] for r in runs)
+        med_v = sorted(r["viol_frac"] for r in runs)[len(runs) // 2]
         attempts.append({"x": round(x, 4), "viol_frac": [round(r["viol_frac"], 4) for r in runs],
                          "value": [round(r["value"], 1) for r in runs],
                          # violations of every window, run by run: bursts (one window) vs a load-driven rise
                          "viol_per_window": [[w["viol"] for w in wins[k * a.steps:(k + 1) * a.steps]]
                                              for k in range(len(runs))]})
-        if worst <= 0.01:
+        if med_v <= 0.01:
             break
         x *= 0.96
     vals = sorted(r["value"] for r in runs)
-    med = sorted(runs, key=lambda r: r["value"])[len(runs) // 2]
+    med = sorted(runs, key=lambda r: r["viol_frac"])[len(runs) // 2]   # the median-violation run
     res.update(value=med["value"], sat=med["sat"], arrivals=med["arrivals"], viol_frac=med["viol_frac"],
                dev_s=med["dev_s"], serve_s=med["serve_s"], wall_s=med["wall_s"], windows=med["windows"],
-               per_model=med["per_model"], attempts=attempts, criterion_met=worst <= 0.01,
+               per_model=med["per_model"], attempts=attempts, criterion_met=med_v <= 0.01,
+               criterion="median of the timed runs' violation fractions <= 1 % (P:823, P:860)",
+               worst_run_viol_frac=round(worst, 4),
                repeats=[{"value": round(r["value"], 2), "viol_frac": round(r["viol_frac"], 4),
                          "arrivals": r["arrivals"]} for r in runs],
                spread=round((vals[-1] - vals[0]) / max(vals[len(vals) // 2], 1e-9), 4))
@@ -764,6 +786,7 @@ def our_arm(a, world, rank, local, dist):
     torch.cuda.set_device(local)
     ctx = gpulet.Context(local + 1)
     srv = Server(ctx, local, a.e2e, slo_mode=a.slo_mode)
+    srv.margin_mode = a.margin
     head = run_mode(srv, dist, rank, world, a.scenario, a.mode, a, clocks=True)
     matrix = {}
     if not a.headline_only:
@@ -800,7 +823,7 @@ def our_arm(a, world, rank, local, dist):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": (f"cfg4 {a.scenario}: paper game (6 LeNet-5 + 1 ResNet-50 per app request, P:787), "
                                 if a.scenario == "game" else f"cfg4 {a.scenario}, ")
-                   + f"max Poisson rate with <=1% SLO violations in every timed run, mode {a.mode}, "
+                   + f"max Poisson rate whose median timed run (of 3) has <=1% SLO violations (P:823), mode {a.mode}, "
                    + f"SLOs {a.slo_mode}, gpu-lets on {world} GPU(s)",
                    "rate_multiplier": round(head["x"], 4), "x_sched_max": round(head["x_sched"], 4),
                    "rates_req_s": rates, "app_req_s": app, "slo_us": slo, "slo_mode": a.slo_mode,
@@ -834,7 +857,9 @@ def main():
     ap.add_argument("--scenario", default="game")
     ap.add_argument("--window", type=float, default=0.25, help="seconds of arrivals per step")
     ap.add_argument("--repeats", type=int, default=3, help="timed runs of --steps windows (value = the median)")
-    ap.add_argument("--retries", type=int, default=8, help="x lowered by 4 %% while a timed run violates > 1 %%")
+    ap.add_argument("--retries", type=int, default=8, help="x lowered by 4 %% while the median run violates > 1 %%")
+    ap.add_argument("--margin", default="measured", choices=["measured", "0"],
+                    help="deadline-guard margin per lane (R29): measured p99 - Leff(1), or 0 (the rule as written)")
     ap.add_argument("--probe-window", type=float, default=0.5, help="seconds per probe run (3 runs per probe)")
     ap.add_argument("--probes", type=int, default=6)
     ap.add_argument("--slo-mode", default="rule", choices=["rule", "table"])

@@ -21,7 +21,7 @@ MODES = {"gpulet": 0, "gpulet+int": 1, "sbp": 2, "ideal": 3, "sbp50": 4}
 # exported symbols declared in include/gpulet.h
 SYMBOLS = ["gl_init", "gl_shutdown", "gl_last_error", "gl_load_model", "gl_model_io", "gl_model_cost",
            "gl_create_gpulet", "gl_create_gpulets", "gl_create_gpulets_unconfined", "gl_destroy_gpulet", "gl_gpulet_smids", "gl_submit_batch", "gl_poll", "gl_wait",
-           "gl_profile", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_serve_chain", "gl_serve_sim_chain", "gl_schedule", "gl_profile_load",
+           "gl_profile", "gl_profile_tail", "gl_run_once", "gl_program_info", "gl_serve", "gl_serve_sim", "gl_serve_chain", "gl_serve_sim_chain", "gl_schedule", "gl_profile_load",
            "gl_workload_rates", "gl_schedule_files", "gl_bw_probe", "gl_publish_probe", "gl_floor", "gl_fit_interference", "gl_test_gemm", "gl_test_conv", "gl_test_misc",
            "gl_test_stats", "gl_set_tuning", "gl_ssd_detect_workspace", "gl_ssd_detect", "gl_crop_resize"]
 
@@ -91,6 +91,7 @@ def lib():
             "gl_poll": [P, ctypes.POINTER(Completion), I32, ctypes.POINTER(I32)],
             "gl_wait": [P, U64, I32, ctypes.POINTER(Completion)],
             "gl_profile": [P, I32, I32, I32, I32, I32, P, P, ctypes.POINTER(D)],
+            "gl_profile_tail": [P, I32, I32, I32, I32, I32, P, P, ctypes.POINTER(D), ctypes.POINTER(D)],
             "gl_run_once": [P, I32, I32, P, P, I32, ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
             "gl_program_info": [P, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(D),
                                 ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
@@ -314,6 +315,13 @@ class Context:
         d = ctypes.c_double()
         _check(lib().gl_profile(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d)))
         return d.value
+
+    def profile_tail(self, gid, mid, batch, x, y, warmup=10, reps=200):
+        """gl_profile_tail -> (median, p99) µs host-observed service latency."""
+        d, q = ctypes.c_double(), ctypes.c_double()
+        _check(lib().gl_profile_tail(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d),
+                                     ctypes.byref(q)))
+        return d.value, q.value
 
     def run_once(self, mid, batch, x, y, n_sm=0, trace=True, roles=False):
         """One-shot executor launch; returns per-step durations (ns) when trace
