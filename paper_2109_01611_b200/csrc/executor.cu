@@ -112,7 +112,9 @@ __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
   if (threadIdx.x == 0) {
     // release-add (orders this CTA's prior writes, made visible CTA-wide by the
     // __syncthreads above), then acquire-poll: tight for the first ~1 us, then
-    // with a short back-off (idle executors wait here for work)
+    // with a short back-off (idle executors wait here for work).  (Counters
+    // spread over 8 lines, CTA b adding to line b % 8 and polling the sum, were
+    // measured 1 us per barrier slower: profiles/ab_r4j_barrier_spread_lines.log)
     const unsigned long long target = (unsigned long long)(epoch + 1) * gridDim.x;
     red_release_gpu_add_u64((unsigned long long*)&st->barrier, 1ull);
     uint32_t spins = 0, ns = 32;
@@ -594,6 +596,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   // after every asm statement (they all clobber "memory")
   const Smem S = Sio;
   Pipe P = Pio;
+#ifdef GL_DBG_START
+  if (threadIdx.x == 0) dbg_mark(S, 2);   // instrumented build: step entry
+#endif
   {
     constexpr int W = (int)sizeof(GemmArgs) / 4;
     const int nc = min(nops, kOpCache);
@@ -602,6 +607,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     for (int i = threadIdx.x; i < nc; i += blockDim.x) S.opn[i] = ops[i].n_units;
     __syncthreads();
   }
+#ifdef GL_DBG_START
+  if (threadIdx.x == 0) dbg_mark(S, 4);   // instrumented build: step args staged
+#endif
   const StepOps so{ops, S.opc, S.opn, nops};
   int total = 0, maxbn = 16;
   bool gstep = false;
@@ -695,6 +703,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     if (t == 0) dbg_mark(S, 1);
   } else if (!gstep && warp == 9) {
     // ---------------- TMA producer (whole warp walks the loop; one elected lane issues)
+#ifdef GL_DBG_START
+    if (lane == 0) dbg_mark(S, 5);          // instrumented build: before the proxy fence
+#endif
     tma_role_fence();
     if (lane == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -769,7 +780,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const uint32_t ko2 = amode == 64 ? 64 : 8192;
       const uint32_t ko3 = amode == 64 ? 96 : amode == 32 ? 8224 : 12288;
       const bool do_mma = !(S.flags & 4);
+#ifndef GL_DBG_START
       if (tile == (int)blockIdx.x && lane == 0) dbg_mark(S, 2);
+#endif
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&S.full[P.stage], par(P));
         if (!(S.flags & 16)) tc_fence_after();
@@ -824,7 +837,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
         c1 = half ? g.BN : split;
       }
       if (lead) tl_mark(S, ntile, 2);
+#ifndef GL_DBG_START
       if (tile == (int)blockIdx.x && lead) dbg_mark(S, 4);
+#endif
       epilogue_cols(g, X, S, taddr, mb, nb, kb0, q, c0, c1, stg, lane, &S.tfull[acc], use & 1, sbias,
                     ((uint32_t)oi << 16) | (uint32_t)nb, bkey);
       if (g.pub_off) {   // this warp's stores of the tile are done: one release per warp
@@ -838,7 +853,9 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       ++ntile;
       ++P.acc;
     }
+#ifndef GL_DBG_START
     if (q == 0 && half == 0 && lane == 0) dbg_mark(S, 5);
+#endif
   }
   // The ring / accumulator state every thread must leave the step with depends
   // on this CTA's tile and k-block counts, which the MMA warp counted as it
