@@ -101,6 +101,14 @@ def main():
         periods, reorg_ms = [], []
         lat_all = np.full(len(t_us), -3, np.int64)
         cur_dump, est = None, None
+        # the server is up before traffic starts (as the paper's is): the first plan is
+        # deployed before the trace clock starts; later changes happen under traffic
+        start = np.array([peak[m] * wave(0.0, a.secs, 0.03 * m) for m in range(M)])
+        want0 = np.asarray(peak, float) if policy == "static-peak" else start * a.headroom
+        dump0, ok0 = plan_for(want0)
+        if ok0:
+            srv.setup(dump0, 0)
+            cur_dump = dump0
         t_glob0 = time.perf_counter()
         for k in range(nper):
             lo, hi = int(k * a.period * 1e6), int((k + 1) * a.period * 1e6)
