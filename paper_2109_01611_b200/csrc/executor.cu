@@ -701,13 +701,17 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     for (int i = 0; i < P.npend; ++i) mbar_arrive(&S.full[P.pend[i]]);
     P.npend = 0;
     if (t == 0) dbg_mark(S, 1);
-  } else if (!gstep && warp == 9) {
-    // ---------------- TMA producer (whole warp walks the loop; one elected lane issues)
+  } else if (!gstep && warp >= 9) {
+    // ---------------- TMA producers (each warp walks the whole loop and every ring
+    // position; warp 9 + p issues the K blocks with index p mod kTmaWarps of this
+    // CTA's step, one elected lane per warp)
+    const int pw = warp - 9;
+    int kbi = 0;
 #ifdef GL_DBG_START
-    if (lane == 0) dbg_mark(S, 5);          // instrumented build: before the proxy fence
+    if (pw == 0 && lane == 0) dbg_mark(S, 5);          // instrumented build: before the proxy fence
 #endif
     tma_role_fence();
-    if (lane == 0) dbg_mark(S, 0);
+    if (pw == 0 && lane == 0) dbg_mark(S, 0);
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int lt;
       const int oi = so.locate(tile, lt);
@@ -734,28 +738,30 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const void* tA = &op->tmap_a;
       const void* tB = &op->tmap_b;
       const bool skip = (S.flags & 8) != 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&S.empty[P.stage], par(P) ^ 1);
-        uint64_t* fb = &S.full[P.stage];
-        if (elect_one()) {
-          if (skip) {
-            mbar_arrive_cnt(fb, 129);
-          } else {
-            const uint32_t sa = ring + P.stage * sbytes;
-            mbar_arrive_expect_tx(fb, tx);
-            if (a2d)
-              tma_load_2d(sa, tA, fb, kb * 64, arow);
-            else
-              im2col_kblock(q, tA, fb, sa, kb, icw, ich, icn);
-            tma_load_2d(sa + kStageBytesA, tB, fb, kb * 64, brow);
-            mbar_arrive_cnt(fb, 128);
+      for (int kb = kb0; kb < kb1; ++kb, ++kbi) {
+        if (kbi % kTmaWarps == pw) {
+          mbar_wait(&S.empty[P.stage], par(P) ^ 1);
+          uint64_t* fb = &S.full[P.stage];
+          if (elect_one()) {
+            if (skip) {
+              mbar_arrive_cnt(fb, 129);
+            } else {
+              const uint32_t sa = ring + P.stage * sbytes;
+              mbar_arrive_expect_tx(fb, tx);
+              if (a2d)
+                tma_load_2d(sa, tA, fb, kb * 64, arow);
+              else
+                im2col_kblock(q, tA, fb, sa, kb, icw, ich, icn);
+              tma_load_2d(sa + kStageBytesA, tB, fb, kb * 64, brow);
+              mbar_arrive_cnt(fb, 128);
+            }
           }
+          __syncwarp();
         }
-        __syncwarp();
         advance(P);
       }
     }
-    if (lane == 0) dbg_mark(S, 1);
+    if (pw == 0 && lane == 0) dbg_mark(S, 1);
   } else if (warp == 8) {
     // ---------------- MMA issuer (whole warp walks the loop; one elected lane issues)
     const uint32_t tbase = *S.tmem_base;

@@ -185,7 +185,15 @@ struct ExecParams {
   uint64_t* tl;                 //   k = 0 MMA start (accumulator acquired), 1 MMA last commit, 2 epilogue start, 3 epilogue end
 };
 
-constexpr int kThreads = 320;   // warps 0-3 gather producers / epilogue, 4-7 epilogue, 8 MMA, 9 TMA producer
+// TMA-producer warps of a TMA-only GEMM step (warps 9 .. 8 + kTmaWarps): one thread
+// issues about one cp.async.bulk.tensor per ~270 ns (measured, tools/tma_micro.cu),
+// so a single producer caps a step at ~0.5 us per 64-wide K block (A + B loads);
+// the producer warps take alternate K blocks.
+#ifndef GL_TMA_WARPS
+#define GL_TMA_WARPS 2
+#endif
+constexpr int kTmaWarps = GL_TMA_WARPS;
+constexpr int kThreads = 288 + 32 * kTmaWarps;   // warps 0-3 gather / epilogue, 4-7 epilogue, 8 MMA, 9.. TMA
 constexpr int kStages = 4;      // fixed stage layout used as scratch by the non-GEMM ops
 constexpr int kStageBytesA = 128 * 128;       // 128 rows x 64 bf16
 constexpr int kStageBytesB = 256 * 128;       // up to 256 rows x 64 bf16
