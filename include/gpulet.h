@@ -141,10 +141,10 @@ gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completio
  * gl_poll. */
 gl_status gl_profile(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t batch, int32_t warmup, int32_t reps,
                      const void* in_dev, void* out_dev, double* median_us);
-/* gl_profile plus the 99th percentile of the same `reps` service latencies (*p99_us,
- * optional): the tail the frontend's deadline-guard margin reserves (DESIGN R29). */
+/* gl_profile plus the q-quantile (0 <= q < 1) of the same `reps` service latencies
+ * (*q_us, optional): the tail the frontend's deadline-guard margin reserves (DESIGN R29). */
 gl_status gl_profile_tail(gl_ctx* ctx, int32_t gpulet_id, int32_t model_id, int32_t batch, int32_t warmup,
-                          int32_t reps, const void* in_dev, void* out_dev, double* median_us, double* p99_us);
+                          int32_t reps, const void* in_dev, void* out_dev, double q, double* median_us, double* q_us);
 
 /* K12 HBM probe (the per-gpu-let HBM roof BW(n) is measured, not
  * assumed to be n/148 of the GPU's): a 16-B grid-stride copy of `bytes` (>= 1 MiB)

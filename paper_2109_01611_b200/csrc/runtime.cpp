@@ -997,14 +997,14 @@ gl_status gl_wait(gl_ctx* ctx, uint64_t ticket, int32_t timeout_ms, gl_completio
 
 gl_status gl_profile(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32_t warmup, int32_t reps,
                      const void* in_dev, void* out_dev, double* median_us) {
-  return gl_profile_tail(ctx, gid, mid, batch, warmup, reps, in_dev, out_dev, median_us, nullptr);
+  return gl_profile_tail(ctx, gid, mid, batch, warmup, reps, in_dev, out_dev, 0.5, median_us, nullptr);
 }
 
 gl_status gl_profile_tail(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, int32_t warmup, int32_t reps,
-                          const void* in_dev, void* out_dev, double* median_us, double* p99_us) {
+                          const void* in_dev, void* out_dev, double q, double* median_us, double* q_us) {
   // Service latency as the frontend sees it: one batch in
   // flight; submit -> its completion record visible to gl_poll (host clock).
-  if (!ctx || !median_us || reps < 1 || warmup < 0) return fail(GL_E_ARG, "gl_profile: bad arguments");
+  if (!ctx || !median_us || reps < 1 || warmup < 0 || !(q >= 0.0 && q < 1.0)) return fail(GL_E_ARG, "gl_profile: bad arguments");
   std::vector<double> lat;
   for (int i = 0; i < warmup + reps; ++i) {
     uint64_t t;
@@ -1030,7 +1030,7 @@ gl_status gl_profile_tail(gl_ctx* ctx, int32_t gid, int32_t mid, int32_t batch, 
   }
   std::sort(lat.begin(), lat.end());
   *median_us = lat[lat.size() / 2];
-  if (p99_us) *p99_us = lat[std::min(lat.size() - 1, (lat.size() * 99) / 100)];
+  if (q_us) *q_us = lat[std::min(lat.size() - 1, (size_t)(q * (double)lat.size()))];
   return GL_OK;
 }
 

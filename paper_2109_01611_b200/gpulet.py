@@ -91,7 +91,7 @@ def lib():
             "gl_poll": [P, ctypes.POINTER(Completion), I32, ctypes.POINTER(I32)],
             "gl_wait": [P, U64, I32, ctypes.POINTER(Completion)],
             "gl_profile": [P, I32, I32, I32, I32, I32, P, P, ctypes.POINTER(D)],
-            "gl_profile_tail": [P, I32, I32, I32, I32, I32, P, P, ctypes.POINTER(D), ctypes.POINTER(D)],
+            "gl_profile_tail": [P, I32, I32, I32, I32, I32, P, P, D, ctypes.POINTER(D), ctypes.POINTER(D)],
             "gl_run_once": [P, I32, I32, P, P, I32, ctypes.POINTER(U64), I32, ctypes.POINTER(I32)],
             "gl_program_info": [P, I32, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(D),
                                 ctypes.POINTER(D), I32, ctypes.POINTER(I32)],
@@ -316,12 +316,12 @@ class Context:
         _check(lib().gl_profile(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d)))
         return d.value
 
-    def profile_tail(self, gid, mid, batch, x, y, warmup=10, reps=200):
-        """gl_profile_tail -> (median, p99) µs host-observed service latency."""
-        d, q = ctypes.c_double(), ctypes.c_double()
-        _check(lib().gl_profile_tail(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), ctypes.byref(d),
-                                     ctypes.byref(q)))
-        return d.value, q.value
+    def profile_tail(self, gid, mid, batch, x, y, warmup=10, reps=200, q=0.99):
+        """gl_profile_tail -> (median, q-quantile) µs host-observed service latency."""
+        d, t = ctypes.c_double(), ctypes.c_double()
+        _check(lib().gl_profile_tail(self.h, gid, mid, batch, warmup, reps, _ptr(x), _ptr(y), float(q),
+                                     ctypes.byref(d), ctypes.byref(t)))
+        return d.value, t.value
 
     def run_once(self, mid, batch, x, y, n_sm=0, trace=True, roles=False):
         """One-shot executor launch; returns per-step durations (ns) when trace
