@@ -94,8 +94,11 @@ gl_status gl_model_cost(gl_ctx* ctx, int32_t model_id, int32_t batch, double* fl
  * Out: *gpulet_id, *sm_count (actual SMs).  Errors: GL_E_GRID, GL_E_PARTITION,
  * GL_E_NOT_CONCURRENT, GL_E_CUDA. */
 gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int sm_pct, int32_t* gpulet_id, int32_t* sm_count);
-/* Create a whole GPU partition of n (1 or 2) gpu-lets, sizes pcts[] summing to <= 100,
- * in slot order.  All green contexts are created before the first executor starts
+/* Create a whole GPU partition of n (1 to 4) gpu-lets, sizes pcts[] summing to <= 100,
+ * in slot order.  With 3-4 gpu-lets (the paper's scheduler uses at
+ * most 2) slot i takes its exact share as a contiguous range of SM pairs from the front,
+ * in slot order; partitions whose exact shares exceed the GPU's SMs (20+20+20+40 %:
+ * 150 > 148) are refused (GL_E_PARTITION).  All green contexts are created before the first executor starts
  * (green-context creation can block behind a running persistent kernel, so this is
  * the way to (re)partition a GPU).  The GPU must have no live gpu-let (GL_E_STATE).
  * Out: ids[n], sm_counts[n] (optional). */

@@ -237,14 +237,18 @@ struct SlotRes {
   std::map<std::pair<int, int>, std::vector<OpDesc*>> progs_sm;
 };
 
+constexpr int kMaxSlots = 4;   // gpu-lets per GPU: 2 by gl_create_gpulet, up to 4 by gl_create_gpulets
+
 struct GpuState {
-  SlotRes slot_res[2];
+  SlotRes slot_res[kMaxSlots];
   bool green_ready = false;
-  CUgreenCtx gctx[2][5] = {};      // [slot][size index of 20,40,50,60,80]
-  CUstream gstream[2][5] = {};
-  int gnsm[2][5] = {};
+  CUgreenCtx gctx[kMaxSlots][5] = {};      // [slot][size index of 20,40,50,60,80]
+  CUstream gstream[kMaxSlots][5] = {};
+  int gnsm[kMaxSlots][5] = {};
   CUstream full_stream = nullptr;  // 100 %: a non-blocking stream of the primary context
-  CUstream ustream[2] = {};        // unconfined executors: one non-blocking primary stream per slot
+  CUstream ustream[kMaxSlots] = {};  // unconfined executors: one non-blocking primary stream per slot
+  bool multi = false;              // a partition of 3-4 gpu-lets: slot s holds SM pairs from layout_pair[s] on
+  int layout_pair[kMaxSlots] = {};
   int dev = 0;
   int nsm = 0;
   bool split = false;
@@ -254,7 +258,12 @@ struct GpuState {
   CUdevResource rem;
   uint32_t used_groups = 0;
   bool rem_used = false;
-  int slots[2] = {-1, -1};
+  int slots[kMaxSlots] = {-1, -1, -1, -1};
+  bool any_live() const {
+    for (int s : slots)
+      if (s >= 0) return true;
+    return false;
+  }
 };
 
 struct gl_ctx {
@@ -359,9 +368,15 @@ static gl_status ensure_green(gl_ctx* ctx, GpuState& G, int slot, int gi) {
   // tests/test_gpu_executor.py checks it).  With the SM-pair split every size
   // is exact; with 8-SM groups it is the smallest group count reaching `want`
   // minus one group (sizes never exceed their share).
+  // A partition of 3-4 gpu-lets (gl_create_gpulets, SM-pair split only) gives
+  // slot s the pairs from layout_pair[s] on, in slot order from the front.
   std::vector<CUdevResource> order;
-  if (slot == 1 && G.rem.sm.smCount > 0) order.push_back(G.rem);
-  for (unsigned k = 0; k < G.ngroups; ++k) order.push_back(G.groups[slot == 0 ? k : G.ngroups - 1 - k]);
+  if (G.multi) {
+    for (unsigned k = (unsigned)G.layout_pair[slot]; k < G.ngroups; ++k) order.push_back(G.groups[k]);
+  } else {
+    if (slot == 1 && G.rem.sm.smCount > 0) order.push_back(G.rem);
+    for (unsigned k = 0; k < G.ngroups; ++k) order.push_back(G.groups[slot == 0 ? k : G.ngroups - 1 - k]);
+  }
   for (const CUdevResource& r : order) {
     if (have >= want) break;
     if (!G.fine && have + (int)r.sm.smCount > want) break;
@@ -386,7 +401,7 @@ static gl_status ensure_green(gl_ctx* ctx, GpuState& G, int slot, int gi) {
 
 // Drop every cached green context of a GPU (only while none of its executors run).
 static void drop_green(GpuState& G) {
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < kMaxSlots; ++s)
     for (int gi = 0; gi < 5; ++gi) {
       if (G.gstream[s][gi]) driver().streamDestroy(G.gstream[s][gi]);
       if (G.gctx[s][gi]) driver().greenCtxDestroy(G.gctx[s][gi]);
@@ -619,15 +634,19 @@ gl_status gl_model_cost(gl_ctx* ctx, int32_t id, int32_t batch, double* flops, d
 // executor runs there: device allocations can synchronise the device and
 // would block behind a persistent executor.  The workspace has 25 % headroom
 // for programs tiled for smaller gpu-lets (more split-K partials).
-static gl_status ensure_slot_res(gl_ctx* ctx, GpuState& G, int gpu) {
-  if (G.slot_res[0].ready) return GL_OK;
+static gl_status ensure_slot_res(gl_ctx* ctx, GpuState& G, int gpu, int nslots = 2) {
+  nslots = std::max(2, std::min(nslots, kMaxSlots));
+  bool all = true;
+  for (int s = 0; s < nslots; ++s) all &= G.slot_res[s].ready;
+  if (all) return GL_OK;
   size_t ws = 256;
   for (auto& m : ctx->models)
     if (m && m->gpu == gpu)
       for (int b = 1; b <= 32; ++b) ws = std::max(ws, m->prog[b].ws_bytes);
   ws = (ws + ws / 4 + 255) / 256 * 256;
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < nslots; ++s) {
     SlotRes& R = G.slot_res[s];
+    if (R.ready) continue;
     R.ws_bytes = ws;
     CK(cudaMalloc(&R.ws, ws), "cudaMalloc(workspace)");
     CK(cudaMemset(R.ws, 0, ws), "memset(workspace)");
@@ -697,6 +716,13 @@ static void bind_sized(gl_ctx* ctx, GpuState& G, int gpu, int slot, int nsm) {
 static gl_status create_gpulet(gl_ctx* ctx, int gpu, int pct, bool unconfined, int32_t* gpulet_id, int32_t* sm_count);
 
 gl_status gl_create_gpulet(gl_ctx* ctx, int gpu, int pct, int32_t* gpulet_id, int32_t* sm_count) {
+  if (ctx && gpu >= 0 && gpu < (int)ctx->gpus.size()) {
+    GpuState& G = ctx->gpus[gpu];
+    if (G.multi && !G.any_live()) {   // back to the front / back layout of 1-2 gpu-lets
+      drop_green(G);
+      G.multi = false;
+    }
+  }
   return create_gpulet(ctx, gpu, pct, false, gpulet_id, sm_count);
 }
 
@@ -707,13 +733,17 @@ static gl_status create_gpulet(gl_ctx* ctx, int gpu, int pct, bool unconfined, i
   std::lock_guard<std::mutex> lk(ctx->mu);
   GpuState& G = ctx->gpus[gpu];
   int used = 0, nlive = 0;
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < kMaxSlots; ++s)
     if (G.slots[s] >= 0) {
       used += ctx->gpulets[G.slots[s]]->pct;
       ++nlive;
     }
-  if (nlive >= 2 || used + pct > 100) return fail(GL_E_PARTITION, "gl_create_gpulet: gpu-let sizes on a GPU must sum to <= 100, at most 2");
-  const int slot = G.slots[0] < 0 ? 0 : 1;
+  const int nmax = G.multi ? kMaxSlots : 2;
+  if (nlive >= nmax || used + pct > 100)
+    return fail(GL_E_PARTITION, "gl_create_gpulet: gpu-let sizes on a GPU must sum to <= 100, at most 2 "
+                                "(4 in one gl_create_gpulets partition)");
+  int slot = 0;
+  while (G.slots[slot] >= 0) ++slot;
   CK(cudaSetDevice(G.dev), "cudaSetDevice");
   dbg_log("create_gpulet: begin");
   auto g = std::make_unique<Gpulet>();
@@ -753,7 +783,7 @@ static gl_status create_gpulet(gl_ctx* ctx, int gpu, int pct, bool unconfined, i
     g->nsm = G.gnsm[slot][gi];
   }
   {
-    gl_status rc = ensure_slot_res(ctx, G, gpu);
+    gl_status rc = ensure_slot_res(ctx, G, gpu, slot + 1);
     if (rc) return rc;
   }
   dbg_log("create_gpulet: slot resources ready");
@@ -1155,7 +1185,7 @@ gl_status gl_bw_probe(gl_ctx* ctx, int gpu, int sm_pct, int64_t bytes, int32_t r
     return fail(GL_E_ARG, "gl_bw_probe: bad arguments");
   if (sm_pct != 100 && grid_index(sm_pct) < 0) return fail(GL_E_GRID, "gl_bw_probe: sm_pct off the grid");
   GpuState& G = ctx->gpus[gpu];
-  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_bw_probe: the GPU has live gpu-lets");
+  if (G.any_live()) return fail(GL_E_STATE, "gl_bw_probe: the GPU has live gpu-lets");
   CK(cudaSetDevice(G.dev), "cudaSetDevice");
   if (!G.green_ready) {
     gl_status rc = prepare_green(ctx, G);
@@ -1338,10 +1368,10 @@ extern "C" gl_status gl_program_info(gl_ctx* ctx, int32_t mid, int32_t batch, in
 // block behind a running persistent kernel).  The GPU must have no live gpu-let.
 extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const int32_t* pcts, int32_t* ids,
                                        int32_t* sm_counts) {
-  if (!ctx || !pcts || !ids || n < 1 || n > 2 || gpu < 0 || gpu >= (int)ctx->gpus.size())
+  if (!ctx || !pcts || !ids || n < 1 || n > kMaxSlots || gpu < 0 || gpu >= (int)ctx->gpus.size())
     return fail(GL_E_ARG, "gl_create_gpulets: bad arguments");
   GpuState& G = ctx->gpus[gpu];
-  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_create_gpulets: GPU has live gpu-lets");
+  if (G.any_live()) return fail(GL_E_STATE, "gl_create_gpulets: GPU has live gpu-lets");
   int sum = 0;
   for (int i = 0; i < n; ++i) {
     if (sm_for_pct(pcts[i]) < 0) return fail(GL_E_GRID, "gl_create_gpulets: sm_pct not in the grid");
@@ -1354,6 +1384,19 @@ extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const in
     if (rc) return rc;
   }
   drop_green(G);
+  // 3-4 gpu-lets: contiguous SM-pair ranges from the front, in slot order
+  G.multi = n > 2;
+  if (G.multi) {
+    if (!G.fine) return fail(GL_E_PARTITION, "gl_create_gpulets: 3-4 gpu-lets need the SM-pair split");
+    int pair = 0;
+    for (int i = 0; i < n; ++i) {
+      if (pcts[i] == 100) return fail(GL_E_PARTITION, "gl_create_gpulets: a 100 % gpu-let has no sibling");
+      G.layout_pair[i] = pair;
+      pair += sm_for_pct(pcts[i], G.nsm) / 2;
+    }
+    if (2 * pair > G.nsm)   // e.g. 20+20+20+40 %: exact shares 30+30+30+60 = 150 > 148 SMs
+      return fail(GL_E_PARTITION, "gl_create_gpulets: the exact shares need " + std::to_string(2 * pair) + " SMs");
+  }
   for (int i = 0; i < n; ++i)
     if (pcts[i] < 100) {
       gl_status rc = ensure_green(ctx, G, i, grid_index(pcts[i]));
@@ -1362,7 +1405,7 @@ extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const in
   // slot resources and the programs tiled for these gpu-let sizes, before any
   // executor of this GPU runs (gpu-let i takes slot i)
   {
-    gl_status rc = ensure_slot_res(ctx, G, gpu);
+    gl_status rc = ensure_slot_res(ctx, G, gpu, n);
     if (rc) return rc;
   }
   for (int i = 0; i < n; ++i)
@@ -1370,7 +1413,9 @@ extern "C" gl_status gl_create_gpulets(gl_ctx* ctx, int gpu, int32_t n, const in
   CK(cudaDeviceSynchronize(), "sized programs");
   for (int i = 0; i < n; ++i) {
     int32_t sm = 0;
-    gl_status rc = gl_create_gpulet(ctx, gpu, pcts[i], &ids[i], &sm);
+    // the internal path: the partition's green contexts were created above and
+    // must survive (the public call resets a 3-4 gpu-let layout on an empty GPU)
+    gl_status rc = create_gpulet(ctx, gpu, pcts[i], false, &ids[i], &sm);
     if (rc) return rc;
     if (sm_counts) sm_counts[i] = sm;
   }
@@ -1382,7 +1427,11 @@ extern "C" gl_status gl_create_gpulets_unconfined(gl_ctx* ctx, int gpu, int32_t 
   if (!ctx || !pcts || !ids || n < 1 || n > 2 || gpu < 0 || gpu >= (int)ctx->gpus.size())
     return fail(GL_E_ARG, "gl_create_gpulets_unconfined: bad arguments");
   GpuState& G = ctx->gpus[gpu];
-  if (G.slots[0] >= 0 || G.slots[1] >= 0) return fail(GL_E_STATE, "gl_create_gpulets_unconfined: GPU has live gpu-lets");
+  if (G.any_live()) return fail(GL_E_STATE, "gl_create_gpulets_unconfined: GPU has live gpu-lets");
+  if (G.multi) {   // forget a 3-4 gpu-let layout's green contexts
+    drop_green(G);
+    G.multi = false;
+  }
   int sum = 0;
   for (int i = 0; i < n; ++i) {
     if (sm_for_pct(pcts[i]) < 0 || pcts[i] == 100)

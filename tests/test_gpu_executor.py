@@ -118,3 +118,43 @@ def test_unconfined_pair_serves_and_places_one_cta_per_sm(c):
     finally:
         c.destroy_gpulet(a)
         c.destroy_gpulet(b)
+
+
+@pytest.mark.parametrize("pcts", [[20, 20, 20], [20, 20, 20, 20], [20, 40, 20]])
+def test_three_and_four_gpulets_per_gpu(c, pcts):
+    """F4's "more than 2 gpu-lets per GPU": 3-4 green-context gpu-lets at their exact
+    shares on disjoint SM sets, each serving LeNet-5 batches that match the oracle;
+    a partition whose exact shares exceed 148 SMs is refused."""
+    import torch
+    from oracle import models as omodels
+    from paper_2109_01611_b200 import gpulet
+    share = {20: 30, 40: 60}
+    x = synthgen.model_input("lenet5", 8)
+    xd = to_dev_bf16(x)
+    ys = [torch.empty(c.model_io(c.mid, 8)[1] // 4, device="cuda") for _ in pcts]
+    torch.cuda.synchronize()
+    made = c.create_gpulets(0, pcts)
+    try:
+        assert [n for _g, n in made] == [share[p] for p in pcts]
+        seen = set()
+        for gid, n in made:
+            sm = set(c.gpulet_smids(gid))
+            assert len(sm) == n and not (sm & seen)
+            seen |= sm
+        ref = omodels.forward("lenet5", synthgen.weights("lenet5"), x)["logits"]
+        tickets = [c.submit_batch(gid, c.mid, xd, y, 8, 10.0) for (gid, _n), y in zip(made, ys)]
+        for t, y in zip(tickets, ys):
+            c.wait(t)
+            got = y.cpu().numpy().astype(np.float64).reshape(ref.shape)
+            assert np.abs(got - ref).max() <= 2e-2 * np.abs(ref).max()
+    finally:
+        for gid, _n in made:
+            c.destroy_gpulet(gid)
+    with pytest.raises(gpulet.GpuletError):
+        c.create_gpulets(0, [20, 20, 20, 40])
+    (a, na), (b, nb) = c.create_gpulets(0, [50, 50])   # back to the two-slot layout
+    try:
+        assert (na, nb) == (74, 74) and not set(c.gpulet_smids(a)) & set(c.gpulet_smids(b))
+    finally:
+        c.destroy_gpulet(a)
+        c.destroy_gpulet(b)
