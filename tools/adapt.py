@@ -71,7 +71,9 @@ def main():
     ap.add_argument("--period", type=float, default=0.5)
     ap.add_argument("--alpha", type=float, default=0.7, help="EWMA weight of the latest period")
     ap.add_argument("--headroom", type=float, default=1.15)
-    ap.add_argument("--peak-frac", type=float, default=0.6, help="peak rate as a fraction of the max schedulable")
+    ap.add_argument("--peak-frac", type=float, default=1.0,
+                    help="the trace's peak rate as a fraction of the measured maximum served rate (<= 1 %% violations "
+                         "at the scheduler's plan, bench.py's search on this box)")
     ap.add_argument("--json", default="")
     a = ap.parse_args()
     import bench
@@ -82,7 +84,12 @@ def main():
     srv = bench.Server(ctx, 0, False)
     slo = srv.slo
     xs = srv.max_sched_x(a.scenario, a.mode, 1)
-    peak = srv.scenario_rates(a.scenario, xs * a.peak_frac)
+    # the box's maximum served multiplier (median of 3 probe windows <= 1 %, as bench.py searches):
+    # a trace peaking above what this box serves would measure overload, not adaptation
+    probe_args = argparse.Namespace(probes=6, probe_window=0.5)
+    x_served, _probes = bench.search(srv, None, 0, 1, a.scenario, a.mode, probe_args, xs, e2e=False, reps=3, win=0.5)
+    x_served = x_served or xs * 0.1
+    peak = srv.scenario_rates(a.scenario, x_served * a.peak_frac)
     t_us, m_idx = trace(peak, a.secs, 42)
     nper = int(round(a.secs / a.period))
     M = len(common.MODELS)
@@ -164,7 +171,8 @@ def main():
                 "periods": periods}
 
     out = {"scenario": a.scenario, "mode": a.mode, "secs": a.secs, "period_s": a.period, "alpha": a.alpha,
-           "headroom": a.headroom, "peak_req_s": peak, "x_sched_max": round(xs, 4), "slo_us": slo,
+           "headroom": a.headroom, "peak_req_s": peak, "x_sched_max": round(xs, 4), "x_served_max": round(x_served, 4),
+           "peak_frac_of_served": a.peak_frac, "slo_us": slo,
            "paper": {"viol_frac": 0.0014, "period_s": 20, "reorg_s": "10-15", "cite": "P:672-676, P:889"},
            "results": [run(p) for p in ("adaptive", "static-peak", "static-start")]}
     for r in out["results"]:
