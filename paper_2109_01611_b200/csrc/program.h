@@ -185,8 +185,10 @@ struct ExecParams {
   uint64_t* tl;                 //   k = 0 MMA start (accumulator acquired), 1 MMA last commit, 2 epilogue start, 3 epilogue end
 };
 
-// TMA-producer warps of a TMA-only GEMM step (warps 9 .. 8 + kTmaWarps): one thread
-// issues about one cp.async.bulk.tensor per ~270 ns (measured, tools/tma_micro.cu),
+// TMA-producer warps of a TMA-only GEMM step (warps 9 .. 8 + kTmaWarps): a thread
+// that waits for a ring stage before each load sustains about one
+// cp.async.bulk.tensor per ~270 ns (measured, tools/tma_micro.cu; back-to-back
+// issues cost ~70 cycles each, the stage wait is the cost: tools/tma_issue_micro.cu),
 // so a single producer caps a step at ~0.5 us per 64-wide K block (A + B loads);
 // the producer warps take alternate K blocks.
 #ifndef GL_TMA_WARPS

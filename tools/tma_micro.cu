@@ -17,8 +17,26 @@
 
 #include "ptx.cuh"
 
+// Non-suspending spin on an mbarrier phase (mbarrier.test_wait), to compare with
+// mbar_wait's try_wait loop (which may suspend the thread until a time limit).
+__device__ __forceinline__ void spin_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void wait_any(uint64_t* bar, uint32_t parity, int spin) {
+  if (spin) spin_wait(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
 __global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUtensorMap map, int rows, int depth,
-                                                    int iters, int row_span, uint64_t* out_ns) {
+                                                    int iters, int row_span, int spin, uint64_t* out_ns) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(base + 196608);
@@ -36,7 +54,7 @@ __global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUte
   if (threadIdx.x == 0) {          // producer
     for (int i = 0; i < iters; ++i) {
       const int s = i % depth;
-      mbar_wait(&empty[s], ((i / depth) & 1) ^ 1);
+      wait_any(&empty[s], ((i / depth) & 1) ^ 1, spin);
       mbar_arrive_expect_tx(&full[s], stage_bytes);
       const int row = (blockIdx.x * iters + i) * rows % row_span;
       tma_load_2d(smem_u32(base + s * stage_bytes), &map, &full[s], (i & 7) * 64, row);
@@ -44,7 +62,7 @@ __global__ void __launch_bounds__(64, 1) tma_stream(const __grid_constant__ CUte
   } else if (threadIdx.x == 32) {  // consumer
     for (int i = 0; i < iters; ++i) {
       const int s = i % depth;
-      mbar_wait(&full[s], (i / depth) & 1);
+      wait_any(&full[s], (i / depth) & 1, spin);
       mbar_arrive(&empty[s]);
     }
   }
@@ -90,7 +108,7 @@ int main() {
   uint64_t* d_ns = nullptr;
   cudaMalloc(&d_ns, 148 * sizeof(uint64_t));
   cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608 + 2048);
-  printf("rows,stage_kb,depth,grid,span,ns_per_stage_per_cta,agg_gbs\n");
+  printf("rows,stage_kb,depth,grid,span,spin,ns_per_stage_per_cta,agg_gbs\n");
   for (int rows : {64, 128, 256}) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)total_rows};
@@ -105,11 +123,12 @@ int main() {
     }
     for (int span : {4096, 1 << 17}) {   // 4 MiB window (L2-resident) or the whole 128 MiB (HBM)
       for (int grid : {1, 148}) {
-        for (int depth : {1, 2, 4, 6, 8}) {
+        for (int depth : {1, 2, 4, 6, 8})
+        for (int spin : {0, 1}) {
           if (depth * rows * 128 > 196608) continue;
           const int iters = 2048;
           for (int w = 0; w < 2; ++w)
-            tma_stream<<<grid, 64, 196608 + 2048>>>(map, rows, depth, iters, span, d_ns);
+            tma_stream<<<grid, 64, 196608 + 2048>>>(map, rows, depth, iters, span, spin, d_ns);
           cudaDeviceSynchronize();
           std::vector<uint64_t> ns(grid);
           cudaMemcpy(ns.data(), d_ns, grid * sizeof(uint64_t), cudaMemcpyDeviceToHost);
@@ -118,7 +137,7 @@ int main() {
           for (auto v : ns) mx = v > mx ? v : mx, sum += (double)v;
           const double per = sum / grid / iters;
           const double gbs = (double)grid * iters * rows * 128 / (double)mx;
-          printf("%d,%d,%d,%d,%d,%.1f,%.1f\n", rows, rows * 128 / 1024, depth, grid, span, per, gbs);
+          printf("%d,%d,%d,%d,%d,%d,%.1f,%.1f\n", rows, rows * 128 / 1024, depth, grid, span, spin, per, gbs);
         }
       }
     }

@@ -15,7 +15,7 @@
 
 #include "ptx.cuh"
 
-__global__ void __launch_bounds__(256, 1) umma_loop(int n, int kb, int lag, int nw, uint64_t* out_ns) {
+__global__ void __launch_bounds__(256, 1) umma_loop(int n, int kb, int lag, int nw, int alt, uint64_t* out_ns) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(base + 4 * 49152);   // [4 warps][8]
@@ -32,27 +32,36 @@ __global__ void __launch_bounds__(256, 1) umma_loop(int n, int kb, int lag, int 
   tc_fence_after();
   fence_proxy_async_smem();
   uint64_t t0 = globaltimer();
+  const long long c0 = clock64();
   if (warp < nw) {   // warp w issues into its own accumulator (512 / nw columns apart)
     const uint32_t idesc = umma_idesc_bf16(128, n);
-    const uint32_t d = *tbase + (uint32_t)warp * (512 / nw);
+    const uint32_t d = *tbase + (uint32_t)warp * (512 / nw);  // alt accumulators of n columns inside
     uint64_t* bars_w = bars + warp * 8;
+    // lag 0: no per-K-block commit / wait at all (one commit at the end): the
+    // tensor pipe's own rate for back-to-back tcgen05.mma from one thread
+    const int L = lag > 0 ? lag : 1;
     for (int k = 0; k < kb; ++k) {
-      const int s = k % lag;
-      if (k >= lag) mbar_wait(&bars_w[s], ((k / lag) - 1) & 1);
+      const int s = k % L;
+      if (lag > 0 && k >= lag) mbar_wait(&bars_w[s], ((k / lag) - 1) & 1);
       if (elect_one()) {
         const uint32_t a0 = smem_u32(base + s * 49152), b0 = a0 + 16384;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          umma_bf16(d, umma_sdesc_sw128(a0 + 32 * j), umma_sdesc_sw128(b0 + 32 * j), idesc, k > 0 || j > 0 ? 1u : 0u);
-        umma_commit(&bars_w[s]);
+          umma_bf16(d + (uint32_t)((j % alt) * n), umma_sdesc_sw128(a0 + 32 * j), umma_sdesc_sw128(b0 + 32 * j), idesc,
+                    k > 0 || j >= alt ? 1u : 0u);
+        if (lag > 0 || k == kb - 1) umma_commit(&bars_w[s]);
       }
       __syncwarp();
     }
-    for (int k = kb - lag; k < kb; ++k)
+    if (lag == 0) mbar_wait(&bars_w[0], 0);
+    for (int k = kb - lag; lag > 0 && k < kb; ++k)
       if (k >= 0) mbar_wait(&bars_w[k % lag], (k / lag) & 1);
   }
   __syncthreads();
-  if (threadIdx.x == 0) out_ns[blockIdx.x] = globaltimer() - t0;
+  if (threadIdx.x == 0) {
+    out_ns[blockIdx.x] = globaltimer() - t0;
+    out_ns[gridDim.x + blockIdx.x] = (uint64_t)(clock64() - c0);
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 7) tmem_dealloc(*tbase, 512);
@@ -60,29 +69,30 @@ __global__ void __launch_bounds__(256, 1) umma_loop(int n, int kb, int lag, int 
 
 int main() {
   uint64_t* d_ns = nullptr;
-  cudaMalloc(&d_ns, 148 * sizeof(uint64_t));
+  cudaMalloc(&d_ns, 2 * 148 * sizeof(uint64_t));
   cudaFuncSetAttribute(umma_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  printf("n,lag,grid,issuing_warps,ns_per_kblock_per_warp,cycles_per_umma_per_warp,tensor_frac_sm\n");
+  printf("n,lag,grid,issuing_warps,alt_accumulators,ns_per_kblock_per_warp,cycles_per_umma_per_warp,tensor_frac_sm\n");
   for (int n : {64, 128, 256})
-    for (int lag : {2, 4})
+    for (int lag : {0, 2, 4})
       for (int nw : {1, 2, 4})
+      for (int alt : {1, 2, 4})
       for (int grid : {1, 148}) {
-        if (n * nw > 512 || (n == 256 && nw > 2)) continue;
+        if (n * nw * alt > 512) continue;
         const int kb = 4096;
-        for (int w = 0; w < 2; ++w) umma_loop<<<grid, 256, 200 * 1024>>>(n, kb, lag, nw, d_ns);
+        for (int w = 0; w < 2; ++w) umma_loop<<<grid, 256, 200 * 1024>>>(n, kb, lag, nw, alt, d_ns);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
           printf("cuda error %s\n", cudaGetErrorString(e));
           return 1;
         }
-        std::vector<uint64_t> ns(grid);
-        cudaMemcpy(ns.data(), d_ns, grid * sizeof(uint64_t), cudaMemcpyDeviceToHost);
-        double sum = 0;
-        for (auto v : ns) sum += (double)v;
+        std::vector<uint64_t> ns(2 * grid);
+        cudaMemcpy(ns.data(), d_ns, 2 * grid * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+        double sum = 0, csum = 0;
+        for (int i = 0; i < grid; ++i) sum += (double)ns[i], csum += (double)ns[grid + i];
         const double per = sum / grid / kb;
-        const double cyc = per * 1.965 / 4;                     // per UMMA
+        const double cyc = csum / grid / kb / 4;                 // SM clock cycles per UMMA (clock64)
         const double floor_cyc = 128.0 * n / 256;               // tcgen05 floor, M = 128, cta_group::1
-        printf("%d,%d,%d,%d,%.1f,%.1f,%.3f\n", n, lag, grid, nw, per, cyc, nw * floor_cyc / cyc);
+        printf("%d,%d,%d,%d,%d,%.1f,%.1f,%.3f\n", n, lag, grid, nw, alt, per, cyc, nw * floor_cyc / cyc);
       }
   return 0;
 }
