@@ -515,7 +515,7 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
                     (e.ldc % 8) == 0 && (e.col_off % 8) == 0 && c1 > c0;
   const int nfull = fast ? min(8, (c1 - c0) / 32) : 0;
   const __nv_bfloat16* bias = (const __nv_bfloat16*)res(e.bias, X);
-  const bool rs = e.res.kind != BUF_NONE;
+  const bool rs = e.res.kind != BUF_NONE && !(S.flags & 128);   // flag 128: tuning, skip the residual (wrong results)
   const int row0 = mb * 128 + q * 32, n00 = nb * g.BN + c0;
   if (nfull > 0) {
     // the tile's bias columns, fp32 in smem; reloaded only when (op, n block) changes
