@@ -5,9 +5,15 @@ their input sizes only, Table `tab:ml-models`; BERT-base is a
 north_star addition, D1).  Quantisation points: C1.4 — every layer consumes
 bf16 values, accumulates exactly (fp64 here), and its epilogue applies
 +bias -> (+bf16 residual) -> activation -> round-to-bf16.  Final logits and the
-SSD heads stay fp32.  Parity status: the layer maths is pinned (test_oracle_nn);
-the topologies themselves are "parity unpinned" readings (C6 #1-#4) except for
-the closed-form MAC/parameter totals pinned in test_oracle_models.
+SSD heads stay fp32.  Parity status: pinned.  The layer maths against torch-CPU
+and brute force (test_oracle_nn); the closed-form MAC / parameter totals
+(test_oracle_models); and each whole model, with the bf16 rounding switched off,
+against an independent torch-CPU fp64 reference in its standard layout to 1e-9
+(test_oracle_models_torch: torchvision resnet50 / vgg16 / GoogLeNet blocks,
+nn.TransformerEncoderLayer for BERT, torch.nn.functional LeNet-5 and SSD), which
+fixes the wiring the totals cannot see (residual order, flatten order, branch
+order, QKV split, post-LN placement, head order).  The topologies remain
+readings of the paper (C6 #1-#4: it names the models and input sizes only).
 """
 import numpy as np
 
