@@ -1688,7 +1688,14 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
 extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  Smem S;
+  // The CTA-uniform executor state (shared-memory layout pointers, the work
+  // item's buffer bases) lives in shared memory: the interpreter's layer
+  // functions take it by reference, and as stack (local-memory) objects every
+  // step re-read it through L1 misses (80 % of local loads miss, ncu r6u).
+  __shared__ Smem S_sh;
+  __shared__ Ctx X_sh;
+  Smem& S = S_sh;
+  if (threadIdx.x == 0) {
   for (int s = 0; s < kStages; ++s) {
     S.a[s] = base + s * kStageBytesA;
     S.b[s] = base + kStages * kStageBytesA + s * kStageBytesB;
@@ -1713,6 +1720,8 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   S.opc = (GemmArgs*)(base + kRingBytes + 1024 + kEpiStageBytes);
   S.opn = (int*)(S.opc + kOpCache);
   S.ebias = (float*)(base + kRingBytes + 1024 + kEpiStageBytes + kOpCacheBytes);
+  }
+  __syncthreads();
 
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -1785,8 +1794,9 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
       dst[0] = q0, dst[1] = q1, dst[2] = q2, dst[3] = q3;
     }
     const uint64_t t_start = globaltimer();
-    Ctx X{(const char*)w.in, (char*)w.out, p.ws, (uint32_t*)(uintptr_t)w.prog[0].cnt_base};
-    run_program(w, X, S, P, p.st, epoch, p.trace, p.trace_cap);
+    if (threadIdx.x == 0) X_sh = Ctx{(const char*)w.in, (char*)w.out, p.ws, (uint32_t*)(uintptr_t)w.prog[0].cnt_base};
+    __syncthreads();
+    run_program(w, X_sh, S, P, p.st, epoch, p.trace, p.trace_cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       // the record as four 16-B stores to the host-mapped ring, published by a
       // release store of comp_tail (cumulative: it also orders the batch's
