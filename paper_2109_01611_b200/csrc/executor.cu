@@ -116,6 +116,7 @@ __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
     // spread over 8 lines, CTA b adding to line b % 8 and polling the sum, were
     // measured 1 us per barrier slower: profiles/ab_r4j_barrier_spread_lines.log)
     const unsigned long long target = (unsigned long long)(epoch + 1) * gridDim.x;
+    epoch += 1;
     red_release_gpu_add_u64((unsigned long long*)&st->barrier, 1ull);
     uint32_t spins = 0, ns = 32;
     uint64_t t0 = 0;
@@ -129,7 +130,6 @@ __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
       }
     }
   }
-  ++epoch;
   __syncthreads();
   // The next step's TMA (async proxy) reads what other CTAs stored (generic
   // proxy): the thread that issues a step's TMA loads executes
@@ -1749,7 +1749,11 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
   }
 
   Pipe P;
-  uint64_t epoch = 0;
+  // barrier epochs passed: read and advanced by thread 0 only (gridsync), kept in
+  // shared memory so the barrier's target is not an L1-missing stack load
+  __shared__ uint64_t epoch_sh;
+  if (threadIdx.x == 0) epoch_sh = 0;
+  uint64_t& epoch = epoch_sh;
   int done = 0;
   // completions published so far (CTA 0 thread 0 is the only writer of the ring's completion side)
   uint64_t completions = (blockIdx.x == 0 && threadIdx.x == 0) ? p.ring->heartbeat : 0;
