@@ -867,10 +867,14 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
   // on this CTA's tile and k-block counts, which the MMA warp counted as it
   // walked them; gemm_finish() applies them after the gpu-let barrier, whose
   // __syncthreads makes the counts visible (no extra CTA barrier here).
-  P.bits = bits0;
-  P.acc = acc0;
-  P.fix = 1;
-  Pio = P;
+  // Pio is the CTA's one shared copy: the step leaves bits / acc as it found them
+  // (bits0 / acc0); thread 0 records the step's ring depth for gemm_finish.
+  (void)bits0;
+  (void)acc0;
+  if (threadIdx.x == 0) {
+    Pio.nst = P.nst;
+    Pio.fix = 1;
+  }
 }
 
 __device__ __forceinline__ void gemm_finish(Pipe& P, const Smem& S) {
@@ -1466,9 +1470,10 @@ __device__ __noinline__ void attention_tc(const OpDesc* op, const Ctx& X, const 
   const uint32_t tbase = *S.tmem_base;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) tma_role_fence();
+  uint32_t aph = P.att_phase;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int seq = u / H, h = u - seq * H, row0 = seq * 128;
-    const uint32_t ph = P.att_phase & 1;
+    const uint32_t ph = aph & 1;
     if (t == 0) {
       mbar_arrive_expect_tx(&S.att[0], 3 * 16384);
       tma_load_2d(smem_u32(sQ), &op->tmap_a, &S.att[0], h * 64, row0);
@@ -1544,8 +1549,9 @@ __device__ __noinline__ void attention_tc(const OpDesc* op, const Ctx& X, const 
     }
     tc_fence_before();
     __syncthreads();
-    ++P.att_phase;
+    ++aph;
   }
+  if (threadIdx.x == 0) P.att_phase = aph;   // the shared pipe state (read again after a barrier)
 }
 
 // ------------------------------------------------------------------ row softmax (K11)
@@ -1659,7 +1665,8 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     if (threadIdx.x == 0 && w.prog[i].type != OP_LENET) *S.wtag = 0;   // smem scratch / ring reused
     const int n_next = min(kPfOps, w.n_ops - j - 1);
     prefetch_desc(w.prog + j + 1, n_next);
-    if (w.prog[i].type == OP_GEMM) {
+    const bool step_gemm = w.prog[i].type == OP_GEMM;
+    if (step_gemm) {
       gemm_step(w.prog + i, j - i + 1, X, S, P, n_next);
     } else {
       if (threadIdx.x >= kThreads - 32) prefetch_ops(w.prog + j + 1, n_next, threadIdx.x - (kThreads - 32));
@@ -1671,7 +1678,10 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
       __syncthreads();   // the next GEMM step waits per M block on completion counters
     else
       gridsync(st, epoch, false);
-    if (P.fix) gemm_finish(P, S);
+    if (step_gemm) {   // thread 0 applies the step's counts to the shared pipe state
+      if (threadIdx.x == 0) gemm_finish(P, S);
+      __syncthreads();
+    }
     if (threadIdx.x == 0) dbg_mark(S, 7);
     ++step;
     if (tr && step < trace_cap) trace[step] = globaltimer();
@@ -1748,7 +1758,12 @@ extern "C" __global__ void __launch_bounds__(kThreads, 1) gl_executor(ExecParams
     __threadfence_system();
   }
 
-  Pipe P;
+  // The pipe state (ring parity bits, accumulator uses, attention phase) is
+  // CTA-uniform between steps: one shared copy, advanced by thread 0
+  // (gemm_finish, attention_tc); each role copies it into registers.
+  __shared__ __align__(16) uint8_t pipe_raw[sizeof(Pipe)];
+  Pipe& P = *reinterpret_cast<Pipe*>(pipe_raw);
+  if (threadIdx.x == 0) P = Pipe{};
   // barrier epochs passed: read and advanced by thread 0 only (gridsync), kept in
   // shared memory so the barrier's target is not an L1-missing stack load
   __shared__ uint64_t epoch_sh;
