@@ -107,17 +107,23 @@ __device__ __forceinline__ void advance(Pipe& p) {
 }
 
 // ------------------------------------------------------------------ gpu-let barrier
-__device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
+// Split-phase gpu-let barrier: arrive (this CTA's step is done: __syncthreads,
+// then thread 0's release-add, which orders the CTA's prior writes, made
+// visible CTA-wide by the __syncthreads) and wait (thread 0 acquire-polls: tight
+// for the first ~1 us, then with a short back-off for idle executors waiting for
+// work; then __syncthreads).  Between the two a CTA may do work that does not
+// depend on the other CTAs' step (staging the next step's GEMM arguments).
+// (Counters spread over 8 lines, CTA b adding to line b % 8 and polling the sum,
+// were measured 1 us per barrier slower: profiles/ab_r4j_barrier_spread_lines.log)
+__device__ __forceinline__ void gridsync_arrive(ExecState* st) {
   __syncthreads();
+  if (threadIdx.x == 0) red_release_gpu_add_u64((unsigned long long*)&st->barrier, 1ull);
+}
+
+__device__ void gridsync_wait(ExecState* st, uint64_t& epoch, bool may_idle) {
   if (threadIdx.x == 0) {
-    // release-add (orders this CTA's prior writes, made visible CTA-wide by the
-    // __syncthreads above), then acquire-poll: tight for the first ~1 us, then
-    // with a short back-off (idle executors wait here for work).  (Counters
-    // spread over 8 lines, CTA b adding to line b % 8 and polling the sum, were
-    // measured 1 us per barrier slower: profiles/ab_r4j_barrier_spread_lines.log)
     const unsigned long long target = (unsigned long long)(epoch + 1) * gridDim.x;
     epoch += 1;
-    red_release_gpu_add_u64((unsigned long long*)&st->barrier, 1ull);
     uint32_t spins = 0, ns = 32;
     uint64_t t0 = 0;
     while (ld_acquire_gpu_u64((volatile uint64_t*)&st->barrier) < target) {
@@ -135,6 +141,11 @@ __device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
   // proxy): the thread that issues a step's TMA loads executes
   // fence.proxy.async.global itself before its first load (tma_role_fence),
   // so the other threads do not wait on the proxy fence here.
+}
+
+__device__ void gridsync(ExecState* st, uint64_t& epoch, bool may_idle) {
+  gridsync_arrive(st);
+  gridsync_wait(st, epoch, may_idle);
 }
 
 // ------------------------------------------------------------------ epilogue helpers
@@ -591,7 +602,21 @@ __device__ __forceinline__ void epilogue_cols(const GemmArgs& g, const Ctx& X, c
   }
 }
 
-__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& Sio, Pipe& Pio, int n_next) {
+// The step's GEMM arguments (first kOpCache ops) and unit counts into shared
+// memory, once per step, by the whole CTA.
+__device__ __forceinline__ void stage_gemm_args(const OpDesc* ops, int nops, const Smem& S) {
+  constexpr int W = (int)sizeof(GemmArgs) / 4;
+  const int nc = min(nops, kOpCache);
+  for (int i = threadIdx.x; i < nc * W; i += blockDim.x)
+    ((uint32_t*)S.opc)[i] = ((const uint32_t*)&ops[i / W].g)[i % W];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) S.opn[i] = ops[i].n_units;
+  __syncthreads();
+}
+
+// staged: the arguments were staged between the previous step's barrier arrive
+// and wait (run_program).
+__device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem& Sio, Pipe& Pio, int n_next,
+                          bool staged) {
   // register copies: the k loops must not reload ring state through memory
   // after every asm statement (they all clobber "memory")
   const Smem S = Sio;
@@ -599,14 +624,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
 #ifdef GL_DBG_START
   if (threadIdx.x == 0) dbg_mark(S, 2);   // instrumented build: step entry
 #endif
-  {
-    constexpr int W = (int)sizeof(GemmArgs) / 4;
-    const int nc = min(nops, kOpCache);
-    for (int i = threadIdx.x; i < nc * W; i += blockDim.x)
-      ((uint32_t*)S.opc)[i] = ((const uint32_t*)&ops[i / W].g)[i % W];
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) S.opn[i] = ops[i].n_units;
-    __syncthreads();
-  }
+  if (!staged) stage_gemm_args(ops, nops, S);
 #ifdef GL_DBG_START
   if (threadIdx.x == 0) dbg_mark(S, 4);   // instrumented build: step args staged
 #endif
@@ -1652,6 +1670,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
   const bool tr = trace && blockIdx.x == 0 && threadIdx.x == 0;
   if (tr && trace_cap > 0) trace[0] = globaltimer();
   S.dbg = (trace && trace_cap >= 1024 + 8 * 1000) ? trace + 1024 : nullptr;
+  bool staged = false;   // this step's GEMM arguments were staged during the last barrier
   while (i < w.n_ops) {
     // the step's extent: bound programs carry it on the step's first op (one
     // load instead of one dependent load per op of the step)
@@ -1667,17 +1686,32 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     prefetch_desc(w.prog + j + 1, n_next);
     const bool step_gemm = w.prog[i].type == OP_GEMM;
     if (step_gemm) {
-      gemm_step(w.prog + i, j - i + 1, X, S, P, n_next);
+      gemm_step(w.prog + i, j - i + 1, X, S, P, n_next, staged);
     } else {
       if (threadIdx.x >= kThreads - 32) prefetch_ops(w.prog + j + 1, n_next, threadIdx.x - (kThreads - 32));
       for (int k = i; k <= j; ++k) run_misc(w.prog + k, X, S, P);
     }
     fence_proxy_async_smem();
     if (threadIdx.x == 0) dbg_mark(S, 6);
-    if (w.prog[j].local_next)
+    staged = false;
+    if (w.prog[j].local_next) {
       __syncthreads();   // the next GEMM step waits per M block on completion counters
-    else
-      gridsync(st, epoch, false);
+    } else {
+      gridsync_arrive(st);
+      // while the other CTAs finish: the next GEMM step's arguments into shared
+      // memory (read-only program data; gemm_finish's counts sit past kOpCache)
+      if (j + 1 < w.n_ops && w.prog[j + 1].type == OP_GEMM) {
+        const int i2 = j + 1, sn2 = w.prog[i2].step_nops;
+        int j2 = i2;
+        if (sn2 > 0)
+          j2 = min(w.n_ops - 1, i2 + sn2 - 1);
+        else
+          while (j2 < w.n_ops - 1 && !w.prog[j2].step_end) ++j2;
+        stage_gemm_args(w.prog + i2, j2 - i2 + 1, S);
+        staged = true;
+      }
+      gridsync_wait(st, epoch, false);
+    }
     if (step_gemm) {   // thread 0 applies the step's counts to the shared pipe state
       if (threadIdx.x == 0) gemm_finish(P, S);
       __syncthreads();
