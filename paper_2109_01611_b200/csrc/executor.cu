@@ -1671,20 +1671,26 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
   if (tr && trace_cap > 0) trace[0] = globaltimer();
   S.dbg = (trace && trace_cap >= 1024 + 8 * 1000) ? trace + 1024 : nullptr;
   bool staged = false;   // this step's GEMM arguments were staged during the last barrier
+  int staged_j = 0;      //   and its last op (the extent was read then)
   while (i < w.n_ops) {
     // the step's extent: bound programs carry it on the step's first op (one
     // load instead of one dependent load per op of the step)
-    const int sn = w.prog[i].step_nops;
     int j = i;
-    if (sn > 0)
-      j = min(w.n_ops - 1, i + sn - 1);
-    else
-      while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
+    if (staged) {
+      j = staged_j;
+    } else {
+      const int sn = w.prog[i].step_nops;
+      if (sn > 0)
+        j = min(w.n_ops - 1, i + sn - 1);
+      else
+        while (j < w.n_ops - 1 && !w.prog[j].step_end) ++j;
+    }
+    const int type = staged ? (int)OP_GEMM : w.prog[i].type;
     S.step = step;
-    if (threadIdx.x == 0 && w.prog[i].type != OP_LENET) *S.wtag = 0;   // smem scratch / ring reused
+    if (threadIdx.x == 0 && type != OP_LENET) *S.wtag = 0;   // smem scratch / ring reused
     const int n_next = min(kPfOps, w.n_ops - j - 1);
     prefetch_desc(w.prog + j + 1, n_next);
-    const bool step_gemm = w.prog[i].type == OP_GEMM;
+    const bool step_gemm = type == OP_GEMM;
     if (step_gemm) {
       gemm_step(w.prog + i, j - i + 1, X, S, P, n_next, staged);
     } else {
@@ -1709,6 +1715,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
           while (j2 < w.n_ops - 1 && !w.prog[j2].step_end) ++j2;
         stage_gemm_args(w.prog + i2, j2 - i2 + 1, S);
         staged = true;
+        staged_j = j2;
       }
       gridsync_wait(st, epoch, false);
     }
