@@ -1700,10 +1700,15 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
     fence_proxy_async_smem();
     if (threadIdx.x == 0) dbg_mark(S, 6);
     staged = false;
+    bool finished = false;   // gemm_finish applied inside the barrier window
     if (w.prog[j].local_next) {
       __syncthreads();   // the next GEMM step waits per M block on completion counters
     } else {
       gridsync_arrive(st);
+      // the step's counts are this CTA's own (the MMA warp wrote them before the
+      // arrive's __syncthreads): thread 0 applies them before waiting
+      if (step_gemm && threadIdx.x == 0) gemm_finish(P, S);
+      finished = step_gemm;
       // while the other CTAs finish: the next GEMM step's arguments into shared
       // memory (read-only program data; gemm_finish's counts sit past kOpCache)
       if (j + 1 < w.n_ops && w.prog[j + 1].type == OP_GEMM) {
@@ -1719,7 +1724,7 @@ __device__ void run_program(const WorkDesc& w, const Ctx& X, Smem& S, Pipe& P, E
       }
       gridsync_wait(st, epoch, false);
     }
-    if (step_gemm) {   // thread 0 applies the step's counts to the shared pipe state
+    if (step_gemm && !finished) {   // thread 0 applies the step's counts to the shared pipe state
       if (threadIdx.x == 0) gemm_finish(P, S);
       __syncthreads();
     }
