@@ -636,7 +636,16 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
     maxbn = max(maxbn, so.g(i).BN);
     gstep |= so.g(i).a_tma == SRC_GATHER || so.g(i).b_tma == SRC_GATHER;
   }
-  const uint32_t sbytes = stage_bytes_for(maxbn);
+  // A stage of a TMA-only step holds kper consecutive K blocks ([A][B] per K block):
+  // one ring wait per kper loads for the producer and per 4·kper MMAs for the
+  // issuer (a wait on an mbarrier an async unit signals costs ~250-300 cycles;
+  // DESIGN §5): the most K blocks (<= kKPair) that leave the ring kKPairMinStages
+  // such stages.
+  const uint32_t sbytes1 = stage_bytes_for(maxbn);
+  int kper = 1;
+  if (!gstep)
+    while (kper < kKPair && kRingBytes / ((kper + 1) * sbytes1) >= (uint32_t)kKPairMinStages) ++kper;
+  const uint32_t sbytes = sbytes1 * (uint32_t)kper;
   P.nst = min((uint32_t)kMaxStages, (uint32_t)kRingBytes / sbytes);
   P.stage = 0;
   const uint32_t ring = smem_u32(S.ring);
@@ -756,7 +765,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       const void* tA = &op->tmap_a;
       const void* tB = &op->tmap_b;
       const bool skip = (S.flags & 8) != 0;
-      for (int kb = kb0; kb < kb1; ++kb, ++kbi) {
+      for (int kb = kb0; kb < kb1; kb += kper, ++kbi) {
         if (kbi % kTmaWarps == pw) {
           mbar_wait(&S.empty[P.stage], par(P) ^ 1);
           uint64_t* fb = &S.full[P.stage];
@@ -764,13 +773,16 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
             if (skip) {
               mbar_arrive_cnt(fb, 129);
             } else {
-              const uint32_t sa = ring + P.stage * sbytes;
-              mbar_arrive_expect_tx(fb, tx);
-              if (a2d)
-                tma_load_2d(sa, tA, fb, kb * 64, arow);
-              else
-                im2col_kblock(q, tA, fb, sa, kb, icw, ich, icn);
-              tma_load_2d(sa + kStageBytesA, tB, fb, kb * 64, brow);
+              const int nk = min(kper, kb1 - kb);
+              uint32_t sa = ring + P.stage * sbytes;
+              mbar_arrive_expect_tx(fb, tx * (uint32_t)nk);
+              for (int j = 0; j < nk; ++j, sa += sbytes1) {
+                if (a2d)
+                  tma_load_2d(sa, tA, fb, (kb + j) * 64, arow);
+                else
+                  im2col_kblock(q, tA, fb, sa, kb + j, icw, ich, icn);
+                tma_load_2d(sa + kStageBytesA, tB, fb, (kb + j) * 64, brow);
+              }
               mbar_arrive_cnt(fb, 128);
             }
           }
@@ -807,16 +819,20 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
 #ifndef GL_DBG_START
       if (tile == (int)blockIdx.x && lane == 0) dbg_mark(S, 2);
 #endif
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; kb += kper) {
         mbar_wait(&S.full[P.stage], par(P));
         if (!(S.flags & 16)) tc_fence_after();
-        const uint32_t a0 = ring + P.stage * sbytes, b0 = a0 + kStageBytesA;
         if (elect_one()) {
           if (do_mma) {
-            umma_bf16(d, ahi | ((a0 & 0x3FFFF) >> 4), bhi | ((b0 & 0x3FFFF) >> 4), idesc, kb > kb0 ? 1u : 0u);
-            umma_bf16(d, ahi | (((a0 + ko1) & 0x3FFFF) >> 4), bhi | (((b0 + 32) & 0x3FFFF) >> 4), idesc, 1u);
-            umma_bf16(d, ahi | (((a0 + ko2) & 0x3FFFF) >> 4), bhi | (((b0 + 64) & 0x3FFFF) >> 4), idesc, 1u);
-            umma_bf16(d, ahi | (((a0 + ko3) & 0x3FFFF) >> 4), bhi | (((b0 + 96) & 0x3FFFF) >> 4), idesc, 1u);
+            const int nk = min(kper, kb1 - kb);
+            uint32_t a0 = ring + P.stage * sbytes;
+            for (int j = 0; j < nk; ++j, a0 += sbytes1) {
+              const uint32_t b0 = a0 + kStageBytesA;
+              umma_bf16(d, ahi | ((a0 & 0x3FFFF) >> 4), bhi | ((b0 & 0x3FFFF) >> 4), idesc, kb + j > kb0 ? 1u : 0u);
+              umma_bf16(d, ahi | (((a0 + ko1) & 0x3FFFF) >> 4), bhi | (((b0 + 32) & 0x3FFFF) >> 4), idesc, 1u);
+              umma_bf16(d, ahi | (((a0 + ko2) & 0x3FFFF) >> 4), bhi | (((b0 + 64) & 0x3FFFF) >> 4), idesc, 1u);
+              umma_bf16(d, ahi | (((a0 + ko3) & 0x3FFFF) >> 4), bhi | (((b0 + 96) & 0x3FFFF) >> 4), idesc, 1u);
+            }
           }
           umma_commit(&S.empty[P.stage]);
         }
@@ -825,7 +841,7 @@ __device__ void gemm_step(const OpDesc* ops, int nops, const Ctx& X, const Smem&
       }
       if (elect_one()) umma_commit(&S.tfull[acc]);
       __syncwarp();
-      nkb_total += kb1 - kb0;
+      nkb_total += (kb1 - kb0 + kper - 1) / kper;   // ring stages consumed
       if (lane == 0) tl_mark(S, ntile, 1);
       ++ntile;
       ++P.acc;

@@ -195,6 +195,15 @@ struct ExecParams {
 #define GL_TMA_WARPS 2
 #endif
 constexpr int kTmaWarps = GL_TMA_WARPS;
+// K blocks per ring stage of a TMA-only GEMM step (executor.cu gemm_step)
+#ifndef GL_KPAIR
+#define GL_KPAIR 2
+#endif
+#ifndef GL_KPAIR_MINST
+#define GL_KPAIR_MINST 3
+#endif
+constexpr int kKPair = GL_KPAIR;
+constexpr int kKPairMinStages = GL_KPAIR_MINST;
 constexpr int kThreads = 288 + 32 * kTmaWarps;   // warps 0-3 gather / epilogue, 4-7 epilogue, 8 MMA, 9.. TMA
 constexpr int kStages = 4;      // fixed stage layout used as scratch by the non-GEMM ops
 constexpr int kStageBytesA = 128 * 128;       // 128 rows x 64 bf16

@@ -3,6 +3,7 @@
 #   bash scripts/ab_round2.sh anatomy      # ResNet-50 b32 per-step anatomy under executor debug flags
 #   bash scripts/ab_round2.sh gemm         # per-op GEMM tile timelines, BN x split-K sweeps
 #   bash scripts/ab_round2.sh micro        # TMA / UMMA issue-rate microbenchmarks
+#   bash scripts/ab_round2.sh kpair        # 1 vs 2 K blocks per ring stage (profiles/ab_r9a_kpair.log)
 # Variant libraries are built from the working tree with compile-time switches
 # (GL_TMA_WARPS, GL_DBG_START) into paper_2109_01611_b200/_ab/ and passed as GL_LIB.
 set -e
@@ -35,6 +36,16 @@ case $WHAT in
       --bn 0,64,128,256 --flags 0,8,4 --json gpurun_out/gemm_micro.json
     python tools/gemm_micro.py --only res_l4_3x3_512,res_l3_3x3_256,res_l2_3x3_128 --bn 64,128,256 \
       --split 1,2,4,8 --json gpurun_out/gemm_split.json ;;
+  kpair)
+    variant kp1 -DGL_KPAIR=1; variant kp2 -DGL_KPAIR=2
+    VARIANTS="kp1=$C/_ab/libkp1.so kp2=$C/_ab/libkp2.so" bash scripts/ab_oneshot.sh kpair \
+      resnet50:1 resnet50:8 resnet50:32 bert_base:8 bert_base:32 vgg16:32 googlenet:32 ssd_mobilenet_v1:8 ;;
+  kpair2)
+    variant kp2m3 -DGL_KPAIR=2; variant kp2m2 -DGL_KPAIR=2 -DGL_KPAIR_MINST=2
+    variant kp4m3 -DGL_KPAIR=4; variant kp4m2 -DGL_KPAIR=4 -DGL_KPAIR_MINST=2
+    VARIANTS="kp2m3=$C/_ab/libkp2m3.so kp2m2=$C/_ab/libkp2m2.so kp4m3=$C/_ab/libkp4m3.so kp4m2=$C/_ab/libkp4m2.so" \
+      bash scripts/ab_oneshot.sh kpair2 \
+      resnet50:1 resnet50:8 resnet50:32 bert_base:8 bert_base:32 vgg16:32 googlenet:32 ssd_mobilenet_v1:8 ;;
   micro)
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I $C/csrc tools/tma_micro.cu -o tools/tma_micro -lcuda
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I $C/csrc tools/umma_micro.cu -o tools/umma_micro
