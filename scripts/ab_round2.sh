@@ -4,6 +4,8 @@
 #   bash scripts/ab_round2.sh gemm         # per-op GEMM tile timelines, BN x split-K sweeps
 #   bash scripts/ab_round2.sh micro        # TMA / UMMA issue-rate microbenchmarks
 #   bash scripts/ab_round2.sh kpair        # 1 vs 2 K blocks per ring stage (profiles/ab_r9a_kpair.log)
+#   bash scripts/ab_round2.sh kpair2       # 2 / 4 K blocks per stage, >= 2 / 3 stages (profiles/ab_r9b_kpair2.log)
+#   bash scripts/ab_round2.sh kpair-tw     # 1 vs 2 TMA-producer warps with paired stages (profiles/ab_r9c_kpair_tw.log)
 # Variant libraries are built from the working tree with compile-time switches
 # (GL_TMA_WARPS, GL_DBG_START) into paper_2109_01611_b200/_ab/ and passed as GL_LIB.
 set -e
@@ -46,6 +48,10 @@ case $WHAT in
     VARIANTS="kp2m3=$C/_ab/libkp2m3.so kp2m2=$C/_ab/libkp2m2.so kp4m3=$C/_ab/libkp4m3.so kp4m2=$C/_ab/libkp4m2.so" \
       bash scripts/ab_oneshot.sh kpair2 \
       resnet50:1 resnet50:8 resnet50:32 bert_base:8 bert_base:32 vgg16:32 googlenet:32 ssd_mobilenet_v1:8 ;;
+  kpair-tw)
+    variant kp2tw1 -DGL_TMA_WARPS=1; variant kp2tw2 -DGL_TMA_WARPS=2
+    VARIANTS="kp2tw1=$C/_ab/libkp2tw1.so kp2tw2=$C/_ab/libkp2tw2.so" bash scripts/ab_oneshot.sh kpairtw \
+      resnet50:1 resnet50:8 resnet50:32 bert_base:8 vgg16:32 googlenet:32 ssd_mobilenet_v1:8 ;;
   micro)
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I $C/csrc tools/tma_micro.cu -o tools/tma_micro -lcuda
     nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I $C/csrc tools/umma_micro.cu -o tools/umma_micro

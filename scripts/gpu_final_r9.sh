@@ -1,9 +1,9 @@
-# Round-2 closing pass on the final kernels (shared-memory executor state): smoke +
+# Round-2 closing pass on the final kernels (two K blocks per ring stage): smoke +
 # its ncu launch list, the GPU parity suite, the p90 latency profile re-measured on
 # these kernels, per-model one-shot traces, extras (floor, K12, cfg1), the per-point
 # profile roofline, ncu DRAM traffic of the ResNet-50 lane's batches, one ncu --set
 # full capture, the bench (full + headline repeat + reference arm), F1 / F3 / F4.
-TAG=${1:-r7}
+TAG=${1:-r9}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_$TAG.txt
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
