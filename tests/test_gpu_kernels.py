@@ -49,6 +49,36 @@ def test_gemm_vs_oracle(ctx, M, N, K, act, in_ws):
     assert np.mean(got == ref) > 0.9
 
 
+# Paired ring stages (executor.cu gemm_step: two K blocks per stage on TMA-only steps
+# while the ring keeps >= 3 stages, i.e. N tiles <= 128): odd K-block counts end in a
+# one-block tail stage; N = 256 tiles keep one block per stage; forced split-K ranges
+# (TUNE_SPLIT) have odd lengths and start at odd block offsets.
+@pytest.mark.parametrize("splitk", [1, 3])
+@pytest.mark.parametrize("M,N,K", [(300, 64, 64), (300, 64, 192), (260, 128, 320), (129, 96, 64 * 9),
+                                   # >= 74 M blocks: the tile rule keeps N = 128 / 256 wide tiles
+                                   (9500, 128, 320), (9500, 128, 448), (9500, 256, 192), (9500, 256, 320)])
+def test_gemm_paired_stages_vs_oracle(ctx, M, N, K, splitk):
+    import torch
+    if splitk > K // 64:
+        pytest.skip("fewer K blocks than splits")
+    r = np.random.default_rng(M * 3 + N + K + splitk)
+    A = _bf16(r, (M, K))
+    W = _bf16(r, (N, K), 1 / np.sqrt(K))
+    b = _bf16(r, (N,), 0.1)
+    out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    from paper_2109_01611_b200 import gpulet
+    gpulet.Context.set_tuning(1, splitk if splitk > 1 else 0)   # TUNE_SPLIT: force the split count
+    try:
+        ctx.test_gemm(0, to_dev_bf16(A), W, b, out, M, N, K, act=1, splitk=1, in_ws=1)
+    finally:
+        gpulet.Context.set_tuning(1, 0)
+    torch.cuda.synchronize()
+    ref = nn.rbf16(nn.relu(nn.linear(bits_to_f64(A), bits_to_f64(W), bits_to_f64(b))))
+    got = bits_to_f64(from_dev_bf16(out))
+    assert rel_err(got, ref) < 1e-2
+    assert np.mean(got == ref) > 0.9
+
+
 @pytest.mark.parametrize("in_ws", [0, 1])
 @pytest.mark.parametrize("M,N,K", [(1, 1000, 2048), (7, 4096, 25088), (32, 1000, 4096), (16, 2, 768), (3, 768, 768)])
 def test_gemm_swap_ab_splitk_vs_oracle(ctx, M, N, K, in_ws):
